@@ -1,0 +1,131 @@
+/*
+ * lightning_attn.h -- C ABI of the B200-native Lightning Attention hot path.
+ *
+ * Drop-in boundary for the reference package `linattn` (arXiv 2405.17381,
+ * /root/reference/pkg/src/linattn).  The reference's hot path is two numpy
+ * functions per head; this ABI replaces them with batched, stream-ordered
+ * CUDA entry points taking plain device pointers.  No torch / CUDA types
+ * appear in the signatures (the stream is an opaque `void*` holding a
+ * cudaStream_t).
+ *
+ *   la_fwd  replaces  lightning_forward_decay(q, k, v, cfg)        kernels.py:253-284
+ *                     lightning_forward(q, k, v, cfg)  (lam == 1)  kernels.py:158-183
+ *   la_bwd  replaces  lightning_backward_decay(q, k, v, do, cfg)   kernels.py:287-334
+ *                     lightning_backward(q, k, v, do, cfg)         kernels.py:186-231
+ *   la_desc           AttentionConfig (n, d, B, lam, precision)    kernels.py:69-105,
+ *                     batched over (batch, heads); one lam per head (model.py:393-401)
+ *   la_status         ShapeError / DomainError                     matrixops.py:28-33
+ *   la_fwd_state /    the d x d carried summaries KvState          kernels.py:108-121,
+ *   la_bwd_state      exported so sequence segments (multi-GPU sequence parallel,
+ *                     chunked prefill) can be chained exactly.
+ *
+ * Semantics (all pinned by the reference's tests):
+ *   o[t]  = sum_{s<=t} lam^(t-s) (q[t].k[s]) v[s]                  causal, decayed
+ *   kv_in / kv_out   : forward state  F(p) = sum_{s<p} lam^(p-1-s) k[s] v[s]^T  (d x d)
+ *                      i.e. the reference's `state.kv` after the block ending at p.
+ *   dkv_in / dkv_out : adjoint state  R(p) = sum_{t>=p} lam^(t-p+1) q[t] do[t]^T
+ *                      i.e. the reference's `state.dkv` after the block starting at p.
+ *   The block size B is validated (>= 1) and otherwise semantically inert, exactly
+ *   as in the reference: the kernels choose their own tile.
+ *
+ * Memory: every pointer is device memory; q,k,v,o,do,dq,dk,dv share the desc's
+ * strides (element strides of batch, head, position; the feature stride is 1).
+ * States are [batch, heads, d, d] row-major in the accumulation type (float for
+ * LA_F32 / LA_BF16, double for LA_F64).  `lam` is a device array of `heads`
+ * doubles in (0, 1].  The caller allocates outputs and the workspace
+ * (la_workspace_bytes); the library keeps no global state besides the
+ * thread-local error string.  Calls are asynchronous on `stream` and reentrant.
+ */
+#ifndef LIGHTNING_ATTN_H_
+#define LIGHTNING_ATTN_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LA_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define LA_API __attribute__((visibility("default")))
+#else
+#define LA_API
+#endif
+
+typedef enum la_status {
+  LA_OK = 0,
+  LA_ERR_SHAPE = 1,       /* ShapeError  (kernels.py:137-146)                    */
+  LA_ERR_DOMAIN = 2,      /* DomainError (kernels.py:84-91, matrixops.py:72-77)  */
+  LA_ERR_CUDA = 3,        /* launch / runtime failure                            */
+  LA_ERR_UNSUPPORTED = 4  /* valid request this build does not implement         */
+} la_status;
+
+typedef enum la_dtype {
+  LA_F32 = 0,   /* reference precision="working"   (float32)                   */
+  LA_F64 = 1,   /* reference precision="reference" (float64)                   */
+  LA_BF16 = 2   /* bf16 operands, fp32 accumulation and fp32 states            */
+} la_dtype;
+
+typedef enum la_backend {
+  LA_BACKEND_AUTO = 0,     /* tcgen05 when eligible, else SIMT                  */
+  LA_BACKEND_SIMT = 1,     /* CUDA-core kernels (any d <= 128, any dtype)       */
+  LA_BACKEND_TCGEN05 = 2   /* TMA + tcgen05/TMEM kernels (bf16, d == 128)       */
+} la_backend;
+
+typedef struct la_desc {
+  int64_t batch;      /* >= 1                                                  */
+  int64_t heads;      /* >= 1                                                  */
+  int64_t n;          /* sequence length >= 1                                  */
+  int64_t d;          /* head dim >= 1                                         */
+  int64_t block;      /* reference B (>= 1); 0 = default min(d, n)             */
+  int32_t dtype;      /* la_dtype                                              */
+  int32_t backend;    /* la_backend                                            */
+  int64_t stride[3];  /* element strides of (batch, head, position); feature stride 1 */
+  int64_t segments;   /* 0 = auto; else sequence segments per (batch, head)    */
+} la_desc;
+
+/* Bytes of scratch the calls below need for this descriptor (may be 0). */
+LA_API size_t la_workspace_bytes(const la_desc* desc);
+
+/* Forward: o = LA(q, k, v).  kv_in (nullable) seeds the state at position 0;
+ * kv_out (nullable) receives F(n). */
+LA_API int la_fwd(const la_desc* desc, const void* q, const void* k, const void* v,
+           const double* lam, const void* kv_in, void* o, void* kv_out,
+           void* workspace, size_t workspace_bytes, void* stream);
+
+/* Backward: (dq, dk, dv) = d<LA(q,k,v), do>.  kv_in is the forward's kv_in
+ * (nullable = zeros); dkv_in (nullable) is R(n), the adjoint state arriving from
+ * beyond the sequence end; dkv_out (nullable) receives R(0). */
+LA_API int la_bwd(const la_desc* desc, const void* q, const void* k, const void* v,
+           const void* dout, const double* lam, const void* kv_in,
+           const void* dkv_in, void* dq, void* dk, void* dv, void* dkv_out,
+           void* workspace, size_t workspace_bytes, void* stream);
+
+/* Local summaries of one sequence segment, for sequence parallelism:
+ *   la_fwd_state: kv_delta  = sum_s lam^(n-1-s) k[s] v[s]^T   (= F(n) with kv_in = 0)
+ *   la_bwd_state: dkv_delta = sum_t lam^(t+1)   q[t] do[t]^T  (= R(0) with dkv_in = 0) */
+LA_API int la_fwd_state(const la_desc* desc, const void* k, const void* v,
+                 const double* lam, void* kv_delta,
+                 void* workspace, size_t workspace_bytes, void* stream);
+LA_API int la_bwd_state(const la_desc* desc, const void* q, const void* dout,
+                 const double* lam, void* dkv_delta,
+                 void* workspace, size_t workspace_bytes, void* stream);
+
+/* Number of kernels la_fwd (which = 0) or la_bwd (which = 1) launches for this
+ * descriptor (segment summaries, scan and the main passes); -1 on a bad desc. */
+LA_API int la_launch_count(const la_desc* desc, int which);
+
+/* Thread-local message for the last non-LA_OK status returned on this thread. */
+LA_API const char* la_last_error(void);
+
+/* ABI version (LA_ABI_VERSION) and a build string. */
+LA_API int la_abi_version(void);
+LA_API const char* la_build_info(void);
+
+#ifdef __cplusplus
+}  /* extern "C" */
+#endif
+
+#endif  /* LIGHTNING_ATTN_H_ */

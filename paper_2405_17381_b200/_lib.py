@@ -1,0 +1,108 @@
+"""ctypes binding of the C ABI in ``include/lightning_attn.h``.
+
+The library is built in-tree (``paper_2405_17381_b200/libla_b200.so``, see
+``build.py``).  There is deliberately no fallback: if the library is missing
+or fails to load, every compute entry point raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from ctypes import POINTER, c_char_p, c_double, c_int, c_int32, c_int64, c_size_t, c_void_p
+from pathlib import Path
+
+from .errors import DomainError, ShapeError
+
+LIB_PATH = Path(os.environ.get("LA_B200_LIB", Path(__file__).resolve().parent / "libla_b200.so"))
+
+LA_OK, LA_ERR_SHAPE, LA_ERR_DOMAIN, LA_ERR_CUDA, LA_ERR_UNSUPPORTED = range(5)
+LA_F32, LA_F64, LA_BF16 = 0, 1, 2
+LA_BACKEND_AUTO, LA_BACKEND_SIMT, LA_BACKEND_TCGEN05 = 0, 1, 2
+BACKENDS = {"auto": LA_BACKEND_AUTO, "simt": LA_BACKEND_SIMT, "tcgen05": LA_BACKEND_TCGEN05}
+
+# every symbol include/lightning_attn.h declares
+EXPORTS = ("la_workspace_bytes", "la_fwd", "la_bwd", "la_fwd_state", "la_bwd_state",
+           "la_launch_count", "la_last_error", "la_abi_version", "la_build_info")
+
+
+class LaDesc(ctypes.Structure):
+    """Mirror of ``la_desc``."""
+
+    _fields_ = [
+        ("batch", c_int64),
+        ("heads", c_int64),
+        ("n", c_int64),
+        ("d", c_int64),
+        ("block", c_int64),
+        ("dtype", c_int32),
+        ("backend", c_int32),
+        ("stride", c_int64 * 3),
+        ("segments", c_int64),
+    ]
+
+
+class LibraryMissing(RuntimeError):
+    """The CUDA library is not built / not loadable; there is no CPU fallback."""
+
+
+class UnsupportedError(NotImplementedError):
+    """LA_ERR_UNSUPPORTED: a valid request this build does not implement."""
+
+
+class CudaError(RuntimeError):
+    """LA_ERR_CUDA: launch or runtime failure inside the library."""
+
+
+_lib = None
+
+
+def load() -> ctypes.CDLL:
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not LIB_PATH.exists():
+        raise LibraryMissing(
+            f"{LIB_PATH} not found: build it with `python -m paper_2405_17381_b200.build` "
+            "(this package has no CPU fallback)")
+    try:
+        lib = ctypes.CDLL(str(LIB_PATH))
+    except OSError as exc:  # pragma: no cover - depends on the box
+        raise LibraryMissing(f"failed to load {LIB_PATH}: {exc}") from exc
+    P = POINTER(LaDesc)
+    lib.la_workspace_bytes.argtypes = [P]
+    lib.la_workspace_bytes.restype = c_size_t
+    lib.la_fwd.argtypes = [P, c_void_p, c_void_p, c_void_p, POINTER(c_double), c_void_p, c_void_p, c_void_p,
+                           c_void_p, c_size_t, c_void_p]
+    lib.la_fwd.restype = c_int
+    lib.la_bwd.argtypes = [P, c_void_p, c_void_p, c_void_p, c_void_p, POINTER(c_double), c_void_p, c_void_p,
+                           c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]
+    lib.la_bwd.restype = c_int
+    lib.la_fwd_state.argtypes = [P, c_void_p, c_void_p, POINTER(c_double), c_void_p, c_void_p, c_size_t, c_void_p]
+    lib.la_fwd_state.restype = c_int
+    lib.la_bwd_state.argtypes = [P, c_void_p, c_void_p, POINTER(c_double), c_void_p, c_void_p, c_size_t, c_void_p]
+    lib.la_bwd_state.restype = c_int
+    lib.la_launch_count.argtypes = [P, c_int]
+    lib.la_launch_count.restype = c_int
+    lib.la_last_error.argtypes = []
+    lib.la_last_error.restype = c_char_p
+    lib.la_abi_version.argtypes = []
+    lib.la_abi_version.restype = c_int
+    lib.la_build_info.argtypes = []
+    lib.la_build_info.restype = c_char_p
+    _lib = lib
+    return lib
+
+
+def check(status: int) -> None:
+    """Map an la_status onto the reference's exception classes (matrixops.py:28-33)."""
+    if status == LA_OK:
+        return
+    msg = load().la_last_error().decode(errors="replace")
+    if status == LA_ERR_SHAPE:
+        raise ShapeError(msg)
+    if status == LA_ERR_DOMAIN:
+        raise DomainError(msg)
+    if status == LA_ERR_UNSUPPORTED:
+        raise UnsupportedError(msg)
+    raise CudaError(msg)

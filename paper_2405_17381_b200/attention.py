@@ -1,0 +1,42 @@
+"""``torch.autograd.Function`` drop-in for the reference's per-head kernel calls.
+
+The reference's model calls ``lightning_forward_decay`` / ``lightning_backward_decay``
+once per head in a Python loop (model.py:393-401, 432-442).  Here one call
+covers every (batch, head): q, k, v are [batch, heads, n, d] (or the
+model-native [batch, n, heads, d] with ``layout="bnhd"``) and ``lam`` holds
+one frozen decay per head (no gradient).  Forward saves q, k, v
+only; the backward recomputes the carried state, as the reference does
+(kernels.py:309-318).
+"""
+
+from __future__ import annotations
+
+import torch
+
+from . import ops
+
+
+class LightningAttention(torch.autograd.Function):
+    """o = LA(q, k, v; lam) with exact causal decayed linear attention."""
+
+    @staticmethod
+    def forward(ctx, q, k, v, lam, block=None, layout="bhnd", backend="auto"):
+        heads = q.shape[1] if layout == "bhnd" else q.shape[2]
+        lam_dev = lam if (isinstance(lam, torch.Tensor) and lam.is_cuda and lam.dtype == torch.float64) \
+            else ops.decay_tensor(lam, heads, q.device)
+        o = ops.la_forward(q, k, v, None, block=block, layout=layout, backend=backend, lam_dev=lam_dev)
+        ctx.save_for_backward(q, k, v, lam_dev)
+        ctx.block, ctx.layout, ctx.backend = block, layout, backend
+        return o
+
+    @staticmethod
+    def backward(ctx, do):
+        q, k, v, lam_dev = ctx.saved_tensors
+        dq, dk, dv = ops.la_backward(q, k, v, do.to(q.dtype), None, block=ctx.block, layout=ctx.layout,
+                                     backend=ctx.backend, lam_dev=lam_dev)
+        return dq, dk, dv, None, None, None, None
+
+
+def lightning_attention(q, k, v, lam, block=None, layout="bhnd", backend="auto"):
+    """Functional form of :class:`LightningAttention`."""
+    return LightningAttention.apply(q, k, v, lam, block, layout, backend)

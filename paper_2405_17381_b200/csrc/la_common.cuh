@@ -1,0 +1,99 @@
+// la_common.cuh -- shared types for the Lightning Attention CUDA path.
+//
+// Every kernel in this library implements ONE primitive, a "pass" of causal
+// decayed linear attention over a (batch, head) sequence:
+//
+//   fwd  (rev = 0):  out[t] = sum_{s<=t} lam^(t-s) (a[t].b[s]) c[s]
+//                    state F(p) = sum_{s<p}  lam^(p-1-s) b[s] c[s]^T
+//   rev  (rev = 1):  out[s] = sum_{t>=s} lam^(t-s) (a[s].b[t]) c[t]
+//                    state R(p) = sum_{t>=p} lam^(t-p+1) b[t] c[t]^T
+//
+// The reference's forward is the fwd pass on (q, k, v) (kernels.py:253-284).
+// Its backward (kernels.py:287-334) is three passes:
+//   dq = fwd(a=do, b=v, c=k)   state = kv^T   (sweep 1, kernels.py:309-318)
+//   dk = rev(a=v,  b=do, c=q)  state = dkv^T  (sweep 2, dk line kernels.py:331)
+//   dv = rev(a=k,  b=q,  c=do) state = dkv    (sweep 2, dv line kernels.py:332)
+// and the reverse pass's state R is exactly the reference's `state.dkv`,
+// updated after use (kernels.py:333).  Per chunk of b rows (local i, j):
+//   fwd: mask M[i][j] = lam^(i-j) (j <= i); out-scale lam^(i+1);  in-scale lam^(b-1-j)
+//   rev: mask M[i][j] = lam^(j-i) (j >= i); out-scale lam^(b-1-i); in-scale lam^(j+1)
+//   state <- lam^b * state + sum_j in_scale[j] b[j] c[j]^T
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+#include "../../include/lightning_attn.h"
+
+namespace la {
+
+constexpr int kNumSMs = 148;  // B200
+
+// Load/convert helpers for the three operand dtypes.
+template <typename T> struct Cvt;
+template <> struct Cvt<float> {
+  __device__ __forceinline__ static float to_f(float x) { return x; }
+  __device__ __forceinline__ static float from_f(float x) { return x; }
+};
+template <> struct Cvt<double> {
+  __device__ __forceinline__ static double to_f(double x) { return x; }
+  __device__ __forceinline__ static double from_f(double x) { return x; }
+};
+template <> struct Cvt<__nv_bfloat16> {
+  __device__ __forceinline__ static float to_f(__nv_bfloat16 x) { return __bfloat162float(x); }
+  __device__ __forceinline__ static __nv_bfloat16 from_f(float x) { return __float2bfloat16_rn(x); }
+};
+
+// One pass over all (batch, head) sequences, split into `nseg` segments of
+// `seg_len` positions (a multiple of the kernel's chunk).  All tensors share
+// strides; the feature stride is 1.
+struct PassDesc {
+  const void* a;
+  const void* b;
+  const void* c;
+  void* out;              // nullptr in state-only mode
+  int64_t sb, sh, sn;     // element strides of batch, head, position
+  int batch, heads, n, d;
+  const double* lam;      // device [heads]
+  int rev;
+  int seg_len, nseg;
+  // state entering each segment (fwd: at its left edge, rev: at its right edge)
+  const void* state_in;   // nullable
+  int64_t state_in_bh_stride, state_in_seg_stride;
+  int state_in_T;         // 1: stored transposed
+  // final state of the pass (fwd: F(n), rev: R(0)), written by the last segment processed
+  void* state_out;        // nullable
+  int state_out_T;
+  // state-only mode: per-segment local summaries [bh][nseg][d][d]
+  void* delta_out;
+};
+
+// Segment plan shared by host code of every backend.
+struct Plan {
+  int chunk;    // rows per chunk in the kernel
+  int nseg;     // segments per (b, h)
+  int seg_len;  // positions per segment (multiple of chunk)
+};
+
+inline Plan make_plan(int64_t bh, int64_t n, int chunk, int64_t want_segments, int64_t target_ctas,
+                      int64_t min_chunks_per_seg) {
+  Plan p;
+  p.chunk = chunk;
+  int64_t nchunks = (n + chunk - 1) / chunk;
+  int64_t nseg = want_segments;
+  if (nseg <= 0) {
+    nseg = (target_ctas + bh - 1) / bh;
+    int64_t max_seg = nchunks / (min_chunks_per_seg > 0 ? min_chunks_per_seg : 1);
+    if (max_seg < 1) max_seg = 1;
+    if (nseg > max_seg) nseg = max_seg;
+  }
+  if (nseg < 1) nseg = 1;
+  if (nseg > nchunks) nseg = nchunks;
+  int64_t chunks_per_seg = (nchunks + nseg - 1) / nseg;
+  p.seg_len = (int)(chunks_per_seg * chunk);
+  p.nseg = (int)((n + p.seg_len - 1) / p.seg_len);
+  return p;
+}
+
+}  // namespace la

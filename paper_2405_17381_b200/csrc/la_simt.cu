@@ -1,0 +1,278 @@
+// la_simt.cu -- CUDA-core (FFMA / DFMA) kernels for every dtype and d <= 128.
+//
+// This is the precision path: fp64 ("reference" precision, kernels.py:66) and
+// fp32 ("working") must meet the reference's 1e-10 / 1e-4 bars, which TF32
+// tensor-core math cannot (SURVEY.md §7 hard part 5).  It is also the generic
+// fallback *inside CUDA* for shapes the tcgen05 kernels do not cover (d != 128),
+// never a CPU path.
+//
+// One CTA owns one (batch, head, segment); it walks the segment's chunks in
+// order (fwd) or reverse order (rev), keeping the d x d state in shared memory
+// in the accumulation type.  Per chunk (see la_common.cuh for the algebra):
+//   S   = (A B^T) * M                                   (b x b)
+//   out = S C + out_scale * (A state)                   (b x d)
+//   state = lam^b state + sum_j in_scale[j] B[j]^T C[j] (d x d)
+#include "la_common.cuh"
+#include "la_simt.cuh"
+
+namespace la {
+
+namespace {
+
+constexpr int kThreads = 256;
+
+template <typename Tacc>
+__device__ __forceinline__ Tacc load_state(const void* base, int64_t off, int d, int r, int c, int T) {
+  const Tacc* p = reinterpret_cast<const Tacc*>(base) + off;
+  return T ? p[(int64_t)c * d + r] : p[(int64_t)r * d + c];
+}
+
+template <typename Tin, typename Tacc, int C, bool STATE_ONLY>
+__global__ void __launch_bounds__(kThreads) simt_pass_kernel(PassDesc p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int d = p.d;
+  const int ld = d + 1;  // padded row stride of the chunk tiles
+  Tacc* sKV = reinterpret_cast<Tacc*>(smem_raw);
+  Tacc* sA = sKV + d * d;
+  Tacc* sB = sA + C * ld;
+  Tacc* sC = sB + C * ld;
+  Tacc* sS = sC + C * ld;
+  Tacc* pw = sS + C * (C + 1);  // lam^0 .. lam^C
+
+  const int tid = threadIdx.x;
+  const int seg = blockIdx.x;
+  const int bh = blockIdx.y;
+  const int bi = bh / p.heads, hi = bh % p.heads;
+  const int p0 = seg * p.seg_len;
+  const int p1 = min(p.n, p0 + p.seg_len);
+  const int nchunks = (p1 - p0 + C - 1) / C;
+  const double lam = p.lam[hi];
+
+  const int64_t base = (int64_t)bi * p.sb + (int64_t)hi * p.sh;
+  const Tin* A = reinterpret_cast<const Tin*>(p.a) + base;
+  const Tin* Bm = reinterpret_cast<const Tin*>(p.b) + base;
+  const Tin* Cm = reinterpret_cast<const Tin*>(p.c) + base;
+  Tin* O = STATE_ONLY ? nullptr : reinterpret_cast<Tin*>(p.out) + base;
+
+  // Power ladder in fp64 by repeated multiplication, then cast
+  // (the reference builds its ladders the same way: matrixops.py:104-119).
+  if (tid == 0) {
+    double x = 1.0;
+    for (int k = 0; k <= C; ++k) {
+      pw[k] = (Tacc)x;
+      x *= lam;
+    }
+  }
+  // State entering this segment.
+  const bool have_in = (!STATE_ONLY) && p.state_in != nullptr;
+  const int64_t in_off = (int64_t)bh * p.state_in_bh_stride + (int64_t)seg * p.state_in_seg_stride;
+  for (int e = tid; e < d * d; e += kThreads) {
+    const int r = e / d, c = e % d;
+    sKV[e] = have_in ? load_state<Tacc>(p.state_in, in_off, d, r, c, p.state_in_T) : (Tacc)0;
+  }
+  __syncthreads();
+
+  for (int ci = 0; ci < nchunks; ++ci) {
+    const int t = p.rev ? (nchunks - 1 - ci) : ci;
+    const int r0 = p0 + t * C;
+    const int b = min(C, p1 - r0);
+
+    for (int idx = tid; idx < b * d; idx += kThreads) {
+      const int i = idx / d, k = idx % d;
+      const int64_t g = (int64_t)(r0 + i) * p.sn + k;
+      if (!STATE_ONLY) sA[i * ld + k] = (Tacc)Cvt<Tin>::to_f(A[g]);
+      sB[i * ld + k] = (Tacc)Cvt<Tin>::to_f(Bm[g]);
+      sC[i * ld + k] = (Tacc)Cvt<Tin>::to_f(Cm[g]);
+    }
+    __syncthreads();
+
+    if (!STATE_ONLY) {
+      // S = (A B^T) * M
+      for (int idx = tid; idx < b * b; idx += kThreads) {
+        const int i = idx / b, j = idx % b;
+        const bool keep = p.rev ? (j >= i) : (j <= i);
+        Tacc s = 0;
+        if (keep) {
+          const Tacc* ar = sA + i * ld;
+          const Tacc* br = sB + j * ld;
+          for (int k = 0; k < d; ++k) s += ar[k] * br[k];
+          s *= pw[p.rev ? (j - i) : (i - j)];
+        }
+        sS[i * (C + 1) + j] = s;
+      }
+      __syncthreads();
+      // out = S C + out_scale * (A state)
+      for (int idx = tid; idx < b * d; idx += kThreads) {
+        const int i = idx / d, col = idx % d;
+        const int jlo = p.rev ? i : 0, jhi = p.rev ? b : i + 1;
+        Tacc intra = 0;
+        for (int j = jlo; j < jhi; ++j) intra += sS[i * (C + 1) + j] * sC[j * ld + col];
+        Tacc inter = 0;
+        const Tacc* ar = sA + i * ld;
+        for (int k = 0; k < d; ++k) inter += ar[k] * sKV[k * d + col];
+        const Tacc osc = pw[p.rev ? (b - 1 - i) : (i + 1)];
+        O[(int64_t)(r0 + i) * p.sn + col] = Cvt<Tin>::from_f(intra + osc * inter);
+      }
+      __syncthreads();
+    }
+    // state <- lam^b state + sum_j in_scale[j] B[j]^T C[j]
+    const Tacc decay = pw[b];
+    for (int e = tid; e < d * d; e += kThreads) {
+      const int k = e / d, col = e % d;
+      Tacc acc = 0;
+      for (int j = 0; j < b; ++j) {
+        const Tacc isc = pw[p.rev ? (j + 1) : (b - 1 - j)];
+        acc += isc * sB[j * ld + k] * sC[j * ld + col];
+      }
+      sKV[e] = decay * sKV[e] + acc;
+    }
+    __syncthreads();
+  }
+
+  if (STATE_ONLY) {
+    Tacc* dst = reinterpret_cast<Tacc*>(p.delta_out) + ((int64_t)bh * p.nseg + seg) * d * d;
+    for (int e = tid; e < d * d; e += kThreads) dst[e] = sKV[e];
+  } else if (p.state_out != nullptr) {
+    const bool last = p.rev ? (seg == 0) : (seg == p.nseg - 1);
+    if (last) {
+      Tacc* dst = reinterpret_cast<Tacc*>(p.state_out) + (int64_t)bh * d * d;
+      for (int e = tid; e < d * d; e += kThreads) {
+        const int r = e / d, c = e % d;
+        dst[p.state_out_T ? (c * d + r) : e] = sKV[e];
+      }
+    }
+  }
+}
+
+// Exclusive decayed scan of the per-segment summaries along the sequence:
+//   fwd: in[0] = user (or 0);   in[s+1] = lam^len(s) in[s] + delta[s]
+//   rev: in[last] = user (or 0); in[s-1] = lam^len(s) in[s] + delta[s]
+// `final_out` (nullable) receives the inclusive total (F(n) / R(0)).
+template <typename Tacc>
+__global__ void __launch_bounds__(kThreads) segment_scan_kernel(
+    const Tacc* __restrict__ delta, Tacc* __restrict__ seg_in, const void* user_in, int user_T,
+    Tacc* final_out, int final_T, const double* lam, int heads, int d, int n, int seg_len, int nseg,
+    int rev) {
+  const int e = blockIdx.x * kThreads + threadIdx.x;
+  const int bh = blockIdx.y;
+  if (e >= d * d) return;
+  const int r = e / d, c = e % d;
+  const double l = lam[bh % heads];
+  Tacc s = 0;
+  if (user_in != nullptr) {
+    const Tacc* u = reinterpret_cast<const Tacc*>(user_in) + (int64_t)bh * d * d;
+    s = user_T ? u[c * d + r] : u[e];
+  }
+  for (int k = 0; k < nseg; ++k) {
+    const int sgi = rev ? (nseg - 1 - k) : k;
+    const int64_t off = ((int64_t)bh * nseg + sgi) * d * d + e;
+    if (seg_in != nullptr) seg_in[off] = s;
+    const int len = min(seg_len, n - sgi * seg_len);
+    s = (Tacc)pow(l, (double)len) * s + delta[off];
+  }
+  if (final_out != nullptr) final_out[(int64_t)bh * d * d + (final_T ? c * d + r : e)] = s;
+}
+
+template <typename Tacc, int C>
+size_t simt_smem_bytes(int d) {
+  return sizeof(Tacc) * ((size_t)d * d + 3 * (size_t)C * (d + 1) + (size_t)C * (C + 1) + C + 1);
+}
+
+template <typename Tin, typename Tacc, int C, bool STATE_ONLY>
+cudaError_t launch_simt(const PassDesc& p, cudaStream_t st) {
+  auto kern = simt_pass_kernel<Tin, Tacc, C, STATE_ONLY>;
+  const size_t smem = simt_smem_bytes<Tacc, C>(p.d);
+  cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (err != cudaSuccess) return err;
+  dim3 grid(p.nseg, p.batch * p.heads);
+  kern<<<grid, kThreads, smem, st>>>(p);
+  return cudaGetLastError();
+}
+
+template <typename Tin> struct SimtTraits;
+template <> struct SimtTraits<double> { using Acc = double; static constexpr int C = 16; };
+template <> struct SimtTraits<float> { using Acc = float; static constexpr int C = 32; };
+template <> struct SimtTraits<__nv_bfloat16> { using Acc = float; static constexpr int C = 32; };
+
+template <typename Tin>
+cudaError_t simt_pass_t(PassDesc p, void* ws, cudaStream_t st) {
+  using Acc = typename SimtTraits<Tin>::Acc;
+  constexpr int C = SimtTraits<Tin>::C;
+  const int bh = p.batch * p.heads;
+  const size_t dd = (size_t)p.d * p.d;
+  if (p.nseg > 1) {
+    Acc* delta = reinterpret_cast<Acc*>(ws);
+    Acc* seg_in = delta + (size_t)bh * p.nseg * dd;
+    PassDesc s = p;
+    s.out = nullptr;
+    s.state_in = nullptr;
+    s.state_out = nullptr;
+    s.delta_out = delta;
+    cudaError_t err = launch_simt<Tin, Acc, C, true>(s, st);
+    if (err != cudaSuccess) return err;
+    dim3 grid((unsigned)((dd + kThreads - 1) / kThreads), bh);
+    segment_scan_kernel<Acc><<<grid, kThreads, 0, st>>>(delta, seg_in, p.state_in, p.state_in_T, nullptr, 0,
+                                                         p.lam, p.heads, p.d, p.n, p.seg_len, p.nseg, p.rev);
+    err = cudaGetLastError();
+    if (err != cudaSuccess) return err;
+    p.state_in = seg_in;
+    p.state_in_T = 0;
+    p.state_in_bh_stride = (int64_t)p.nseg * dd;
+    p.state_in_seg_stride = (int64_t)dd;
+  } else {
+    p.state_in_bh_stride = (int64_t)dd;
+    p.state_in_seg_stride = 0;
+  }
+  return launch_simt<Tin, Acc, C, false>(p, st);
+}
+
+template <typename Tin>
+cudaError_t simt_state_t(PassDesc p, void* ws, cudaStream_t st) {
+  using Acc = typename SimtTraits<Tin>::Acc;
+  constexpr int C = SimtTraits<Tin>::C;
+  const int bh = p.batch * p.heads;
+  const size_t dd = (size_t)p.d * p.d;
+  if (p.nseg == 1) {
+    p.delta_out = p.state_out;  // single segment: its summary is the answer
+    return launch_simt<Tin, Acc, C, true>(p, st);
+  }
+  Acc* delta = reinterpret_cast<Acc*>(ws);
+  p.delta_out = delta;
+  cudaError_t err = launch_simt<Tin, Acc, C, true>(p, st);
+  if (err != cudaSuccess) return err;
+  dim3 grid((unsigned)((dd + kThreads - 1) / kThreads), bh);
+  segment_scan_kernel<Acc><<<grid, kThreads, 0, st>>>(delta, nullptr, nullptr, 0, reinterpret_cast<Acc*>(p.state_out),
+                                                       p.state_out_T, p.lam, p.heads, p.d, p.n, p.seg_len, p.nseg,
+                                                       p.rev);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+int simt_chunk(int dtype) { return dtype == LA_F64 ? SimtTraits<double>::C : SimtTraits<float>::C; }
+
+size_t simt_workspace_bytes(int dtype, int64_t bh, int nseg, int d) {
+  if (nseg <= 1) return 0;
+  const size_t acc = dtype == LA_F64 ? sizeof(double) : sizeof(float);
+  return 2 * acc * (size_t)bh * nseg * d * d;
+}
+
+cudaError_t simt_pass(int dtype, const PassDesc& p, void* ws, cudaStream_t st) {
+  switch (dtype) {
+    case LA_F64: return simt_pass_t<double>(p, ws, st);
+    case LA_F32: return simt_pass_t<float>(p, ws, st);
+    case LA_BF16: return simt_pass_t<__nv_bfloat16>(p, ws, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t simt_state(int dtype, const PassDesc& p, void* ws, cudaStream_t st) {
+  switch (dtype) {
+    case LA_F64: return simt_state_t<double>(p, ws, st);
+    case LA_F32: return simt_state_t<float>(p, ws, st);
+    case LA_BF16: return simt_state_t<__nv_bfloat16>(p, ws, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace la

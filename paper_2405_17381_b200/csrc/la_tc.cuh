@@ -1,0 +1,11 @@
+// la_tc.cuh -- host-side entry points of the TMA + tcgen05 backend (la_tc.cu).
+#pragma once
+#include "la_common.cuh"
+
+namespace la {
+bool tc_supported(int dtype, int d, const int64_t* strides);
+Plan tc_plan(int64_t bh, int64_t n, int d, int64_t want_segments);
+size_t tc_workspace_bytes(int64_t bh, int nseg, int d);
+cudaError_t tc_pass(const PassDesc& p, void* ws, cudaStream_t st);
+cudaError_t tc_state(const PassDesc& p, void* ws, cudaStream_t st);
+}  // namespace la

@@ -1,0 +1,216 @@
+"""Batched device entry points: torch CUDA tensors in, torch CUDA tensors out.
+
+These are thin host wrappers over the C ABI (``_lib``): they validate like
+the reference (``AttentionConfig`` / ``_prep``, kernels.py:84-150), build the
+``la_desc``, allocate outputs and workspace with torch's caching allocator,
+and launch on the current stream.  Nothing here computes on the CPU.
+
+Tensor layouts: ``"bhnd"`` = [batch, heads, n, d] (default) or ``"bnhd"`` =
+[batch, n, heads, d] (the model-native projection layout; no transpose copy).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+from typing import Sequence
+
+import torch
+
+from . import _lib
+from .errors import DomainError, ShapeError, check_decay
+
+_DTYPES = {torch.float32: _lib.LA_F32, torch.float64: _lib.LA_F64, torch.bfloat16: _lib.LA_BF16}
+
+
+def state_dtype(dtype: torch.dtype) -> torch.dtype:
+    """Carried-state dtype: fp64 for the fp64 path, fp32 otherwise."""
+    return torch.float64 if dtype == torch.float64 else torch.float32
+
+
+def decay_tensor(lam, heads: int, device) -> torch.Tensor:
+    """Validate per-head decays (host side) and return a device fp64 [heads] tensor."""
+    if isinstance(lam, torch.Tensor):
+        vals = lam.detach().to("cpu", torch.float64).reshape(-1).tolist()
+    elif isinstance(lam, (int, float)):
+        vals = [float(lam)] * heads
+    else:
+        vals = [float(x) for x in lam]
+    if len(vals) == 1 and heads > 1:
+        vals = vals * heads
+    if len(vals) != heads:
+        raise ShapeError(f"need one decay per head: got {len(vals)} for {heads} heads")
+    for x in vals:
+        check_decay(x)
+    return torch.tensor(vals, dtype=torch.float64, device=device)
+
+
+@dataclass(frozen=True)
+class Geometry:
+    batch: int
+    heads: int
+    n: int
+    d: int
+    strides: tuple[int, int, int]
+
+
+def _geometry(x: torch.Tensor, layout: str) -> Geometry:
+    if x.dim() != 4:
+        raise ShapeError(f"expected a 4-D tensor ({layout}), got shape {tuple(x.shape)}")
+    if layout == "bhnd":
+        b, h, n, d = x.shape
+        s = (x.stride(0), x.stride(1), x.stride(2))
+    elif layout == "bnhd":
+        b, n, h, d = x.shape
+        s = (x.stride(0), x.stride(2), x.stride(1))
+    else:
+        raise DomainError(f"layout must be 'bhnd' or 'bnhd', got {layout!r}")
+    return Geometry(b, h, n, d, s)
+
+
+def _prep(tensors: Sequence[torch.Tensor], names: str, layout: str):
+    """Shape/dtype/device checks; returns tensors sharing one contiguous layout."""
+    first = tensors[0]
+    if not isinstance(first, torch.Tensor):
+        raise ShapeError(f"{names[0]}: expected a torch.Tensor")
+    if first.dtype not in _DTYPES:
+        raise DomainError(f"dtype must be float32, float64 or bfloat16, got {first.dtype}")
+    if not first.is_cuda:
+        raise DomainError(f"{names[0]}: tensors must live on a CUDA device (no CPU path)")
+    for t, name in zip(tensors, names):
+        if not isinstance(t, torch.Tensor):
+            raise ShapeError(f"{name}: expected a torch.Tensor")
+        if t.shape != first.shape:
+            raise ShapeError(f"{name}: shape {tuple(t.shape)} != {tuple(first.shape)}")
+        if t.dtype != first.dtype or t.device != first.device:
+            raise ShapeError(f"{name}: dtype/device {t.dtype}/{t.device} != {first.dtype}/{first.device}")
+    out = [t if t.is_contiguous() else t.contiguous() for t in tensors]
+    return out, _geometry(out[0], layout)
+
+
+def _desc(g: Geometry, dtype: torch.dtype, block, backend: str, segments: int) -> _lib.LaDesc:
+    if block is not None and int(block) < 1:
+        raise DomainError(f"block size must be >= 1, got {block}")
+    if backend not in _lib.BACKENDS:
+        raise DomainError(f"backend must be one of {sorted(_lib.BACKENDS)}, got {backend!r}")
+    desc = _lib.LaDesc()
+    desc.batch, desc.heads, desc.n, desc.d = g.batch, g.heads, g.n, g.d
+    desc.block = 0 if block is None else int(block)
+    desc.dtype = _DTYPES[dtype]
+    desc.backend = _lib.BACKENDS[backend]
+    for i in range(3):
+        desc.stride[i] = g.strides[i]
+    desc.segments = int(segments)
+    return desc
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _lam_ptr(lam_dev: torch.Tensor):
+    return ctypes.cast(ctypes.c_void_p(lam_dev.data_ptr()), ctypes.POINTER(ctypes.c_double))
+
+
+def _state(t, g: Geometry, dtype, name):
+    if t is None:
+        return None
+    if t.shape != (g.batch, g.heads, g.d, g.d):
+        raise ShapeError(f"{name}: expected shape {(g.batch, g.heads, g.d, g.d)}, got {tuple(t.shape)}")
+    return t.to(dtype=state_dtype(dtype)).contiguous()
+
+
+def _workspace(lib, desc, device):
+    nbytes = lib.la_workspace_bytes(ctypes.byref(desc))
+    ws = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=device)
+    return ws, nbytes
+
+
+def _stream(device) -> ctypes.c_void_p:
+    return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+def la_forward(q, k, v, lam, *, block=None, kv_in=None, want_state=False, layout="bhnd",
+               backend="auto", segments=0, lam_dev=None):
+    """o (and kv_out) for batched q, k, v.  ``lam``: float or one value per head."""
+    (q, k, v), g = _prep([q, k, v], "QKV", layout)
+    lib = _lib.load()
+    desc = _desc(g, q.dtype, block, backend, segments)
+    lam_dev = decay_tensor(lam, g.heads, q.device) if lam_dev is None else lam_dev
+    kv_in = _state(kv_in, g, q.dtype, "kv_in")
+    o = torch.empty_like(q)
+    kv_out = torch.empty((g.batch, g.heads, g.d, g.d), dtype=state_dtype(q.dtype), device=q.device) \
+        if want_state else None
+    ws, nbytes = _workspace(lib, desc, q.device)
+    _lib.check(lib.la_fwd(ctypes.byref(desc), _ptr(q), _ptr(k), _ptr(v), _lam_ptr(lam_dev), _ptr(kv_in),
+                          _ptr(o), _ptr(kv_out), _ptr(ws), nbytes, _stream(q.device)))
+    return (o, kv_out) if want_state else o
+
+
+def la_backward(q, k, v, do, lam, *, block=None, kv_in=None, dkv_in=None, want_state=False, layout="bhnd",
+                backend="auto", segments=0, lam_dev=None):
+    """(dq, dk, dv) (and dkv_out = R(0)) of <LA(q, k, v), do>."""
+    (q, k, v, do), g = _prep([q, k, v, do], ["Q", "K", "V", "dO"], layout)
+    lib = _lib.load()
+    desc = _desc(g, q.dtype, block, backend, segments)
+    lam_dev = decay_tensor(lam, g.heads, q.device) if lam_dev is None else lam_dev
+    kv_in = _state(kv_in, g, q.dtype, "kv_in")
+    dkv_in = _state(dkv_in, g, q.dtype, "dkv_in")
+    dq, dk, dv = torch.empty_like(q), torch.empty_like(q), torch.empty_like(q)
+    dkv_out = torch.empty((g.batch, g.heads, g.d, g.d), dtype=state_dtype(q.dtype), device=q.device) \
+        if want_state else None
+    ws, nbytes = _workspace(lib, desc, q.device)
+    _lib.check(lib.la_bwd(ctypes.byref(desc), _ptr(q), _ptr(k), _ptr(v), _ptr(do), _lam_ptr(lam_dev),
+                          _ptr(kv_in), _ptr(dkv_in), _ptr(dq), _ptr(dk), _ptr(dv), _ptr(dkv_out), _ptr(ws),
+                          nbytes, _stream(q.device)))
+    return (dq, dk, dv, dkv_out) if want_state else (dq, dk, dv)
+
+
+def la_forward_state(k, v, lam, *, layout="bhnd", backend="auto", segments=0, lam_dev=None):
+    """Local forward summary sum_s lam^(n-1-s) k_s v_s^T, [batch, heads, d, d]."""
+    (k, v), g = _prep([k, v], "KV", layout)
+    lib = _lib.load()
+    desc = _desc(g, k.dtype, None, backend, segments)
+    lam_dev = decay_tensor(lam, g.heads, k.device) if lam_dev is None else lam_dev
+    out = torch.empty((g.batch, g.heads, g.d, g.d), dtype=state_dtype(k.dtype), device=k.device)
+    ws, nbytes = _workspace(lib, desc, k.device)
+    _lib.check(lib.la_fwd_state(ctypes.byref(desc), _ptr(k), _ptr(v), _lam_ptr(lam_dev), _ptr(out), _ptr(ws),
+                                nbytes, _stream(k.device)))
+    return out
+
+
+def la_backward_state(q, do, lam, *, layout="bhnd", backend="auto", segments=0, lam_dev=None):
+    """Local adjoint summary sum_t lam^(t+1) q_t do_t^T, [batch, heads, d, d]."""
+    (q, do), g = _prep([q, do], ["Q", "dO"], layout)
+    lib = _lib.load()
+    desc = _desc(g, q.dtype, None, backend, segments)
+    lam_dev = decay_tensor(lam, g.heads, q.device) if lam_dev is None else lam_dev
+    out = torch.empty((g.batch, g.heads, g.d, g.d), dtype=state_dtype(q.dtype), device=q.device)
+    ws, nbytes = _workspace(lib, desc, q.device)
+    _lib.check(lib.la_bwd_state(ctypes.byref(desc), _ptr(q), _ptr(do), _lam_ptr(lam_dev), _ptr(out), _ptr(ws),
+                                nbytes, _stream(q.device)))
+    return out
+
+
+def workspace_bytes(shape, dtype=torch.bfloat16, *, layout="bhnd", backend="auto", segments=0) -> int:
+    """la_workspace_bytes for a [b, h, n, d] (or bnhd) problem, without tensors."""
+    if layout == "bhnd":
+        b, h, n, d = shape
+        strides = (h * n * d, n * d, d)
+    else:
+        b, n, h, d = shape
+        strides = (n * h * d, d, h * d)
+    desc = _desc(Geometry(b, h, n, d, strides), dtype, None, backend, segments)
+    return int(_lib.load().la_workspace_bytes(ctypes.byref(desc)))
+
+
+def launch_count(shape, dtype=torch.bfloat16, *, which="fwd", layout="bhnd", backend="auto", segments=0) -> int:
+    """Kernels one la_fwd / la_bwd call launches for this problem (la_launch_count)."""
+    if layout == "bhnd":
+        b, h, n, d = shape
+        strides = (h * n * d, n * d, d)
+    else:
+        b, n, h, d = shape
+        strides = (n * h * d, d, h * d)
+    desc = _desc(Geometry(b, h, n, d, strides), dtype, None, backend, segments)
+    return int(_lib.load().la_launch_count(ctypes.byref(desc), 0 if which == "fwd" else 1))

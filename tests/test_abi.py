@@ -1,0 +1,84 @@
+"""CPU-side checks of the C ABI: the library loads, exports every symbol the
+header declares, and validates descriptors exactly like the reference's
+AttentionConfig/_prep (no device work happens on these paths)."""
+
+import ctypes
+import re
+from pathlib import Path
+
+import pytest
+
+from paper_2405_17381_b200 import _lib
+from paper_2405_17381_b200.errors import DomainError, ShapeError
+
+HEADER = Path(__file__).resolve().parent.parent / "include" / "lightning_attn.h"
+
+
+def _declared():
+    text = HEADER.read_text()
+    return sorted(set(re.findall(r"LA_API\s+[\w\s\*]+?\b(la_\w+)\s*\(", text)))
+
+
+def test_header_declares_what_binding_expects():
+    assert _declared() == sorted(_lib.EXPORTS)
+
+
+def test_library_exports_every_declared_symbol():
+    lib = _lib.load()
+    for name in _declared():
+        assert hasattr(lib, name), name
+    assert lib.la_abi_version() == 1
+    assert b"sm_100a" in lib.la_build_info()
+
+
+def _desc(**kw):
+    d = _lib.LaDesc()
+    d.batch, d.heads, d.n, d.d = kw.get("batch", 1), kw.get("heads", 2), kw.get("n", 64), kw.get("d", 16)
+    d.block = kw.get("block", 0)
+    d.dtype = kw.get("dtype", _lib.LA_F32)
+    d.backend = kw.get("backend", _lib.LA_BACKEND_AUTO)
+    s = kw.get("stride", (d.heads * d.n * d.d, d.n * d.d, d.d))
+    for i in range(3):
+        d.stride[i] = s[i]
+    d.segments = kw.get("segments", 0)
+    return d
+
+
+def _fwd(desc):
+    lib = _lib.load()
+    dummy = ctypes.c_void_p(16)
+    lam = ctypes.cast(ctypes.c_void_p(16), ctypes.POINTER(ctypes.c_double))
+    return lib.la_fwd(ctypes.byref(desc), dummy, dummy, dummy, lam, None, dummy, None, None, 0, None)
+
+
+@pytest.mark.parametrize("kw,code", [
+    (dict(n=0), _lib.LA_ERR_DOMAIN),            # kernels.py:85-86
+    (dict(d=0), _lib.LA_ERR_DOMAIN),
+    (dict(block=-1), _lib.LA_ERR_DOMAIN),       # kernels.py:90-91
+    (dict(dtype=7), _lib.LA_ERR_DOMAIN),        # kernels.py:88-89 (precision)
+    (dict(batch=0), _lib.LA_ERR_SHAPE),
+    (dict(stride=(0, 0, 3)), _lib.LA_ERR_SHAPE),
+    (dict(d=256), _lib.LA_ERR_UNSUPPORTED),
+    (dict(dtype=_lib.LA_F64, backend=_lib.LA_BACKEND_TCGEN05), _lib.LA_ERR_UNSUPPORTED),
+])
+def test_descriptor_validation(kw, code):
+    assert _fwd(_desc(**kw)) == code
+    assert _lib.load().la_last_error()
+
+
+def test_status_maps_to_reference_exceptions():
+    with pytest.raises(DomainError):
+        _lib.check(_fwd(_desc(n=0)))
+    with pytest.raises(ShapeError):
+        _lib.check(_fwd(_desc(batch=0)))
+    with pytest.raises(_lib.UnsupportedError):
+        _lib.check(_fwd(_desc(d=512)))
+
+
+def test_workspace_is_bounded_in_n():
+    lib = _lib.load()
+    sizes = set()
+    for n in (1 << 14, 1 << 17, 1 << 20):
+        sizes.add(lib.la_workspace_bytes(ctypes.byref(_desc(n=n, d=128, heads=16, dtype=_lib.LA_BF16))))
+    assert len(sizes) == 1, sizes
+    assert lib.la_workspace_bytes(ctypes.byref(_desc(n=0))) == 0
