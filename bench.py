@@ -191,7 +191,8 @@ def run_ours(args) -> None:
     launches = sum(ops.launch_count(tuple(inputs[n][0].shape), which="fwd")
                    + ops.launch_count(tuple(inputs[n][0].shape), which="bwd") for n in seq_lens) * args.steps
 
-    e2e = run_e2e(ops, seq_lens, tokens, lam_dev, device, min(args.steps, args.e2e_steps), world)
+    e2e = None if args.no_e2e else run_e2e(ops, seq_lens, tokens, lam_dev, device, min(args.steps, args.e2e_steps),
+                                           world)
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -387,6 +388,7 @@ def main() -> None:
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")

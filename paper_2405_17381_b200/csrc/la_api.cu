@@ -83,8 +83,8 @@ la::Plan plan_for(const la_desc* desc, int backend) {
 
 size_t ws_bytes_for(const la_desc* desc, int backend, const la::Plan& plan) {
   const int64_t bh = desc->batch * desc->heads;
-  if (backend == LA_BACKEND_TCGEN05) return la::tc_workspace_bytes(bh, plan.nseg, (int)desc->d);
-  return la::simt_workspace_bytes(desc->dtype, bh, plan.nseg, (int)desc->d);
+  if (backend == LA_BACKEND_TCGEN05) return la::tc_workspace_bytes(bh, plan.nseg_ws, (int)desc->d);
+  return la::simt_workspace_bytes(desc->dtype, bh, plan.nseg_ws, (int)desc->d);
 }
 
 la::PassDesc base_pass(const la_desc* desc, const la::Plan& plan, const double* lam) {
@@ -104,12 +104,18 @@ la::PassDesc base_pass(const la_desc* desc, const la::Plan& plan, const double* 
 }
 
 cudaError_t run_pass(int backend, int dtype, const la::PassDesc& p, void* ws, cudaStream_t st) {
-  if (backend == LA_BACKEND_TCGEN05) return la::tc_pass(p, ws, st);
+  if (backend == LA_BACKEND_TCGEN05) {
+    if (!la::tc_pointers_ok(p)) return cudaErrorMisalignedAddress;  // TMA needs 16-byte aligned bases
+    return la::tc_pass(p, ws, st);
+  }
   return la::simt_pass(dtype, p, ws, st);
 }
 
 cudaError_t run_state(int backend, int dtype, const la::PassDesc& p, void* ws, cudaStream_t st) {
-  if (backend == LA_BACKEND_TCGEN05) return la::tc_state(p, ws, st);
+  if (backend == LA_BACKEND_TCGEN05) {
+    if (!la::tc_pointers_ok(p)) return cudaErrorMisalignedAddress;
+    return la::tc_state(p, ws, st);
+  }
   return la::simt_state(dtype, p, ws, st);
 }
 

@@ -74,6 +74,7 @@ struct Plan {
   int chunk;    // rows per chunk in the kernel
   int nseg;     // segments per (b, h)
   int seg_len;  // positions per segment (multiple of chunk)
+  int nseg_ws;  // segments the workspace is sized for: independent of n (kernels.py:342-368 c05)
 };
 
 inline Plan make_plan(int64_t bh, int64_t n, int chunk, int64_t want_segments, int64_t target_ctas,
@@ -90,6 +91,8 @@ inline Plan make_plan(int64_t bh, int64_t n, int chunk, int64_t want_segments, i
   }
   if (nseg < 1) nseg = 1;
   if (nseg > nchunks) nseg = nchunks;
+  int64_t cap = want_segments > 0 ? want_segments : (target_ctas + bh - 1) / bh;
+  p.nseg_ws = (int)(cap < 1 ? 1 : cap);
   int64_t chunks_per_seg = (nchunks + nseg - 1) / nseg;
   p.seg_len = (int)(chunks_per_seg * chunk);
   p.nseg = (int)((n + p.seg_len - 1) / p.seg_len);

@@ -13,6 +13,7 @@
 //   out = S C + out_scale * (A state)                   (b x d)
 //   state = lam^b state + sum_j in_scale[j] B[j]^T C[j] (d x d)
 #include "la_common.cuh"
+#include "la_scan.cuh"
 #include "la_simt.cuh"
 
 namespace la {
@@ -144,35 +145,6 @@ __global__ void __launch_bounds__(kThreads) simt_pass_kernel(PassDesc p) {
   }
 }
 
-// Exclusive decayed scan of the per-segment summaries along the sequence:
-//   fwd: in[0] = user (or 0);   in[s+1] = lam^len(s) in[s] + delta[s]
-//   rev: in[last] = user (or 0); in[s-1] = lam^len(s) in[s] + delta[s]
-// `final_out` (nullable) receives the inclusive total (F(n) / R(0)).
-template <typename Tacc>
-__global__ void __launch_bounds__(kThreads) segment_scan_kernel(
-    const Tacc* __restrict__ delta, Tacc* __restrict__ seg_in, const void* user_in, int user_T,
-    Tacc* final_out, int final_T, const double* lam, int heads, int d, int n, int seg_len, int nseg,
-    int rev) {
-  const int e = blockIdx.x * kThreads + threadIdx.x;
-  const int bh = blockIdx.y;
-  if (e >= d * d) return;
-  const int r = e / d, c = e % d;
-  const double l = lam[bh % heads];
-  Tacc s = 0;
-  if (user_in != nullptr) {
-    const Tacc* u = reinterpret_cast<const Tacc*>(user_in) + (int64_t)bh * d * d;
-    s = user_T ? u[c * d + r] : u[e];
-  }
-  for (int k = 0; k < nseg; ++k) {
-    const int sgi = rev ? (nseg - 1 - k) : k;
-    const int64_t off = ((int64_t)bh * nseg + sgi) * d * d + e;
-    if (seg_in != nullptr) seg_in[off] = s;
-    const int len = min(seg_len, n - sgi * seg_len);
-    s = (Tacc)pow(l, (double)len) * s + delta[off];
-  }
-  if (final_out != nullptr) final_out[(int64_t)bh * d * d + (final_T ? c * d + r : e)] = s;
-}
-
 template <typename Tacc, int C>
 size_t simt_smem_bytes(int d) {
   return sizeof(Tacc) * ((size_t)d * d + 3 * (size_t)C * (d + 1) + (size_t)C * (C + 1) + C + 1);
@@ -210,10 +182,8 @@ cudaError_t simt_pass_t(PassDesc p, void* ws, cudaStream_t st) {
     s.delta_out = delta;
     cudaError_t err = launch_simt<Tin, Acc, C, true>(s, st);
     if (err != cudaSuccess) return err;
-    dim3 grid((unsigned)((dd + kThreads - 1) / kThreads), bh);
-    segment_scan_kernel<Acc><<<grid, kThreads, 0, st>>>(delta, seg_in, p.state_in, p.state_in_T, nullptr, 0,
-                                                         p.lam, p.heads, p.d, p.n, p.seg_len, p.nseg, p.rev);
-    err = cudaGetLastError();
+    err = launch_segment_scan(sizeof(Acc) == 8, delta, seg_in, p.state_in, p.state_in_T, nullptr, 0, p.lam, bh,
+                              p.heads, p.d, p.n, p.seg_len, p.nseg, p.rev, st);
     if (err != cudaSuccess) return err;
     p.state_in = seg_in;
     p.state_in_T = 0;
@@ -240,11 +210,8 @@ cudaError_t simt_state_t(PassDesc p, void* ws, cudaStream_t st) {
   p.delta_out = delta;
   cudaError_t err = launch_simt<Tin, Acc, C, true>(p, st);
   if (err != cudaSuccess) return err;
-  dim3 grid((unsigned)((dd + kThreads - 1) / kThreads), bh);
-  segment_scan_kernel<Acc><<<grid, kThreads, 0, st>>>(delta, nullptr, nullptr, 0, reinterpret_cast<Acc*>(p.state_out),
-                                                       p.state_out_T, p.lam, p.heads, p.d, p.n, p.seg_len, p.nseg,
-                                                       p.rev);
-  return cudaGetLastError();
+  return launch_segment_scan(sizeof(Acc) == 8, delta, nullptr, nullptr, 0, p.state_out, p.state_out_T, p.lam, bh,
+                             p.heads, p.d, p.n, p.seg_len, p.nseg, p.rev, st);
 }
 
 }  // namespace

@@ -84,7 +84,8 @@ def _prep(tensors: Sequence[torch.Tensor], names: str, layout: str):
             raise ShapeError(f"{name}: shape {tuple(t.shape)} != {tuple(first.shape)}")
         if t.dtype != first.dtype or t.device != first.device:
             raise ShapeError(f"{name}: dtype/device {t.dtype}/{t.device} != {first.dtype}/{first.device}")
-    out = [t if t.is_contiguous() else t.contiguous() for t in tensors]
+    # contiguous, 16-byte aligned operands (TMA descriptors need aligned bases)
+    out = [t if (t.is_contiguous() and t.data_ptr() % 16 == 0) else t.contiguous().clone() for t in tensors]
     return out, _geometry(out[0], layout)
 
 
