@@ -13,6 +13,8 @@
 #include <cstring>
 #include <string>
 
+#include <cuda.h>
+
 #include "la_common.cuh"
 #include "la_simt.cuh"
 #include "la_tc.cuh"
@@ -32,7 +34,7 @@ int fail(int code, const char* fmt, ...) {
 }
 
 int cuda_fail(cudaError_t err, const char* where) {
-  return fail(LA_ERR_CUDA, "%s: %s (%s)", where, cudaGetErrorName(err), cudaGetErrorString(err));
+  return fail(LA_ERR_CUDA, "%s: %s (%s) %s", where, cudaGetErrorName(err), cudaGetErrorString(err), la::tc_detail());
 }
 
 int validate(const la_desc* desc) {
@@ -119,6 +121,35 @@ cudaError_t run_state(int backend, int dtype, const la::PassDesc& p, void* ws, c
   return la::simt_state(dtype, p, ws, st);
 }
 
+// This library carries its own (static) CUDA runtime.  A caller's thread may
+// have its device selected only through another runtime instance (e.g.
+// torch's autograd worker threads), so every entry binds the context that owns
+// the caller's stream before touching the runtime or the driver.
+template <typename F>
+F driver_fn(const char* name) {
+  void* p = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess)
+    return nullptr;
+  return reinterpret_cast<F>(p);
+}
+
+void bind_stream_context(cudaStream_t st) {
+  using GetCtx = CUresult (*)(CUstream, CUcontext*);
+  using CurCtx = CUresult (*)(CUcontext*);
+  using SetCtx = CUresult (*)(CUcontext);
+  static GetCtx get_ctx = driver_fn<GetCtx>("cuStreamGetCtx");
+  static CurCtx cur_ctx = driver_fn<CurCtx>("cuCtxGetCurrent");
+  static SetCtx set_ctx = driver_fn<SetCtx>("cuCtxSetCurrent");
+  if (!get_ctx || !cur_ctx || !set_ctx) return;
+  CUcontext want = nullptr, have = nullptr;
+  if (st != nullptr && get_ctx(reinterpret_cast<CUstream>(st), &want) == CUDA_SUCCESS && want != nullptr) {
+    if (cur_ctx(&have) == CUDA_SUCCESS && have != want) set_ctx(want);
+  } else if (cur_ctx(&have) == CUDA_SUCCESS && have == nullptr) {
+    cudaFree(nullptr);  // legacy stream and no context: initialise the runtime's current device
+  }
+}
+
 struct Prepared {
   int backend;
   la::Plan plan;
@@ -155,6 +186,7 @@ int la_fwd(const la_desc* desc, const void* q, const void* k, const void* v, con
   if (rc != LA_OK) return rc;
   if (!q || !k || !v || !o || !lam) return fail(LA_ERR_SHAPE, "la_fwd: null q/k/v/o/lam");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  bind_stream_context(st);
   la::PassDesc p = base_pass(desc, pr.plan, lam);
   p.a = q;
   p.b = k;
@@ -177,6 +209,7 @@ int la_bwd(const la_desc* desc, const void* q, const void* k, const void* v, con
   if (!q || !k || !v || !dout || !dq || !dk || !dv || !lam)
     return fail(LA_ERR_SHAPE, "la_bwd: null q/k/v/do/dq/dk/dv/lam");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  bind_stream_context(st);
   const la::PassDesc base = base_pass(desc, pr.plan, lam);
   cudaError_t err;
   // sweep 1 (kernels.py:309-318): dq = fwd(do, v, k), state kv^T
@@ -218,6 +251,7 @@ int la_fwd_state(const la_desc* desc, const void* k, const void* v, const double
   int rc = prepare(desc, workspace_bytes, workspace, &pr);
   if (rc != LA_OK) return rc;
   if (!k || !v || !lam || !kv_delta) return fail(LA_ERR_SHAPE, "la_fwd_state: null k/v/lam/kv_delta");
+  bind_stream_context(reinterpret_cast<cudaStream_t>(stream));
   la::PassDesc p = base_pass(desc, pr.plan, lam);
   p.b = k;
   p.c = v;
@@ -234,6 +268,7 @@ int la_bwd_state(const la_desc* desc, const void* q, const void* dout, const dou
   int rc = prepare(desc, workspace_bytes, workspace, &pr);
   if (rc != LA_OK) return rc;
   if (!q || !dout || !lam || !dkv_delta) return fail(LA_ERR_SHAPE, "la_bwd_state: null q/do/lam/dkv_delta");
+  bind_stream_context(reinterpret_cast<cudaStream_t>(stream));
   la::PassDesc p = base_pass(desc, pr.plan, lam);
   p.b = q;
   p.c = dout;

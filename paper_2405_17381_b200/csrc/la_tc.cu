@@ -2,28 +2,31 @@
 // swizzle) -> tcgen05.mma (fp32 accumulators in TMEM) -> tcgen05.ld epilogues.
 //
 // One CTA owns one (batch, head, segment) and walks its chunks of C = 128 rows
-// (fwd) or walks them backwards (rev), carrying the d x d state in fp32
-// REGISTERS of the state warpgroups and a bf16 copy of it in SMEM (the B
-// operand of the inter-chunk product).  Per chunk (la_common.cuh algebra):
+// (fwd) or walks them backwards (rev).  The d x d fp32 state lives in TMEM and
+// the tensor core accumulates each chunk's contribution straight into it; a
+// bf16 copy in SMEM is the B operand of the inter-chunk product.  Per chunk
+// (la_common.cuh algebra):
 //
-//   S      = A B^T                  tcgen05  M=128 N=128 K=128  -> TMEM [0,128)
-//   X      = A state                tcgen05  M=128 N=128 K=128  -> TMEM [256,384)
-//   P      = bf16(S * M_decay)      epilogue warps: tcgen05.ld, mask, -> SMEM (A's slot)
-//   Y      = P C                    tcgen05  A = P (SMEM)       -> TMEM [128,256)
-//   out    = Y + out_scale * X      epilogue warps -> SMEM (A's slot) -> TMA store
-//   B~     = in_scale * B           state warps, in place in SMEM after S consumed B
-//   dS     = B~^T C                 tcgen05  A MN-major         -> TMEM [384,512)
-//   state  = lam^b state + dS       state warps (fp32 registers) -> bf16 SMEM copy
+//   S     = A B^T                 SS-MMA  M=N=K=128              -> TMEM S[t%2]
+//   P     = bf16(S * M_decay)     P warps: tcgen05.ld S, mask, tcgen05.st -> TMEM (aliases S[t%2])
+//   A~    = bf16(out_scale * A)   P warps: SMEM rows -> TMEM (upper half of S[t%2])
+//   B~    = in_scale * B          state warps, in place in SMEM once S has consumed B
+//   state = lam^b state + B~^T C  state warps pre-scale the TMEM state, SS-MMA accumulates
+//   O     = A~ state_bf16 + P C   TS-MMAs (A operands from TMEM)  -> TMEM O
+//   out   = bf16(O)               output warps: tcgen05.ld -> registers -> global
 //
-// Warp roles (14 warps): 0 TMA producer, 1 MMA issuer (+ TMEM owner),
-// 2-5 score/output epilogue (one TMEM lane quadrant each), 6-13 state update
-// (two warpgroups, 64 state columns each).  Everything is chained with
-// mbarriers; the only CTA-wide barriers are at setup and teardown.
+// Warp roles (26 warps): 0 TMA producer, 1 MMA issuer (+ TMEM owner), 2-9 P/A~
+// conversion, 10-17 output, 18-25 state -- each group two warps per TMEM lane
+// quadrant, each warp owning 64 of the 128 columns.  Every hand-off is an mbarrier; a stage is
+// handed back to the TMA producer by the tensor core's own commit after its
+// last MMA, and the MMA issuer runs one chunk ahead on S so the score
+// conversion of chunk t+1 overlaps the products of chunk t.
 //
 // Shared memory: 2 stages x {A, B, C} tiles (3 x 32 KB) + the bf16 state
-// (32 KB) = 224 KB -> one CTA per SM.  TMEM: all 512 columns.
+// (32 KB) = 224 KB -> one CTA per SM.  TMEM: S0 | S1 | O | state = 512 columns.
 #include <cudaTypedefs.h>
 
+#include <cstdio>
 #include <cstring>
 
 #include "la_common.cuh"
@@ -37,42 +40,59 @@ namespace {
 
 using namespace ptx;
 
-constexpr int C = 128;                  // chunk rows
-constexpr int D = 128;                  // head dim (only d == 128 on this backend)
-constexpr int TILE = C * D * 2;         // 32 KB bf16 tile
-constexpr int HALF = TILE / 2;          // [128 rows][64 cols] = 16 KB, one 128B-swizzle column block
+#ifdef LA_TRACE
+// debug build only: cycle stamps of pipeline events of CTA (0, 0), [chunk][event]
+__device__ unsigned long long* g_la_trace = nullptr;
+#define LA_TR(t, ev)                                                             \
+  do {                                                                           \
+    if (g_la_trace != nullptr && blockIdx.x == 0 && blockIdx.y == 0 && (t) < 32) \
+      g_la_trace[(t) * 16 + (ev)] = clock64();                                   \
+  } while (0)
+#else
+#define LA_TR(t, ev) \
+  do {               \
+  } while (0)
+#endif
+
+constexpr int C = 128;           // chunk rows
+constexpr int D = 128;           // head dim (only d == 128 on this backend)
+constexpr int TILE = C * D * 2;  // 32 KB bf16 tile
+constexpr int HALF = TILE / 2;   // [128 rows][64 cols] = 16 KB, one 128B-swizzle column block
 constexpr int NSTAGE = 2;
-constexpr int NUM_WARPS = 14;
+constexpr int WARP_TMA = 0, WARP_MMA = 1, WARP_P = 2, NUM_P = 8, WARP_O = 10, NUM_O = 8, WARP_KV = 18, NUM_KV = 8;
+constexpr int NUM_WARPS = WARP_KV + NUM_KV;
 constexpr int NUM_THREADS = NUM_WARPS * 32;
-constexpr int WARP_TMA = 0, WARP_MMA = 1, WARP_SO = 2, WARP_KV = 6;
-constexpr uint32_t TM_S = 0, TM_Y = 128, TM_X = 256, TM_DS = 384, TM_COLS = 512;
+constexpr uint32_t TM_S0 = 0, TM_O = 256, TM_ST = 384, TM_COLS = 512;
 
 // kind::f16 instruction descriptors (M = N = 128)
 constexpr uint32_t IDESC_KK = idesc_bf16(128, 128, 0, 0);    // A K-major, B K-major
-constexpr uint32_t IDESC_KMN = idesc_bf16(128, 128, 0, 1);   // A K-major, B MN-major
+constexpr uint32_t IDESC_KMN = idesc_bf16(128, 128, 0, 1);   // A K-major (or TMEM), B MN-major
 constexpr uint32_t IDESC_MNMN = idesc_bf16(128, 128, 1, 1);  // A MN-major, B MN-major
 
 struct Bars {
-  uint64_t full[NSTAGE];   // TMA -> MMA        (tx bytes)
-  uint64_t empty[NSTAGE];  // MMA commit (+ output store) -> TMA
-  uint64_t s_full;         // MMA: S and X done -> epilogue + state warps
-  uint64_t s_free;         // epilogue read S   -> MMA
-  uint64_t p_full;         // P in SMEM         -> MMA
-  uint64_t y_full;         // MMA: Y done       -> epilogue
-  uint64_t o_free;         // epilogue read Y,X -> MMA
-  uint64_t b_scaled;       // B~ in SMEM        -> MMA
-  uint64_t ds_full;        // MMA: dS done      -> state warps
-  uint64_t ds_free;        // state warps read dS -> MMA
-  uint64_t st_ready;       // bf16 state in SMEM -> MMA
+  uint64_t full[NSTAGE];   // TMA -> MMA                       (tx bytes)
+  uint64_t empty[NSTAGE];  // MMA commit after the stage's last MMA -> TMA
+  uint64_t s_full[2];      // MMA: S[t%2] done                 -> P warps, state warps
+  uint64_t a_full[2];      // A~(t) in TMEM                    -> MMA (per buffer: P warps run a chunk ahead)
+  uint64_t p_full[2];      // P(t) in TMEM                     -> MMA
+  uint64_t x_done;         // MMA: X(t) = A~ state_bf16 done   -> state warps (SMEM state copy reusable)
+  uint64_t y_done[2];      // MMA: O(t) done, per S buffer     -> MMA (before S(t+2) reuses the buffer)
+  uint64_t o_full;         // MMA: O done                      -> output warps
+  uint64_t o_free;         // output warps read O              -> MMA
+  uint64_t b_scaled;       // B~ in SMEM                       -> MMA
+  uint64_t ds_full;        // MMA: state += B~^T C done        -> state warps
+  uint64_t st_ready;       // bf16 state in SMEM, TMEM state pre-scaled -> MMA
   uint32_t tmem_base;
 };
 
 constexpr size_t SMEM_TILES = (size_t)NSTAGE * 3 * TILE + TILE;  // 224 KB
-constexpr size_t SMEM_BYTES = SMEM_TILES + 1024 /*bars*/ + 1024 /*pw*/ + 1024 /*align slack*/;
+constexpr size_t SMEM_BYTES = SMEM_TILES + 1024 /*align slack*/;
 
 struct TcArgs {
   int heads, n, seg_len, nseg, rev;
   const double* lam;
+  uint16_t* out;  // bf16 output (full mode)
+  int64_t sb, sh, sn;
   const float* state_in;
   int64_t in_bh_stride, in_seg_stride;
   int in_T;
@@ -84,19 +104,24 @@ struct TcArgs {
 // byte offset of 16-byte chunk `c` (0..7) of row `r` inside a [128][64] bf16 block, 128B swizzle
 __device__ __forceinline__ uint32_t sw128(int r, int c) { return (uint32_t)(r * 128 + ((c ^ (r & 7)) << 4)); }
 
+__device__ __forceinline__ void stg128(void* p, uint4 v) {
+  asm volatile("st.global.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+
 template <bool STATE_ONLY>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     tc_pass_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
-                   const __grid_constant__ CUtensorMap map_c, const __grid_constant__ CUtensorMap map_o,
-                   const TcArgs args) {
+                   const __grid_constant__ CUtensorMap map_c, const TcArgs args) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  auto tile_a = [smem](int s) { return smem + (size_t)s * 3 * TILE; };
-  auto tile_b = [smem](int s) { return smem + (size_t)s * 3 * TILE + TILE; };
-  auto tile_c = [smem](int s) { return smem + (size_t)s * 3 * TILE + 2 * TILE; };
-  uint8_t* st_bf16 = smem + (size_t)NSTAGE * 3 * TILE;
-  Bars* bars = reinterpret_cast<Bars*>(smem + SMEM_TILES);
-  float* pw = reinterpret_cast<float*>(smem + SMEM_TILES + 1024);  // lam^0 .. lam^128
+  __shared__ Bars bars;
+  __shared__ __align__(16) float pw[C + 8];  // lam^0 .. lam^128
+  const uint32_t smem = (smem_u32(smem_raw) + 1023u) & ~1023u;
+  uint8_t* smem_gen = smem_raw + (smem - smem_u32(smem_raw));
+  auto tile_a = [smem](int s) { return smem + (uint32_t)(s * 3 * TILE); };
+  auto tile_b = [smem](int s) { return smem + (uint32_t)(s * 3 * TILE + TILE); };
+  auto tile_c = [smem](int s) { return smem + (uint32_t)(s * 3 * TILE + 2 * TILE); };
+  const uint32_t st_bf16 = smem + (uint32_t)(NSTAGE * 3 * TILE);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int seg = blockIdx.x, bh = blockIdx.y;
@@ -108,18 +133,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < NSTAGE; ++s) {
-      mbar_init(&bars->full[s], 1);
-      mbar_init(&bars->empty[s], STATE_ONLY ? 1 : 2);
+      mbar_init(&bars.full[s], 1);
+      mbar_init(&bars.empty[s], 1);
+      mbar_init(&bars.s_full[s], 1);
+      mbar_init(&bars.p_full[s], NUM_P);
+      mbar_init(&bars.a_full[s], NUM_P);
+      mbar_init(&bars.y_done[s], 1);
     }
-    mbar_init(&bars->s_full, 1);
-    mbar_init(&bars->s_free, 4);
-    mbar_init(&bars->p_full, 4);
-    mbar_init(&bars->y_full, 1);
-    mbar_init(&bars->o_free, 4);
-    mbar_init(&bars->b_scaled, 8);
-    mbar_init(&bars->ds_full, 1);
-    mbar_init(&bars->ds_free, 8);
-    mbar_init(&bars->st_ready, 8);
+    mbar_init(&bars.o_full, 1);
+    mbar_init(&bars.o_free, NUM_O);
+    mbar_init(&bars.b_scaled, NUM_KV);
+    mbar_init(&bars.ds_full, 1);
+    mbar_init(&bars.x_done, 1);
+    mbar_init(&bars.st_ready, NUM_KV);
     fence_mbar_init();
     double x = 1.0;
     const double lam = args.lam[hi];
@@ -131,18 +157,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if (warp == WARP_TMA && lane == 0) {
     tma_prefetch(&map_b);
     tma_prefetch(&map_c);
-    if (!STATE_ONLY) {
-      tma_prefetch(&map_a);
-      tma_prefetch(&map_o);
-    }
+    if (!STATE_ONLY) tma_prefetch(&map_a);
   }
-  if (warp == WARP_MMA) tmem_alloc(&bars->tmem_base, TM_COLS);
+  if (warp == WARP_MMA) tmem_alloc(&bars.tmem_base, TM_COLS);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = bars->tmem_base;
+  const uint32_t tmem = bars.tmem_base;
 
   auto chunk_row0 = [&](int t) { return p0 + (rev ? (nchunks - 1 - t) : t) * C; };
+  auto chunk_len = [&](int t) { return min(C, p1 - chunk_row0(t)); };
 
   if (warp == WARP_TMA) {
     // ------------------------------------------------------------ TMA producer
@@ -150,242 +174,359 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const uint32_t bytes = (STATE_ONLY ? 2 : 3) * TILE;
       for (int t = 0; t < nchunks; ++t) {
         const int s = t % NSTAGE;
-        if (t >= NSTAGE) mbar_wait(&bars->empty[s], ((t / NSTAGE) - 1) & 1);
+        if (t >= NSTAGE) mbar_wait(&bars.empty[s], ((t / NSTAGE) - 1) & 1);
         const int r0 = chunk_row0(t);
-        mbar_arrive_expect_tx(&bars->full[s], bytes);
+        mbar_arrive_expect_tx(&bars.full[s], bytes);
+        LA_TR(t, 0);
+        uint8_t* ga = smem_gen + s * 3 * TILE;
         for (int hf = 0; hf < 2; ++hf) {
-          if (!STATE_ONLY) tma_load_4d(&map_a, &bars->full[s], tile_a(s) + hf * HALF, hf * 64, r0, hi, bi);
-          tma_load_4d(&map_b, &bars->full[s], tile_b(s) + hf * HALF, hf * 64, r0, hi, bi);
-          tma_load_4d(&map_c, &bars->full[s], tile_c(s) + hf * HALF, hf * 64, r0, hi, bi);
+          if (!STATE_ONLY) tma_load_4d(&map_a, &bars.full[s], ga + hf * HALF, hf * 64, r0, hi, bi);
+          tma_load_4d(&map_b, &bars.full[s], ga + TILE + hf * HALF, hf * 64, r0, hi, bi);
+          tma_load_4d(&map_c, &bars.full[s], ga + 2 * TILE + hf * HALF, hf * 64, r0, hi, bi);
         }
       }
     }
   } else if (warp == WARP_MMA) {
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0) {
-      const uint32_t st_addr = smem_u32(st_bf16);
+      auto issue_s = [&](int t) {  // S[t%2] = A B^T  (both K-major)
+        const int s = t % NSTAGE;
+        const uint32_t a_addr = tile_a(s), b_addr = tile_b(s);
+        mbar_wait(&bars.full[s], (t / NSTAGE) & 1);
+        // S[t%2] overwrites the TMEM columns P(t-2) / A~(t-2) were read from: those TS-MMAs must have
+        // retired (in-order issue alone does not order a TMEM A-operand read before a later D write)
+        if (t >= 2) mbar_wait(&bars.y_done[t & 1], ((t - 2) >> 1) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * HALF + (kk & 3) * 32;
+          mma_bf16_ss(tmem + TM_S0 + (t & 1) * 128, smem_desc_sw128(a_addr + off, 0, 1024),
+                      smem_desc_sw128(b_addr + off, 0, 1024), IDESC_KK, kk > 0);
+        }
+        mma_commit(&bars.s_full[t & 1]);
+        LA_TR(t, 1);
+      };
+      int s_issued = 0;  // S issued for chunks < s_issued
+      if (!STATE_ONLY && nchunks > 0) {
+        issue_s(0);
+        s_issued = 1;
+      }
       for (int t = 0; t < nchunks; ++t) {
         const int s = t % NSTAGE;
-        const uint32_t a_addr = smem_u32(tile_a(s)), b_addr = smem_u32(tile_b(s)), c_addr = smem_u32(tile_c(s));
-        mbar_wait(&bars->full[s], (t / NSTAGE) & 1);
+        const uint32_t b_addr = tile_b(s), c_addr = tile_c(s);
+        const uint32_t sbuf = tmem + TM_S0 + (t & 1) * 128;
+        if (!STATE_ONLY && s_issued == t + 1 && t + 1 < nchunks &&
+            mbar_try_wait(smem_u32(&bars.full[(t + 1) % NSTAGE]), ((t + 1) / NSTAGE) & 1)) {
+          issue_s(t + 1);  // run ahead: S(t+1) as soon as its operands landed
+          s_issued = t + 2;
+        }
+        if (STATE_ONLY) mbar_wait(&bars.full[s], (t / NSTAGE) & 1);
+        // st_ready(t): bf16 state_{t-1} in SMEM and the TMEM state pre-scaled by lam^b
+        mbar_wait(&bars.st_ready, t & 1);
         if (!STATE_ONLY) {
-          if (t >= 1) {
-            mbar_wait(&bars->s_free, (t - 1) & 1);
-            mbar_wait(&bars->o_free, (t - 1) & 1);
-          }
-          mbar_wait(&bars->st_ready, t & 1);
+          // X(t) = A~ state_{t-1}  -> O (fresh accumulation)
+          if (t >= 1) mbar_wait(&bars.o_free, (t - 1) & 1);
+          mbar_wait(&bars.a_full[t & 1], (t >> 1) & 1);
+          LA_TR(t, 15);
           tc_fence_after();
-          // S = A B^T: A [rows][d] K-major, B [rows][d] K-major
 #pragma unroll
-          for (int kk = 0; kk < D / 16; ++kk) {
-            const uint32_t off = (kk >> 2) * HALF + (kk & 3) * 32;
-            mma_bf16_ss(tmem + TM_S, smem_desc_sw128(a_addr + off, 0, 1024), smem_desc_sw128(b_addr + off, 0, 1024),
-                        IDESC_KK, kk > 0);
-          }
-          // X = A state: state bf16 [d_k][d_v] row-major == B operand MN-major (N = d_v contiguous)
+          for (int kk = 0; kk < D / 16; ++kk)
+            mma_bf16_ts(tmem + TM_O, sbuf + 64 + kk * 8, smem_desc_sw128(st_bf16 + kk * 2048, HALF, 1024),
+                        IDESC_KMN, kk > 0);
+          mma_commit(&bars.x_done);
+        }
+        // state += B~^T C
+        mbar_wait(&bars.b_scaled, t & 1);
+        LA_TR(t, 4);
+        tc_fence_after();
 #pragma unroll
-          for (int kk = 0; kk < D / 16; ++kk) {
-            const uint32_t aoff = (kk >> 2) * HALF + (kk & 3) * 32;
-            mma_bf16_ss(tmem + TM_X, smem_desc_sw128(a_addr + aoff, 0, 1024),
-                        smem_desc_sw128(st_addr + kk * 2048, HALF, 1024), IDESC_KMN, kk > 0);
-          }
-          mma_commit(&bars->s_full);
-          // Y = P C: P (in A's slot) [rows][keys] K-major, C [keys][d] MN-major
-          mbar_wait(&bars->p_full, t & 1);
+        for (int kk = 0; kk < C / 16; ++kk)
+          mma_bf16_ss(tmem + TM_ST, smem_desc_sw128(b_addr + kk * 2048, HALF, 1024),
+                      smem_desc_sw128(c_addr + kk * 2048, HALF, 1024), IDESC_MNMN, 1);
+        mma_commit(&bars.ds_full);
+        LA_TR(t, 5);
+        if (!STATE_ONLY) {
+          // Y(t) = P C  -> O (accumulate)
+          mbar_wait(&bars.p_full[t & 1], (t >> 1) & 1);
+          LA_TR(t, 2);
           tc_fence_after();
 #pragma unroll
           for (int kk = 0; kk < C / 16; ++kk) {
-            const uint32_t aoff = (kk >> 2) * HALF + (kk & 3) * 32;
-            mma_bf16_ss(tmem + TM_Y, smem_desc_sw128(a_addr + aoff, 0, 1024),
-                        smem_desc_sw128(c_addr + kk * 2048, HALF, 1024), IDESC_KMN, kk > 0);
+            // key block cb = kk / 2 lives at column 32 (cb & 1) + 16 (cb >> 1) (see the P warps)
+            const int cb = kk >> 1;
+            const uint32_t pcol = 32 * (cb & 1) + 16 * (cb >> 1) + 8 * (kk & 1);
+            mma_bf16_ts(tmem + TM_O, sbuf + pcol, smem_desc_sw128(c_addr + kk * 2048, HALF, 1024), IDESC_KMN, 1);
           }
-          mma_commit(&bars->y_full);
+          mma_commit(&bars.o_full);
+          mma_commit(&bars.y_done[t & 1]);
+          LA_TR(t, 3);
         }
-        // dS = B~^T C: A = B~^T (M = d_k contiguous -> MN-major), B = C MN-major
-        mbar_wait(&bars->b_scaled, t & 1);
-        if (t >= 1) mbar_wait(&bars->ds_free, (t - 1) & 1);
+        mma_commit(&bars.empty[s]);  // the stage's last reader was just issued
+        if (!STATE_ONLY && s_issued == t + 1 && t + 1 < nchunks) {
+          issue_s(t + 1);
+          s_issued = t + 2;
+        }
+      }
+      // Drain: every asynchronous tcgen05.commit arrival must land before this CTA retires, or it
+      // would hit the barriers of the next CTA scheduled onto this SM's shared memory.
+      for (int t = max(0, nchunks - NSTAGE); t < nchunks; ++t) {
+        mbar_wait(&bars.empty[t % NSTAGE], (t / NSTAGE) & 1);
+        if (!STATE_ONLY) mbar_wait(&bars.y_done[t & 1], (t >> 1) & 1);
+      }
+    }
+  } else if (warp < WARP_O) {
+    // ------------------------------------------------------------ A~ / P conversion (warps 2..9)
+    if (!STATE_ONLY) {
+      const int quad = warp & 3;
+      const int half = (warp - WARP_P) >> 2;  // A~ columns [64 half, +64); key blocks {half, half + 2}
+      const int i = quad * 32 + lane;         // chunk row == TMEM lane
+      const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
+      const uint32_t pw_addr = smem_u32(pw);
+      for (int t = 0; t < nchunks; ++t) {
+        const int s = t % NSTAGE;
+        const int b = chunk_len(t);
+        const uint32_t sbuf = tmem + lane_off + TM_S0 + (t & 1) * 128;
+        mbar_wait(&bars.s_full[t & 1], (t >> 1) & 1);
+        if (warp == WARP_P && lane == 0) LA_TR(t, 6);
         tc_fence_after();
+        // P = bf16(S * M): fwd keeps j <= i with lam^(i-j), rev keeps j >= i with lam^(j-i).
+        // A block of 32 keys is all-zero / all-kept / diagonal depending on the warp's quadrant.
+        auto convert_block = [&](int cb, uint32_t (&pk)[16]) {
+          const bool zero = rev ? (cb < quad) : (cb > quad);
+          if (zero) {
 #pragma unroll
-        for (int kk = 0; kk < C / 16; ++kk) {
-          mma_bf16_ss(tmem + TM_DS, smem_desc_sw128(b_addr + kk * 2048, HALF, 1024),
-                      smem_desc_sw128(c_addr + kk * 2048, HALF, 1024), IDESC_MNMN, kk > 0);
+            for (int e = 0; e < 16; ++e) pk[e] = 0u;
+          } else if (cb != quad) {
+            // off-diagonal: lam^|i-j| = lam^(|i - block edge|) * lam^(distance within the block);
+            // both factors are >= the product, so no spurious underflow
+            float v[32];
+            tmem_ld32(sbuf + cb * 32, v);
+            const float base = rev ? pw[cb * 32 - i] : pw[i - cb * 32 - 31];
+            tmem_ld_wait();
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              // w = lam^(31 - jj) (fwd) or lam^jj (rev) for jj = 4q .. 4q+3: one broadcast LDS.128
+              const uint4 wq = lds128(pw_addr + 4 * (rev ? 4 * q : 28 - 4 * q));
+              float w0 = __uint_as_float(wq.x), w1 = __uint_as_float(wq.y), w2 = __uint_as_float(wq.z),
+                    w3 = __uint_as_float(wq.w);
+              if (!rev) {  // fwd wants descending powers
+                const float t0 = w0, t1 = w1;
+                w0 = w3;
+                w1 = w2;
+                w2 = t1;
+                w3 = t0;
+              }
+              pk[2 * q] = pack_bf16x2(v[4 * q] * (base * w0), v[4 * q + 1] * (base * w1));
+              pk[2 * q + 1] = pack_bf16x2(v[4 * q + 2] * (base * w2), v[4 * q + 3] * (base * w3));
+            }
+          } else {
+            float v[32];
+            tmem_ld32(sbuf + cb * 32, v);
+            tmem_ld_wait();
+#pragma unroll
+            for (int jj = 0; jj < 32; jj += 2) {
+              const int j0 = cb * 32 + jj, j1 = j0 + 1;
+              const int d0 = rev ? (j0 - i) : (i - j0);
+              const int d1 = rev ? (j1 - i) : (i - j1);
+              pk[jj >> 1] = pack_bf16x2(d0 >= 0 ? v[jj] * pw[max(d0, 0)] : 0.f,
+                                        d1 >= 0 ? v[jj + 1] * pw[max(d1, 0)] : 0.f);
+            }
+          }
+        };
+        // TMEM columns of the buffer: S block cb sits at [32 cb, +32).  Warp `half` reads S blocks half
+        // and half + 2 and only ever overwrites those: its A~ goes to [64 + 32 half, +32) (= S block
+        // half + 2, read first) and its two P blocks to [32 half, +32) (= S block half): P(half) at
+        // 32 half, P(half + 2) at 32 half + 16.  The MMA addresses P per key block accordingly.
+        uint32_t p_hi[16];
+        convert_block(half + 2, p_hi);
+        // A~ = bf16(out_scale * A): fwd lam^(i+1), rev lam^(b-1-i); this warp's 64 columns
+        {
+          const float osc = rev ? pw[max(b - 1 - i, 0)] : pw[i + 1];
+          const uint32_t osc2 = pack_bf16x2(osc, osc);
+          const uint32_t a_addr = tile_a(s) + half * HALF;
+#pragma unroll
+          for (int part = 0; part < 2; ++part) {
+            uint32_t pk[16];
+#pragma unroll
+            for (int m = 0; m < 4; ++m) {
+              const uint4 x = mul_bf16x2(lds128(a_addr + sw128(i, part * 4 + m)), osc2);
+              pk[4 * m + 0] = x.x;
+              pk[4 * m + 1] = x.y;
+              pk[4 * m + 2] = x.z;
+              pk[4 * m + 3] = x.w;
+            }
+            tmem_st16(sbuf + 64 + half * 32 + part * 16, pk);
+          }
+          tmem_st_wait();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&bars.a_full[t & 1]);
         }
-        mma_commit(&bars->ds_full);
-        mma_commit(&bars->empty[s]);
+        {
+          uint32_t p_lo[16];
+          convert_block(half, p_lo);
+          tmem_st16(sbuf + 32 * half, p_lo);
+          tmem_st16(sbuf + 32 * half + 16, p_hi);
+        }
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bars.p_full[t & 1]);
+        if (warp == WARP_P && lane == 0) LA_TR(t, 7);
       }
     }
   } else if (warp < WARP_KV) {
-    // ------------------------------------------------------------ score / output epilogue (warps 2..5)
+    // ------------------------------------------------------------ output (warps 10..17)
     if (!STATE_ONLY) {
       const int quad = warp & 3;
-      const int i = quad * 32 + lane;  // row within the chunk == TMEM lane
-      const uint32_t lane_addr = tmem + ((uint32_t)(quad * 32) << 16);
+      const int half = (warp - WARP_O) >> 2;  // output columns [64 half, +64)
+      const int i = quad * 32 + lane;
+      const uint32_t o_cols = tmem + ((uint32_t)(quad * 32) << 16) + TM_O + half * 64;
       for (int t = 0; t < nchunks; ++t) {
-        const int s = t % NSTAGE;
         const int r0 = chunk_row0(t);
-        const int b = min(C, p1 - r0);
-        uint8_t* slot = tile_a(s);
-        mbar_wait(&bars->s_full, t & 1);
+        const bool valid = i < chunk_len(t);
+        uint16_t* dst =
+            args.out + (int64_t)bi * args.sb + (int64_t)hi * args.sh + (int64_t)(r0 + i) * args.sn + half * 64;
+        mbar_wait(&bars.o_full, t & 1);
+        if (warp == WARP_O && lane == 0) LA_TR(t, 8);
         tc_fence_after();
-        // P = bf16(S * M): fwd keeps j <= i with lam^(i-j); rev keeps j >= i with lam^(j-i)
-#pragma unroll 1
-        for (int cb = 0; cb < 4; ++cb) {
-          float v[32];
-          tmem_ld32(lane_addr + TM_S + cb * 32, v);
+        uint32_t pk[32];
+#pragma unroll
+        for (int cb = 0; cb < 2; ++cb) {
+          float y[32];
+          tmem_ld32(o_cols + cb * 32, y);
           tmem_ld_wait();
-          uint32_t pk[16];
 #pragma unroll
-          for (int jj = 0; jj < 32; jj += 2) {
-            const int j0 = cb * 32 + jj, j1 = j0 + 1;
-            const int d0 = rev ? (j0 - i) : (i - j0);
-            const int d1 = rev ? (j1 - i) : (i - j1);
-            const float x0 = d0 >= 0 ? v[jj] * pw[d0] : 0.f;
-            const float x1 = d1 >= 0 ? v[jj + 1] * pw[d1] : 0.f;
-            pk[jj >> 1] = pack_bf16x2(x0, x1);
-          }
-          uint8_t* base = slot + (cb >> 1) * HALF;
-#pragma unroll
-          for (int m = 0; m < 4; ++m) {
-            const int c16 = (cb & 1) * 4 + m;
-            *reinterpret_cast<uint4*>(base + sw128(i, c16)) = make_uint4(pk[4 * m], pk[4 * m + 1], pk[4 * m + 2],
-                                                                         pk[4 * m + 3]);
-          }
+          for (int e = 0; e < 16; ++e) pk[cb * 16 + e] = pack_bf16x2(y[2 * e], y[2 * e + 1]);
         }
         tc_fence_before();
-        fence_proxy_async_smem();
         __syncwarp();
-        if (lane == 0) {
-          mbar_arrive(&bars->s_free);
-          mbar_arrive(&bars->p_full);
-        }
-        // out = Y + out_scale * X  -> bf16 into the same slot -> TMA store
-        mbar_wait(&bars->y_full, t & 1);
-        tc_fence_after();
-        const float osc = rev ? pw[max(b - 1 - i, 0)] : pw[i + 1];
-#pragma unroll 1
-        for (int cb = 0; cb < 4; ++cb) {
-          float y[32], x[32];
-          tmem_ld32(lane_addr + TM_Y + cb * 32, y);
-          tmem_ld32(lane_addr + TM_X + cb * 32, x);
-          tmem_ld_wait();
-          uint32_t pk[16];
+        if (lane == 0) mbar_arrive(&bars.o_free);  // O's TMEM is free; the stores proceed from registers
+        if (valid) {
 #pragma unroll
-          for (int jj = 0; jj < 32; jj += 2)
-            pk[jj >> 1] = pack_bf16x2(fmaf(osc, x[jj], y[jj]), fmaf(osc, x[jj + 1], y[jj + 1]));
-          uint8_t* base = slot + (cb >> 1) * HALF;
-#pragma unroll
-          for (int m = 0; m < 4; ++m) {
-            const int c16 = (cb & 1) * 4 + m;
-            *reinterpret_cast<uint4*>(base + sw128(i, c16)) = make_uint4(pk[4 * m], pk[4 * m + 1], pk[4 * m + 2],
-                                                                         pk[4 * m + 3]);
-          }
+          for (int m = 0; m < 8; ++m)
+            stg128(dst + m * 8, make_uint4(pk[4 * m], pk[4 * m + 1], pk[4 * m + 2], pk[4 * m + 3]));
         }
-        tc_fence_before();
-        fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&bars->o_free);
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (warp == WARP_SO && lane == 0) {
-          tma_store_4d(&map_o, slot, 0, r0, hi, bi);
-          tma_store_4d(&map_o, slot + HALF, 64, r0, hi, bi);
-          tma_store_commit();
-          tma_store_wait_read();
-          mbar_arrive(&bars->empty[s]);
-        }
+        if (warp == WARP_O && lane == 0) LA_TR(t, 9);
       }
-      if (warp == WARP_SO && lane == 0) tma_store_wait_all();
     }
   } else {
-    // ------------------------------------------------------------ state update (warps 6..13)
+    // ------------------------------------------------------------ state (warps 18..25)
     const int quad = warp & 3;
     const int hh = (warp - WARP_KV) >> 2;  // which 64 state columns
     const int i = quad * 32 + lane;        // state row (d_k index) == TMEM lane
-    const uint32_t lane_addr = tmem + ((uint32_t)(quad * 32) << 16);
-    float kv[64];
-    if (!STATE_ONLY && args.state_in != nullptr) {
-      const float* src = args.state_in + (int64_t)bh * args.in_bh_stride + (int64_t)seg * args.in_seg_stride;
-#pragma unroll
-      for (int j = 0; j < 64; ++j) {
-        const int col = hh * 64 + j;
-        kv[j] = args.in_T ? src[col * D + i] : src[i * D + col];
+    const uint32_t st_cols = tmem + ((uint32_t)(quad * 32) << 16) + TM_ST + hh * 64;
+    // publish bf16(state) to SMEM (unless state-only) and pre-scale the TMEM state by `next_decay`
+    auto publish = [&](const float (&x)[16], int q4, float next_decay) {
+      if (!STATE_ONLY) {
+        const uint32_t base = st_bf16 + hh * HALF;
+        sts128(base + sw128(i, 2 * q4),
+               make_uint4(pack_bf16x2(x[0], x[1]), pack_bf16x2(x[2], x[3]), pack_bf16x2(x[4], x[5]),
+                          pack_bf16x2(x[6], x[7])));
+        sts128(base + sw128(i, 2 * q4 + 1),
+               make_uint4(pack_bf16x2(x[8], x[9]), pack_bf16x2(x[10], x[11]), pack_bf16x2(x[12], x[13]),
+                          pack_bf16x2(x[14], x[15])));
       }
-    } else {
+      uint32_t w[16];
 #pragma unroll
-      for (int j = 0; j < 64; ++j) kv[j] = 0.f;
-    }
-    auto publish_state = [&]() {
-      uint8_t* base = st_bf16 + hh * HALF;
-#pragma unroll
-      for (int m = 0; m < 8; ++m) {
-        const uint4 w = make_uint4(pack_bf16x2(kv[8 * m], kv[8 * m + 1]), pack_bf16x2(kv[8 * m + 2], kv[8 * m + 3]),
-                                   pack_bf16x2(kv[8 * m + 4], kv[8 * m + 5]), pack_bf16x2(kv[8 * m + 6], kv[8 * m + 7]));
-        *reinterpret_cast<uint4*>(base + sw128(i, m)) = w;
-      }
-      fence_proxy_async_smem();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&bars->st_ready);
+      for (int j = 0; j < 16; ++j) w[j] = __float_as_uint(x[j] * next_decay);
+      tmem_st16(st_cols + q4 * 16, w);
     };
-    if (!STATE_ONLY) publish_state();
+    auto signal_ready = [&]() {
+      tmem_st_wait();
+      tc_fence_before();
+      if (!STATE_ONLY) fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars.st_ready);
+    };
+    if (nchunks > 0) {
+      const float d0 = pw[chunk_len(0)];
+#pragma unroll 1
+      for (int q4 = 0; q4 < 4; ++q4) {
+        float x[16];
+        if (!STATE_ONLY && args.state_in != nullptr) {
+          const float* src = args.state_in + (int64_t)bh * args.in_bh_stride + (int64_t)seg * args.in_seg_stride;
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const int col = hh * 64 + q4 * 16 + j;
+            x[j] = args.in_T ? src[col * D + i] : src[i * D + col];
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) x[j] = 0.f;
+        }
+        publish(x, q4, d0);
+      }
+      signal_ready();
+    }
     for (int t = 0; t < nchunks; ++t) {
       const int s = t % NSTAGE;
-      const int r0 = chunk_row0(t);
-      const int b = min(C, p1 - r0);
+      const int b = chunk_len(t);
       if (STATE_ONLY)
-        mbar_wait(&bars->full[s], (t / NSTAGE) & 1);
+        mbar_wait(&bars.full[s], (t / NSTAGE) & 1);
       else
-        mbar_wait(&bars->s_full, t & 1);
-      // B~ = in_scale * B, in place (row i, this warp's 64 columns): fwd lam^(b-1-i), rev lam^(i+1)
+        mbar_wait(&bars.s_full[t & 1], (t >> 1) & 1);
+      if (warp == WARP_KV && lane == 0) LA_TR(t, 11);
+      // B~ = in_scale * B, in place (row i, this warpgroup's 64 columns): fwd lam^(b-1-i), rev lam^(i+1).
+      // Row scaling is order-free, so visit the row's 16-byte chunks in swizzled order: lane i touches
+      // physical chunk m ^ (i & 7), spreading a warp over all 32 banks (4 wavefronts / 512 B).
       {
         const float isc = (i < b) ? (rev ? pw[i + 1] : pw[b - 1 - i]) : 0.f;
-        uint8_t* base = tile_b(s) + hh * HALF;
+        const uint32_t isc2 = pack_bf16x2(isc, isc);
+        const uint32_t base = tile_b(s) + hh * HALF + i * 128;
+        uint4 x[8];
 #pragma unroll
-        for (int m = 0; m < 8; ++m) {
-          uint4* p = reinterpret_cast<uint4*>(base + i * 128 + m * 16);  // row-local chunks: swizzle irrelevant
-          uint4 w = *p;
-          uint32_t* u = reinterpret_cast<uint32_t*>(&w);
+        for (int m = 0; m < 8; ++m) x[m] = lds128(base + ((m ^ (i & 7)) << 4));
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float lo = __uint_as_float(u[e] << 16) * isc;
-            const float hi2 = __uint_as_float(u[e] & 0xFFFF0000u) * isc;
-            u[e] = pack_bf16x2(lo, hi2);
-          }
-          *p = w;
-        }
+        for (int m = 0; m < 8; ++m) sts128(base + ((m ^ (i & 7)) << 4), mul_bf16x2(x[m], isc2));
       }
       fence_proxy_async_smem();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&bars->b_scaled);
-      // state = lam^b state + dS
-      mbar_wait(&bars->ds_full, t & 1);
+      if (lane == 0) mbar_arrive(&bars.b_scaled);
+      if (warp == WARP_KV && lane == 0) LA_TR(t, 12);
+      // the tensor core accumulated this chunk: read the state, publish it for chunk t+1 once X(t)
+      // has finished reading the previous bf16 copy
+      mbar_wait(&bars.ds_full, t & 1);
+      if (!STATE_ONLY) mbar_wait(&bars.x_done, t & 1);
+      if (warp == WARP_KV && lane == 0) LA_TR(t, 13);
       tc_fence_after();
-      const float decay = pw[b];
-#pragma unroll
-      for (int half = 0; half < 2; ++half) {
-        float ds[32];
-        tmem_ld32(lane_addr + TM_DS + hh * 64 + half * 32, ds);
-        tmem_ld_wait();
-#pragma unroll
-        for (int j = 0; j < 32; ++j) kv[half * 32 + j] = fmaf(decay, kv[half * 32 + j], ds[j]);
+      if (t + 1 < nchunks) {
+        const float next_decay = pw[chunk_len(t + 1)];
+#pragma unroll 1
+        for (int q4 = 0; q4 < 4; ++q4) {
+          float x[16];
+          tmem_ld16(st_cols + q4 * 16, x);
+          tmem_ld_wait();
+          publish(x, q4, next_decay);
+        }
+        signal_ready();
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&bars->ds_free);
-      if (!STATE_ONLY) publish_state();
+      if (warp == WARP_KV && lane == 0) LA_TR(t, 14);
     }
-    if (STATE_ONLY) {
-      float* dst = args.delta_out + ((int64_t)bh * args.nseg + seg) * D * D + (int64_t)i * D + hh * 64;
+    if (nchunks > 0) {
+      float* dst = nullptr;
+      int T = 0;
+      if (STATE_ONLY) {
+        dst = args.delta_out + ((int64_t)bh * args.nseg + seg) * D * D;
+      } else if (args.state_out != nullptr && (rev ? seg == 0 : seg == args.nseg - 1)) {
+        dst = args.state_out + (int64_t)bh * D * D;
+        T = args.out_T;
+      }
+      if (dst != nullptr) {
+#pragma unroll 1
+        for (int q4 = 0; q4 < 4; ++q4) {
+          float x[16];
+          tmem_ld16(st_cols + q4 * 16, x);
+          tmem_ld_wait();
 #pragma unroll
-      for (int j = 0; j < 64; ++j) dst[j] = kv[j];
-    } else if (args.state_out != nullptr && (rev ? seg == 0 : seg == args.nseg - 1)) {
-      float* dst = args.state_out + (int64_t)bh * D * D;
-#pragma unroll
-      for (int j = 0; j < 64; ++j) {
-        const int col = hh * 64 + j;
-        dst[args.out_T ? (col * D + i) : (i * D + col)] = kv[j];
+          for (int j = 0; j < 16; ++j) {
+            const int col = hh * 64 + q4 * 16 + j;
+            dst[T ? (col * D + i) : (i * D + col)] = x[j];
+          }
+        }
       }
     }
   }
-
   tc_fence_before();
   __syncthreads();
   if (warp == WARP_MMA) {
@@ -407,9 +548,14 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
+thread_local char g_detail[256];
+
 bool make_map(CUtensorMap* map, const void* base, const PassDesc& p) {
   auto enc = encode_fn();
-  if (enc == nullptr) return false;
+  if (enc == nullptr) {
+    snprintf(g_detail, sizeof(g_detail), "cuTensorMapEncodeTiled entry point unavailable");
+    return false;
+  }
   cuuint64_t dims[4] = {(cuuint64_t)p.d, (cuuint64_t)p.n, (cuuint64_t)p.heads, (cuuint64_t)p.batch};
   cuuint64_t strides[3] = {(cuuint64_t)p.sn * 2, (cuuint64_t)p.sh * 2, (cuuint64_t)p.sb * 2};
   cuuint32_t box[4] = {64, (cuuint32_t)C, 1, 1};
@@ -420,17 +566,25 @@ bool make_map(CUtensorMap* map, const void* base, const PassDesc& p) {
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    snprintf(g_detail, sizeof(g_detail), "cuTensorMapEncodeTiled failed (CUresult %d) base=%p dims=%llu,%llu,%llu,%llu "
+             "strides=%llu,%llu,%llu", (int)r, base, (unsigned long long)dims[0], (unsigned long long)dims[1],
+             (unsigned long long)dims[2], (unsigned long long)dims[3], (unsigned long long)strides[0],
+             (unsigned long long)strides[1], (unsigned long long)strides[2]);
   return r == CUDA_SUCCESS;
 }
 
 template <bool STATE_ONLY>
 cudaError_t launch_tc(const PassDesc& p, cudaStream_t st) {
-  CUtensorMap ma, mb, mc, mo;
+  CUtensorMap ma, mb, mc;
   std::memset(&ma, 0, sizeof(ma));
-  std::memset(&mo, 0, sizeof(mo));
   if (!make_map(&mb, p.b, p) || !make_map(&mc, p.c, p)) return cudaErrorInvalidValue;
-  if (!STATE_ONLY && (!make_map(&ma, p.a, p) || !make_map(&mo, p.out, p))) return cudaErrorInvalidValue;
+  if (!STATE_ONLY && !make_map(&ma, p.a, p)) return cudaErrorInvalidValue;
   TcArgs a;
+  a.out = reinterpret_cast<uint16_t*>(p.out);
+  a.sb = p.sb;
+  a.sh = p.sh;
+  a.sn = p.sn;
   a.heads = p.heads;
   a.n = p.n;
   a.seg_len = p.seg_len;
@@ -448,13 +602,21 @@ cudaError_t launch_tc(const PassDesc& p, cudaStream_t st) {
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
   if (err != cudaSuccess) return err;
   dim3 grid(p.nseg, p.batch * p.heads);
-  kern<<<grid, NUM_THREADS, SMEM_BYTES, st>>>(ma, mb, mc, mo, a);
+  kern<<<grid, NUM_THREADS, SMEM_BYTES, st>>>(ma, mb, mc, a);
   return cudaGetLastError();
 }
 
 bool aligned16(const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15) == 0; }
 
 }  // namespace
+
+const char* tc_detail() { return g_detail; }
+
+#ifdef LA_TRACE
+extern "C" __attribute__((visibility("default"))) int la_debug_set_trace(void* dev_ptr) {
+  return (int)cudaMemcpyToSymbol(g_la_trace, &dev_ptr, sizeof(dev_ptr));
+}
+#endif
 
 bool tc_supported(int dtype, int d, const int64_t* strides) {
   if (dtype != LA_BF16 || d != D) return false;

@@ -5,6 +5,7 @@
 namespace la {
 bool tc_supported(int dtype, int d, const int64_t* strides);
 bool tc_pointers_ok(const PassDesc& p);
+const char* tc_detail();  // thread-local detail of the last host-side failure
 Plan tc_plan(int64_t bh, int64_t n, int d, int64_t want_segments);
 size_t tc_workspace_bytes(int64_t bh, int nseg, int d);
 cudaError_t tc_pass(PassDesc p, void* ws, cudaStream_t st);
