@@ -227,3 +227,15 @@ __device__ __forceinline__ uint4 mul_bf16x2(uint4 a, uint32_t s) {
 __device__ __forceinline__ uint4 lds128_bcast(uint32_t a) { return lds128(a); }
 }  // namespace ptx
 }  // namespace la
+
+namespace la {
+namespace ptx {
+// TMA prefetch of a tensor tile into L2 (no shared memory, no barrier)
+__device__ __forceinline__ void tma_prefetch_l2_4d(const CUtensorMap* map, int c0, int c1, int c2, int c3) {
+  asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global.tile [%0, {%1, %2, %3, %4}];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+               : "memory");
+}
+}  // namespace ptx
+}  // namespace la

@@ -201,7 +201,6 @@ cudaError_t simt_state_t(PassDesc p, void* ws, cudaStream_t st) {
   using Acc = typename SimtTraits<Tin>::Acc;
   constexpr int C = SimtTraits<Tin>::C;
   const int bh = p.batch * p.heads;
-  const size_t dd = (size_t)p.d * p.d;
   if (p.nseg == 1) {
     p.delta_out = p.state_out;  // single segment: its summary is the answer
     return launch_simt<Tin, Acc, C, true>(p, st);

@@ -16,7 +16,7 @@
 //   out   = bf16(O)               output warps: tcgen05.ld -> registers -> global
 //
 // Warp roles (26 warps): 0 TMA producer, 1 MMA issuer (+ TMEM owner), 2-9 P/A~
-// conversion, 10-17 output, 18-25 state -- each group two warps per TMEM lane
+// conversion, 10-17 B scaling + output, 18-25 state publish -- each group two warps per TMEM lane
 // quadrant, each warp owning 64 of the 128 columns.  Every hand-off is an mbarrier; a stage is
 // handed back to the TMA producer by the tensor core's own commit after its
 // last MMA, and the MMA issuer runs one chunk ahead on S so the score
@@ -48,11 +48,21 @@ __device__ unsigned long long* g_la_trace = nullptr;
     if (g_la_trace != nullptr && blockIdx.x == 0 && blockIdx.y == 0 && (t) < 32) \
       g_la_trace[(t) * 16 + (ev)] = clock64();                                   \
   } while (0)
+// per-P-warp stamps: [chunk][p warp][event 0..3] after the 512 slots above
+#define LA_TRP(t, pw_, ev)                                                                              \
+  do {                                                                                                  \
+    if (g_la_trace != nullptr && blockIdx.x == 0 && blockIdx.y == 0 && (t) < 32 && (threadIdx.x & 31) == 0) \
+      g_la_trace[512 + ((t) * 8 + (pw_)) * 4 + (ev)] = clock64();                                       \
+  } while (0)
 #else
 #define LA_TR(t, ev) \
   do {               \
   } while (0)
+#define LA_TRP(t, pw_, ev) \
+  do {                     \
+  } while (0)
 #endif
+
 
 constexpr int C = 128;           // chunk rows
 constexpr int D = 128;           // head dim (only d == 128 on this backend)
@@ -70,8 +80,8 @@ constexpr uint32_t IDESC_KMN = idesc_bf16(128, 128, 0, 1);   // A K-major (or TM
 constexpr uint32_t IDESC_MNMN = idesc_bf16(128, 128, 1, 1);  // A MN-major, B MN-major
 
 struct Bars {
-  uint64_t full[NSTAGE];   // TMA -> MMA                       (tx bytes)
-  uint64_t empty[NSTAGE];  // MMA commit after the stage's last MMA -> TMA
+  uint64_t full[3][NSTAGE];   // TMA -> consumers, one ring per operand tile A, B, C (tx bytes)
+  uint64_t empty[3][NSTAGE];  // MMA commit after the tile's last reader -> TMA
   uint64_t s_full[2];      // MMA: S[t%2] done                 -> P warps, state warps
   uint64_t a_full[2];      // A~(t) in TMEM                    -> MMA (per buffer: P warps run a chunk ahead)
   uint64_t p_full[2];      // P(t) in TMEM                     -> MMA
@@ -79,6 +89,7 @@ struct Bars {
   uint64_t y_done[2];      // MMA: O(t) done, per S buffer     -> MMA (before S(t+2) reuses the buffer)
   uint64_t o_full;         // MMA: O done                      -> output warps
   uint64_t o_free;         // output warps read O              -> MMA
+  uint64_t o_staged;       // bf16 O(t) staged in C's slot     -> store lane (TMA store, then C slot free)
   uint64_t b_scaled;       // B~ in SMEM                       -> MMA
   uint64_t ds_full;        // MMA: state += B~^T C done        -> state warps
   uint64_t st_ready;       // bf16 state in SMEM, TMEM state pre-scaled -> MMA
@@ -104,15 +115,12 @@ struct TcArgs {
 // byte offset of 16-byte chunk `c` (0..7) of row `r` inside a [128][64] bf16 block, 128B swizzle
 __device__ __forceinline__ uint32_t sw128(int r, int c) { return (uint32_t)(r * 128 + ((c ^ (r & 7)) << 4)); }
 
-__device__ __forceinline__ void stg128(void* p, uint4 v) {
-  asm volatile("st.global.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
-               : "memory");
-}
 
 template <bool STATE_ONLY>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     tc_pass_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
-                   const __grid_constant__ CUtensorMap map_c, const TcArgs args) {
+                   const __grid_constant__ CUtensorMap map_c, const __grid_constant__ CUtensorMap map_o,
+                   const TcArgs args) {
   extern __shared__ uint8_t smem_raw[];
   __shared__ Bars bars;
   __shared__ __align__(16) float pw[C + 8];  // lam^0 .. lam^128
@@ -133,8 +141,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < NSTAGE; ++s) {
-      mbar_init(&bars.full[s], 1);
-      mbar_init(&bars.empty[s], 1);
+      for (int x = 0; x < 3; ++x) {
+        mbar_init(&bars.full[x][s], 1);
+        mbar_init(&bars.empty[x][s], 1);
+      }
       mbar_init(&bars.s_full[s], 1);
       mbar_init(&bars.p_full[s], NUM_P);
       mbar_init(&bars.a_full[s], NUM_P);
@@ -142,6 +152,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
     mbar_init(&bars.o_full, 1);
     mbar_init(&bars.o_free, NUM_O);
+    mbar_init(&bars.o_staged, NUM_O);
     mbar_init(&bars.b_scaled, NUM_KV);
     mbar_init(&bars.ds_full, 1);
     mbar_init(&bars.x_done, 1);
@@ -157,7 +168,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if (warp == WARP_TMA && lane == 0) {
     tma_prefetch(&map_b);
     tma_prefetch(&map_c);
-    if (!STATE_ONLY) tma_prefetch(&map_a);
+    if (!STATE_ONLY) {
+      tma_prefetch(&map_a);
+      tma_prefetch(&map_o);
+    }
   }
   if (warp == WARP_MMA) tmem_alloc(&bars.tmem_base, TM_COLS);
   tc_fence_before();
@@ -170,21 +184,36 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   if (warp == WARP_TMA) {
     // ------------------------------------------------------------ TMA producer
-    if (lane == 0) {
-      const uint32_t bytes = (STATE_ONLY ? 2 : 3) * TILE;
+    // Lanes 0/1/2 each run the ring of one operand tile (A, B, C), so a tile is refilled as soon as
+    // its own last reader retires: A after X(t), B after the state update, C after Y(t).
+    const int x = lane;
+    if (x < 3 && !(STATE_ONLY && x == 0)) {
+      const CUtensorMap* map = x == 0 ? &map_a : (x == 1 ? &map_b : &map_c);
       for (int t = 0; t < nchunks; ++t) {
         const int s = t % NSTAGE;
-        if (t >= NSTAGE) mbar_wait(&bars.empty[s], ((t / NSTAGE) - 1) & 1);
+        if (t >= NSTAGE) mbar_wait(&bars.empty[x][s], ((t / NSTAGE) - 1) & 1);
         const int r0 = chunk_row0(t);
-        mbar_arrive_expect_tx(&bars.full[s], bytes);
-        LA_TR(t, 0);
-        uint8_t* ga = smem_gen + s * 3 * TILE;
-        for (int hf = 0; hf < 2; ++hf) {
-          if (!STATE_ONLY) tma_load_4d(&map_a, &bars.full[s], ga + hf * HALF, hf * 64, r0, hi, bi);
-          tma_load_4d(&map_b, &bars.full[s], ga + TILE + hf * HALF, hf * 64, r0, hi, bi);
-          tma_load_4d(&map_c, &bars.full[s], ga + 2 * TILE + hf * HALF, hf * 64, r0, hi, bi);
-        }
+        mbar_arrive_expect_tx(&bars.full[x][s], TILE);
+        if (x == 0) LA_TR(t, 0);
+        uint8_t* g = smem_gen + (s * 3 + x) * TILE;
+        tma_load_4d(map, &bars.full[x][s], g, 0, r0, hi, bi);
+        tma_load_4d(map, &bars.full[x][s], g + HALF, 64, r0, hi, bi);
       }
+    } else if (x == 3 && !STATE_ONLY) {
+      // store lane: bf16 O(t) is staged in C(t)'s slot (C's MMA readers are done by then); TMA-store it
+      // and hand the slot back to the C ring once the store has read it
+      for (int t = 0; t < nchunks; ++t) {
+        const int s = t % NSTAGE;
+        mbar_wait(&bars.o_staged, t & 1);
+        uint8_t* g = smem_gen + (s * 3 + 2) * TILE;
+        const int r0 = chunk_row0(t);
+        tma_store_4d(&map_o, g, 0, r0, hi, bi);
+        tma_store_4d(&map_o, g + HALF, 64, r0, hi, bi);
+        tma_store_commit();
+        tma_store_wait_read();
+        mbar_arrive(&bars.empty[2][s]);
+      }
+      tma_store_wait_all();
     }
   } else if (warp == WARP_MMA) {
     // ------------------------------------------------------------ MMA issuer
@@ -192,7 +221,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       auto issue_s = [&](int t) {  // S[t%2] = A B^T  (both K-major)
         const int s = t % NSTAGE;
         const uint32_t a_addr = tile_a(s), b_addr = tile_b(s);
-        mbar_wait(&bars.full[s], (t / NSTAGE) & 1);
+        mbar_wait(&bars.full[0][s], (t / NSTAGE) & 1);
+        mbar_wait(&bars.full[1][s], (t / NSTAGE) & 1);
         // S[t%2] overwrites the TMEM columns P(t-2) / A~(t-2) were read from: those TS-MMAs must have
         // retired (in-order issue alone does not order a TMEM A-operand read before a later D write)
         if (t >= 2) mbar_wait(&bars.y_done[t & 1], ((t - 2) >> 1) & 1);
@@ -216,11 +246,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const uint32_t b_addr = tile_b(s), c_addr = tile_c(s);
         const uint32_t sbuf = tmem + TM_S0 + (t & 1) * 128;
         if (!STATE_ONLY && s_issued == t + 1 && t + 1 < nchunks &&
-            mbar_try_wait(smem_u32(&bars.full[(t + 1) % NSTAGE]), ((t + 1) / NSTAGE) & 1)) {
+            mbar_try_wait(smem_u32(&bars.full[0][(t + 1) % NSTAGE]), ((t + 1) / NSTAGE) & 1) &&
+            mbar_try_wait(smem_u32(&bars.full[1][(t + 1) % NSTAGE]), ((t + 1) / NSTAGE) & 1)) {
           issue_s(t + 1);  // run ahead: S(t+1) as soon as its operands landed
           s_issued = t + 2;
         }
-        if (STATE_ONLY) mbar_wait(&bars.full[s], (t / NSTAGE) & 1);
+        if (STATE_ONLY) mbar_wait(&bars.full[1][s], (t / NSTAGE) & 1);
         // st_ready(t): bf16 state_{t-1} in SMEM and the TMEM state pre-scaled by lam^b
         mbar_wait(&bars.st_ready, t & 1);
         if (!STATE_ONLY) {
@@ -234,9 +265,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             mma_bf16_ts(tmem + TM_O, sbuf + 64 + kk * 8, smem_desc_sw128(st_bf16 + kk * 2048, HALF, 1024),
                         IDESC_KMN, kk > 0);
           mma_commit(&bars.x_done);
+          mma_commit(&bars.empty[0][s]);  // A's readers (S(t), the A~ build) are done
         }
         // state += B~^T C
         mbar_wait(&bars.b_scaled, t & 1);
+        mbar_wait(&bars.full[2][s], (t / NSTAGE) & 1);
         LA_TR(t, 4);
         tc_fence_after();
 #pragma unroll
@@ -244,6 +277,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           mma_bf16_ss(tmem + TM_ST, smem_desc_sw128(b_addr + kk * 2048, HALF, 1024),
                       smem_desc_sw128(c_addr + kk * 2048, HALF, 1024), IDESC_MNMN, 1);
         mma_commit(&bars.ds_full);
+        mma_commit(&bars.empty[1][s]);  // B's last reader
         LA_TR(t, 5);
         if (!STATE_ONLY) {
           // Y(t) = P C  -> O (accumulate)
@@ -261,7 +295,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           mma_commit(&bars.y_done[t & 1]);
           LA_TR(t, 3);
         }
-        mma_commit(&bars.empty[s]);  // the stage's last reader was just issued
+        if (STATE_ONLY) mma_commit(&bars.empty[2][s]);  // C's last reader (else: the store lane frees it)
         if (!STATE_ONLY && s_issued == t + 1 && t + 1 < nchunks) {
           issue_s(t + 1);
           s_issued = t + 2;
@@ -270,7 +304,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       // Drain: every asynchronous tcgen05.commit arrival must land before this CTA retires, or it
       // would hit the barriers of the next CTA scheduled onto this SM's shared memory.
       for (int t = max(0, nchunks - NSTAGE); t < nchunks; ++t) {
-        mbar_wait(&bars.empty[t % NSTAGE], (t / NSTAGE) & 1);
+        for (int x = STATE_ONLY ? 1 : 0; x < 3; ++x) mbar_wait(&bars.empty[x][t % NSTAGE], (t / NSTAGE) & 1);
         if (!STATE_ONLY) mbar_wait(&bars.y_done[t & 1], (t >> 1) & 1);
       }
     }
@@ -288,6 +322,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const uint32_t sbuf = tmem + lane_off + TM_S0 + (t & 1) * 128;
         mbar_wait(&bars.s_full[t & 1], (t >> 1) & 1);
         if (warp == WARP_P && lane == 0) LA_TR(t, 6);
+        LA_TRP(t, warp - WARP_P, 0);
         tc_fence_after();
         // P = bf16(S * M): fwd keeps j <= i with lam^(i-j), rev keeps j >= i with lam^(j-i).
         // A block of 32 keys is all-zero / all-kept / diagonal depending on the warp's quadrant.
@@ -320,16 +355,28 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               pk[2 * q + 1] = pack_bf16x2(v[4 * q + 2] * (base * w2), v[4 * q + 3] * (base * w3));
             }
           } else {
+            // diagonal block: row i = 32 quad + lane, key j = 32 quad + jj, distance |lane - jj| < 32.
+            // fwd needs lam^(lane - jj) = (lam^l of lane l - jj): a shuffle-up by the constant jj;
+            // rev needs lam^(jj - lane) = (lam^(31-l) of lane l + 31 - jj): a shuffle-down.
             float v[32];
             tmem_ld32(sbuf + cb * 32, v);
+            const float own = rev ? pw[31 - lane] : pw[lane];
             tmem_ld_wait();
 #pragma unroll
             for (int jj = 0; jj < 32; jj += 2) {
-              const int j0 = cb * 32 + jj, j1 = j0 + 1;
-              const int d0 = rev ? (j0 - i) : (i - j0);
-              const int d1 = rev ? (j1 - i) : (i - j1);
-              pk[jj >> 1] = pack_bf16x2(d0 >= 0 ? v[jj] * pw[max(d0, 0)] : 0.f,
-                                        d1 >= 0 ? v[jj + 1] * pw[max(d1, 0)] : 0.f);
+              float x0, x1;
+              if (!rev) {
+                const float f0 = __shfl_up_sync(0xffffffffu, own, jj);
+                const float f1 = __shfl_up_sync(0xffffffffu, own, jj + 1);
+                x0 = lane >= jj ? v[jj] * f0 : 0.f;
+                x1 = lane >= jj + 1 ? v[jj + 1] * f1 : 0.f;
+              } else {
+                const float f0 = __shfl_down_sync(0xffffffffu, own, 31 - jj);
+                const float f1 = __shfl_down_sync(0xffffffffu, own, 30 - jj);
+                x0 = lane <= jj ? v[jj] * f0 : 0.f;
+                x1 = lane <= jj + 1 ? v[jj + 1] * f1 : 0.f;
+              }
+              pk[jj >> 1] = pack_bf16x2(x0, x1);
             }
           }
         };
@@ -339,6 +386,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         // 32 half, P(half + 2) at 32 half + 16.  The MMA addresses P per key block accordingly.
         uint32_t p_hi[16];
         convert_block(half + 2, p_hi);
+        LA_TRP(t, warp - WARP_P, 1);
         // A~ = bf16(out_scale * A): fwd lam^(i+1), rev lam^(b-1-i); this warp's 64 columns
         {
           const float osc = rev ? pw[max(b - 1 - i, 0)] : pw[i + 1];
@@ -362,6 +410,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           __syncwarp();
           if (lane == 0) mbar_arrive(&bars.a_full[t & 1]);
         }
+        LA_TRP(t, warp - WARP_P, 2);
         {
           uint32_t p_lo[16];
           convert_block(half, p_lo);
@@ -373,42 +422,69 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(&bars.p_full[t & 1]);
         if (warp == WARP_P && lane == 0) LA_TR(t, 7);
+        LA_TRP(t, warp - WARP_P, 3);
       }
     }
   } else if (warp < WARP_KV) {
-    // ------------------------------------------------------------ output (warps 10..17)
-    if (!STATE_ONLY) {
-      const int quad = warp & 3;
-      const int half = (warp - WARP_O) >> 2;  // output columns [64 half, +64)
-      const int i = quad * 32 + lane;
-      const uint32_t o_cols = tmem + ((uint32_t)(quad * 32) << 16) + TM_O + half * 64;
-      for (int t = 0; t < nchunks; ++t) {
-        const int r0 = chunk_row0(t);
-        const bool valid = i < chunk_len(t);
-        uint16_t* dst =
-            args.out + (int64_t)bi * args.sb + (int64_t)hi * args.sh + (int64_t)(r0 + i) * args.sn + half * 64;
-        mbar_wait(&bars.o_full, t & 1);
-        if (warp == WARP_O && lane == 0) LA_TR(t, 8);
-        tc_fence_after();
-        uint32_t pk[32];
+    // ------------------------------------------------------------ B scaling + output (warps 10..17)
+    const int quad = warp & 3;
+    const int hh = (warp - WARP_O) >> 2;  // 64-column half this warp owns (of B and of O)
+    const int i = quad * 32 + lane;       // chunk row == TMEM lane
+    const uint32_t o_cols = tmem + ((uint32_t)(quad * 32) << 16) + TM_O + hh * 64;
+    for (int t = 0; t < nchunks; ++t) {
+      const int s = t % NSTAGE;
+      const int r0 = chunk_row0(t);
+      const int b = chunk_len(t);
+      if (STATE_ONLY)
+        mbar_wait(&bars.full[1][s], (t / NSTAGE) & 1);
+      else
+        mbar_wait(&bars.s_full[t & 1], (t >> 1) & 1);
+      if (warp == WARP_O && lane == 0) LA_TR(t, 11);
+      // B~ = in_scale * B, in place once S has consumed B (row i, this warp's 64 columns):
+      // fwd lam^(b-1-i), rev lam^(i+1).  Row scaling is order-free, so visit the row's 16-byte chunks in
+      // swizzled order: lane i touches physical chunk m ^ (i & 7), spreading a warp over all 32 banks.
+      {
+        const float isc = (i < b) ? (rev ? pw[i + 1] : pw[b - 1 - i]) : 0.f;
+        const uint32_t isc2 = pack_bf16x2(isc, isc);
+        const uint32_t base = tile_b(s) + hh * HALF + i * 128;
+        uint4 x[8];
 #pragma unroll
-        for (int cb = 0; cb < 2; ++cb) {
-          float y[32];
-          tmem_ld32(o_cols + cb * 32, y);
-          tmem_ld_wait();
+        for (int m = 0; m < 8; ++m) x[m] = lds128(base + ((m ^ (i & 7)) << 4));
 #pragma unroll
-          for (int e = 0; e < 16; ++e) pk[cb * 16 + e] = pack_bf16x2(y[2 * e], y[2 * e + 1]);
-        }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&bars.o_free);  // O's TMEM is free; the stores proceed from registers
-        if (valid) {
-#pragma unroll
-          for (int m = 0; m < 8; ++m)
-            stg128(dst + m * 8, make_uint4(pk[4 * m], pk[4 * m + 1], pk[4 * m + 2], pk[4 * m + 3]));
-        }
-        if (warp == WARP_O && lane == 0) LA_TR(t, 9);
+        for (int m = 0; m < 8; ++m) sts128(base + ((m ^ (i & 7)) << 4), mul_bf16x2(x[m], isc2));
       }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars.b_scaled);
+      if (warp == WARP_O && lane == 0) LA_TR(t, 12);
+      if (STATE_ONLY) continue;
+      // out = bf16(O): TMEM -> registers (then O's columns are released) -> C's SMEM slot -> TMA store
+      (void)r0;
+      mbar_wait(&bars.o_full, t & 1);
+      if (warp == WARP_O && lane == 0) LA_TR(t, 8);
+      tc_fence_after();
+      uint32_t pk[32];
+#pragma unroll
+      for (int cb = 0; cb < 2; ++cb) {
+        float y[32];
+        tmem_ld32(o_cols + cb * 32, y);
+        tmem_ld_wait();
+#pragma unroll
+        for (int e = 0; e < 16; ++e) pk[cb * 16 + e] = pack_bf16x2(y[2 * e], y[2 * e + 1]);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars.o_free);  // O's TMEM is free; the stores proceed from registers
+      {
+        const uint32_t base = tile_c(s) + hh * HALF;
+#pragma unroll
+        for (int m = 0; m < 8; ++m)
+          sts128(base + sw128(i, m), make_uint4(pk[4 * m], pk[4 * m + 1], pk[4 * m + 2], pk[4 * m + 3]));
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars.o_staged);
+      if (warp == WARP_O && lane == 0) LA_TR(t, 9);
     }
   } else {
     // ------------------------------------------------------------ state (warps 18..25)
@@ -460,30 +536,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       signal_ready();
     }
     for (int t = 0; t < nchunks; ++t) {
-      const int s = t % NSTAGE;
-      const int b = chunk_len(t);
-      if (STATE_ONLY)
-        mbar_wait(&bars.full[s], (t / NSTAGE) & 1);
-      else
-        mbar_wait(&bars.s_full[t & 1], (t >> 1) & 1);
-      if (warp == WARP_KV && lane == 0) LA_TR(t, 11);
-      // B~ = in_scale * B, in place (row i, this warpgroup's 64 columns): fwd lam^(b-1-i), rev lam^(i+1).
-      // Row scaling is order-free, so visit the row's 16-byte chunks in swizzled order: lane i touches
-      // physical chunk m ^ (i & 7), spreading a warp over all 32 banks (4 wavefronts / 512 B).
-      {
-        const float isc = (i < b) ? (rev ? pw[i + 1] : pw[b - 1 - i]) : 0.f;
-        const uint32_t isc2 = pack_bf16x2(isc, isc);
-        const uint32_t base = tile_b(s) + hh * HALF + i * 128;
-        uint4 x[8];
-#pragma unroll
-        for (int m = 0; m < 8; ++m) x[m] = lds128(base + ((m ^ (i & 7)) << 4));
-#pragma unroll
-        for (int m = 0; m < 8; ++m) sts128(base + ((m ^ (i & 7)) << 4), mul_bf16x2(x[m], isc2));
-      }
-      fence_proxy_async_smem();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&bars.b_scaled);
-      if (warp == WARP_KV && lane == 0) LA_TR(t, 12);
       // the tensor core accumulated this chunk: read the state, publish it for chunk t+1 once X(t)
       // has finished reading the previous bf16 copy
       mbar_wait(&bars.ds_full, t & 1);
@@ -576,10 +628,11 @@ bool make_map(CUtensorMap* map, const void* base, const PassDesc& p) {
 
 template <bool STATE_ONLY>
 cudaError_t launch_tc(const PassDesc& p, cudaStream_t st) {
-  CUtensorMap ma, mb, mc;
+  CUtensorMap ma, mb, mc, mo;
   std::memset(&ma, 0, sizeof(ma));
+  std::memset(&mo, 0, sizeof(mo));
   if (!make_map(&mb, p.b, p) || !make_map(&mc, p.c, p)) return cudaErrorInvalidValue;
-  if (!STATE_ONLY && !make_map(&ma, p.a, p)) return cudaErrorInvalidValue;
+  if (!STATE_ONLY && (!make_map(&ma, p.a, p) || !make_map(&mo, p.out, p))) return cudaErrorInvalidValue;
   TcArgs a;
   a.out = reinterpret_cast<uint16_t*>(p.out);
   a.sb = p.sb;
@@ -602,7 +655,7 @@ cudaError_t launch_tc(const PassDesc& p, cudaStream_t st) {
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
   if (err != cudaSuccess) return err;
   dim3 grid(p.nseg, p.batch * p.heads);
-  kern<<<grid, NUM_THREADS, SMEM_BYTES, st>>>(ma, mb, mc, a);
+  kern<<<grid, NUM_THREADS, SMEM_BYTES, st>>>(ma, mb, mc, mo, a);
   return cudaGetLastError();
 }
 
