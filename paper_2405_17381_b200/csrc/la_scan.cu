@@ -24,12 +24,13 @@ __global__ void __launch_bounds__(256) segment_scan_kernel(
     const Tacc* u = reinterpret_cast<const Tacc*>(user_in) + (int64_t)bh * d * d;
     s = user_T ? u[c * d + r] : u[e];
   }
+  const Tacc full_decay = (Tacc)pow(l, (double)seg_len);                     // every segment but the last
+  const Tacc last_decay = (Tacc)pow(l, (double)(n - (nseg - 1) * seg_len));  // the (possibly short) last one
   for (int k = 0; k < nseg; ++k) {
     const int sgi = rev ? (nseg - 1 - k) : k;
     const int64_t off = ((int64_t)bh * nseg + sgi) * d * d + e;
     if (seg_in != nullptr) seg_in[off] = s;
-    const int len = min(seg_len, n - sgi * seg_len);
-    s = (Tacc)pow(l, (double)len) * s + delta[off];
+    s = (sgi == nseg - 1 ? last_decay : full_decay) * s + delta[off];
   }
   if (final_out != nullptr) final_out[(int64_t)bh * d * d + (final_T ? c * d + r : e)] = s;
 }

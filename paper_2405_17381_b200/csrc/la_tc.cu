@@ -27,6 +27,8 @@
 #include <cudaTypedefs.h>
 
 #include <cstdio>
+#include <algorithm>
+#include <cmath>
 #include <cstring>
 
 #include "la_common.cuh"
@@ -93,6 +95,7 @@ struct Bars {
   uint64_t b_scaled;       // B~ in SMEM                       -> MMA
   uint64_t ds_full;        // MMA: state += B~^T C done        -> state warps
   uint64_t st_ready;       // bf16 state in SMEM, TMEM state pre-scaled -> MMA
+  uint64_t ds_last;        // MMA: last chunk accumulated      -> state warps (state-only mode)
   uint32_t tmem_base;
 };
 
@@ -124,6 +127,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   extern __shared__ uint8_t smem_raw[];
   __shared__ Bars bars;
   __shared__ __align__(16) float pw[C + 8];  // lam^0 .. lam^128
+  __shared__ double s_lam;
   const uint32_t smem = (smem_u32(smem_raw) + 1023u) & ~1023u;
   uint8_t* smem_gen = smem_raw + (smem - smem_u32(smem_raw));
   auto tile_a = [smem](int s) { return smem + (uint32_t)(s * 3 * TILE); };
@@ -157,9 +161,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     mbar_init(&bars.ds_full, 1);
     mbar_init(&bars.x_done, 1);
     mbar_init(&bars.st_ready, NUM_KV);
+    mbar_init(&bars.ds_last, 1);
     fence_mbar_init();
     double x = 1.0;
     const double lam = args.lam[hi];
+    s_lam = lam;
     for (int k = 0; k <= C; ++k) {
       pw[k] = (float)x;
       x *= lam;
@@ -252,8 +258,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           s_issued = t + 2;
         }
         if (STATE_ONLY) mbar_wait(&bars.full[1][s], (t / NSTAGE) & 1);
-        // st_ready(t): bf16 state_{t-1} in SMEM and the TMEM state pre-scaled by lam^b
-        mbar_wait(&bars.st_ready, t & 1);
+        // st_ready(t): bf16 state_{t-1} in SMEM and the TMEM state pre-scaled by lam^b.  State-only
+        // mode folds the decay into B~ instead and accumulates straight onto the zeroed state.
+        if (!STATE_ONLY || t == 0) mbar_wait(&bars.st_ready, t & 1);
         if (!STATE_ONLY) {
           // X(t) = A~ state_{t-1}  -> O (fresh accumulation)
           if (t >= 1) mbar_wait(&bars.o_free, (t - 1) & 1);
@@ -276,7 +283,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         for (int kk = 0; kk < C / 16; ++kk)
           mma_bf16_ss(tmem + TM_ST, smem_desc_sw128(b_addr + kk * 2048, HALF, 1024),
                       smem_desc_sw128(c_addr + kk * 2048, HALF, 1024), IDESC_MNMN, 1);
-        mma_commit(&bars.ds_full);
+        if (!STATE_ONLY)
+          mma_commit(&bars.ds_full);
+        else if (t == nchunks - 1)
+          mma_commit(&bars.ds_last);
         mma_commit(&bars.empty[1][s]);  // B's last reader
         LA_TR(t, 5);
         if (!STATE_ONLY) {
@@ -305,6 +315,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       // would hit the barriers of the next CTA scheduled onto this SM's shared memory.
       for (int t = max(0, nchunks - NSTAGE); t < nchunks; ++t) {
         for (int x = STATE_ONLY ? 1 : 0; x < 3; ++x) mbar_wait(&bars.empty[x][t % NSTAGE], (t / NSTAGE) & 1);
+        if (STATE_ONLY && t == nchunks - 1) mbar_wait(&bars.ds_last, 0);
         if (!STATE_ONLY) mbar_wait(&bars.y_done[t & 1], (t >> 1) & 1);
       }
     }
@@ -444,7 +455,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       // fwd lam^(b-1-i), rev lam^(i+1).  Row scaling is order-free, so visit the row's 16-byte chunks in
       // swizzled order: lane i touches physical chunk m ^ (i & 7), spreading a warp over all 32 banks.
       {
-        const float isc = (i < b) ? (rev ? pw[i + 1] : pw[b - 1 - i]) : 0.f;
+        float isc = (i < b) ? (rev ? pw[i + 1] : pw[b - 1 - i]) : 0.f;
+        if (STATE_ONLY) {
+          // state-only: weight rows by their full distance to the segment's far edge, lam^(p1-1-s) (fwd)
+          // or lam^(s-p0+1) (rev), so chunks accumulate without decaying the running state
+          isc *= (float)pow(s_lam, (double)(rev ? (r0 - p0) : (p1 - r0 - b)));
+        }
         const uint32_t isc2 = pack_bf16x2(isc, isc);
         const uint32_t base = tile_b(s) + hh * HALF + i * 128;
         uint4 x[8];
@@ -535,7 +551,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
       signal_ready();
     }
-    for (int t = 0; t < nchunks; ++t) {
+    for (int t = 0; t < (STATE_ONLY ? 0 : nchunks); ++t) {
       // the tensor core accumulated this chunk: read the state, publish it for chunk t+1 once X(t)
       // has finished reading the previous bf16 copy
       mbar_wait(&bars.ds_full, t & 1);
@@ -554,6 +570,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         signal_ready();
       }
       if (warp == WARP_KV && lane == 0) LA_TR(t, 14);
+    }
+    if (STATE_ONLY && nchunks > 0) {
+      mbar_wait(&bars.ds_last, 0);
+      tc_fence_after();
     }
     if (nchunks > 0) {
       float* dst = nullptr;
@@ -683,9 +703,31 @@ bool tc_pointers_ok(const PassDesc& p) {
          (p.out == nullptr || aligned16(p.out));
 }
 
+// Segment count from a small cost model in units of one chunk-time of the main pass: waves of CTAs
+// times chunks per segment (+ a per-CTA pipeline fill), plus, when the sequence is split, the
+// state-only pre-pass over K and V (~0.45 chunk-time per chunk) and the scan.  Segments are capped so
+// the workspace does not depend on n (4 waves' worth of CTAs).
 Plan tc_plan(int64_t bh, int64_t n, int d, int64_t want_segments) {
   (void)d;
-  return make_plan(bh, n, C, want_segments, kNumSMs, 2);
+  if (want_segments > 0) return make_plan(bh, n, C, want_segments, kNumSMs, 1);
+  const int64_t nchunks = (n + C - 1) / C;
+  const int64_t cap = (4 * kNumSMs + bh - 1) / bh;
+  double best = 1e300;
+  int64_t best_nseg = 1;
+  for (int64_t want = 1; want <= std::min<int64_t>(nchunks, cap); ++want) {
+    const int64_t cps = (nchunks + want - 1) / want;
+    const int64_t nseg = (nchunks + cps - 1) / cps;
+    const int64_t waves = (bh * nseg + kNumSMs - 1) / kNumSMs;
+    double cost = (double)waves * (cps + 1.5);
+    if (nseg > 1) cost += (double)waves * (0.45 * cps + 1.0) + 1.0;
+    if (cost < best * 0.98) {
+      best = cost;
+      best_nseg = nseg;
+    }
+  }
+  Plan p = make_plan(bh, n, C, best_nseg, kNumSMs, 1);
+  p.nseg_ws = (int)std::max<int64_t>(1, cap);
+  return p;
 }
 
 size_t tc_workspace_bytes(int64_t bh, int nseg, int d) {
