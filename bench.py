@@ -140,10 +140,11 @@ def run_ours(args) -> None:
             q, k, v, do = inputs[n]
             if record is not None:
                 record[n][0].record(stream)
-            ops.la_forward(q, k, v, None, lam_dev=lam_dev)
+            # what the autograd op does: the forward hands its per-segment states to the backward
+            _, seg = ops.la_forward(q, k, v, None, lam_dev=lam_dev, want_seg_states=True)
             if record is not None:
                 record[n][1].record(stream)
-            ops.la_backward(q, k, v, do, None, lam_dev=lam_dev)
+            ops.la_backward(q, k, v, do, None, lam_dev=lam_dev, fwd_seg_states=seg)
             if record is not None:
                 record[n][2].record(stream)
 
@@ -189,7 +190,7 @@ def run_ours(args) -> None:
     # dominant kernel: the pass (one la_fwd = one pass over q,k,v -> o), timed alone on the same stream
     roof = pass_roofline(ops, inputs[args.roofline_n], lam_dev, stream, pk)
     launches = sum(ops.launch_count(tuple(inputs[n][0].shape), which="fwd")
-                   + ops.launch_count(tuple(inputs[n][0].shape), which="bwd") for n in seq_lens) * args.steps
+                   + ops.launch_count(tuple(inputs[n][0].shape), which="bwd_saved") for n in seq_lens) * args.steps
 
     e2e = None if args.no_e2e else run_e2e(ops, seq_lens, tokens, lam_dev, device, min(args.steps, args.e2e_steps),
                                            world)
@@ -264,8 +265,8 @@ def run_e2e(ops, seq_lens, tokens, lam_dev, device, steps, world) -> dict:
         b = tokens[n] // n
         el = tokens[n] * H * D
         dev_in = [h[:el].view(b, H, n, D).to(device, non_blocking=True) for h in host_in]
-        o = ops.la_forward(*dev_in[:3], None, lam_dev=lam_dev)
-        dq, dk, dv = ops.la_backward(*dev_in, None, lam_dev=lam_dev)
+        o, seg = ops.la_forward(*dev_in[:3], None, lam_dev=lam_dev, want_seg_states=True)
+        dq, dk, dv = ops.la_backward(*dev_in, None, lam_dev=lam_dev, fwd_seg_states=seg)
         for h, t in zip(host_out, (o, dq, dk, dv)):
             h[:el].view(b, H, n, D).copy_(t, non_blocking=True)
         return 4 * el * 2, 4 * el * 2

@@ -89,19 +89,29 @@ typedef struct la_desc {
 /* Bytes of scratch the calls below need for this descriptor (may be 0). */
 LA_API size_t la_workspace_bytes(const la_desc* desc);
 
+/* Number of sequence segments the library splits each (batch, head) into for
+ * this descriptor (1 = no split); -1 on a bad descriptor. */
+LA_API int la_segment_count(const la_desc* desc);
+
 /* Forward: o = LA(q, k, v).  kv_in (nullable) seeds the state at position 0;
- * kv_out (nullable) receives F(n). */
+ * kv_out (nullable) receives F(n).  seg_states_out (nullable; used only when
+ * la_segment_count > 1) receives the state entering every segment,
+ * [batch, heads, segments, d, d]; passing it to la_bwd spares the backward
+ * one summary pass. */
 LA_API int la_fwd(const la_desc* desc, const void* q, const void* k, const void* v,
            const double* lam, const void* kv_in, void* o, void* kv_out,
-           void* workspace, size_t workspace_bytes, void* stream);
+           void* seg_states_out, void* workspace, size_t workspace_bytes, void* stream);
 
 /* Backward: (dq, dk, dv) = d<LA(q,k,v), do>.  kv_in is the forward's kv_in
  * (nullable = zeros); dkv_in (nullable) is R(n), the adjoint state arriving from
- * beyond the sequence end; dkv_out (nullable) receives R(0). */
+ * beyond the sequence end; fwd_seg_states (nullable) is the forward's
+ * seg_states_out for the same descriptor and kv_in; dkv_out (nullable)
+ * receives R(0). */
 LA_API int la_bwd(const la_desc* desc, const void* q, const void* k, const void* v,
            const void* dout, const double* lam, const void* kv_in,
-           const void* dkv_in, void* dq, void* dk, void* dv, void* dkv_out,
-           void* workspace, size_t workspace_bytes, void* stream);
+           const void* dkv_in, const void* fwd_seg_states, void* dq, void* dk,
+           void* dv, void* dkv_out, void* workspace, size_t workspace_bytes,
+           void* stream);
 
 /* Local summaries of one sequence segment, for sequence parallelism:
  *   la_fwd_state: kv_delta  = sum_s lam^(n-1-s) k[s] v[s]^T   (= F(n) with kv_in = 0)
@@ -113,8 +123,9 @@ LA_API int la_bwd_state(const la_desc* desc, const void* q, const void* dout,
                  const double* lam, void* dkv_delta,
                  void* workspace, size_t workspace_bytes, void* stream);
 
-/* Number of kernels la_fwd (which = 0) or la_bwd (which = 1) launches for this
- * descriptor (segment summaries, scan and the main passes); -1 on a bad desc. */
+/* Number of kernels la_fwd (which = 0), la_bwd (which = 1) or la_bwd given the
+ * forward's segment states (which = 2) launches for this descriptor; -1 on a
+ * bad descriptor. */
 LA_API int la_launch_count(const la_desc* desc, int which);
 
 /* Thread-local message for the last non-LA_OK status returned on this thread. */

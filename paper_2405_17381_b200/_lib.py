@@ -22,7 +22,7 @@ LA_BACKEND_AUTO, LA_BACKEND_SIMT, LA_BACKEND_TCGEN05 = 0, 1, 2
 BACKENDS = {"auto": LA_BACKEND_AUTO, "simt": LA_BACKEND_SIMT, "tcgen05": LA_BACKEND_TCGEN05}
 
 # every symbol include/lightning_attn.h declares
-EXPORTS = ("la_workspace_bytes", "la_fwd", "la_bwd", "la_fwd_state", "la_bwd_state",
+EXPORTS = ("la_workspace_bytes", "la_segment_count", "la_fwd", "la_bwd", "la_fwd_state", "la_bwd_state",
            "la_launch_count", "la_last_error", "la_abi_version", "la_build_info")
 
 
@@ -72,11 +72,13 @@ def load() -> ctypes.CDLL:
     P = POINTER(LaDesc)
     lib.la_workspace_bytes.argtypes = [P]
     lib.la_workspace_bytes.restype = c_size_t
+    lib.la_segment_count.argtypes = [P]
+    lib.la_segment_count.restype = c_int
     lib.la_fwd.argtypes = [P, c_void_p, c_void_p, c_void_p, POINTER(c_double), c_void_p, c_void_p, c_void_p,
-                           c_void_p, c_size_t, c_void_p]
+                           c_void_p, c_void_p, c_size_t, c_void_p]
     lib.la_fwd.restype = c_int
     lib.la_bwd.argtypes = [P, c_void_p, c_void_p, c_void_p, c_void_p, POINTER(c_double), c_void_p, c_void_p,
-                           c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]
+                           c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]
     lib.la_bwd.restype = c_int
     lib.la_fwd_state.argtypes = [P, c_void_p, c_void_p, POINTER(c_double), c_void_p, c_void_p, c_size_t, c_void_p]
     lib.la_fwd_state.restype = c_int

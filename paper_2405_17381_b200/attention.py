@@ -24,16 +24,18 @@ class LightningAttention(torch.autograd.Function):
         heads = q.shape[1] if layout == "bhnd" else q.shape[2]
         lam_dev = lam if (isinstance(lam, torch.Tensor) and lam.is_cuda and lam.dtype == torch.float64) \
             else ops.decay_tensor(lam, heads, q.device)
-        o = ops.la_forward(q, k, v, None, block=block, layout=layout, backend=backend, lam_dev=lam_dev)
-        ctx.save_for_backward(q, k, v, lam_dev)
+        o, seg = ops.la_forward(q, k, v, None, block=block, layout=layout, backend=backend, lam_dev=lam_dev,
+                                want_seg_states=True)
+        # the per-segment states of a split sequence spare the backward one summary pass (la_bwd)
+        ctx.save_for_backward(q, k, v, lam_dev, seg)
         ctx.block, ctx.layout, ctx.backend = block, layout, backend
         return o
 
     @staticmethod
     def backward(ctx, do):
-        q, k, v, lam_dev = ctx.saved_tensors
+        q, k, v, lam_dev, seg = ctx.saved_tensors
         dq, dk, dv = ops.la_backward(q, k, v, do.to(q.dtype), None, block=ctx.block, layout=ctx.layout,
-                                     backend=ctx.backend, lam_dev=lam_dev)
+                                     backend=ctx.backend, lam_dev=lam_dev, fwd_seg_states=seg)
         return dq, dk, dv, None, None, None, None
 
 

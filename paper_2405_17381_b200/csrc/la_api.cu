@@ -16,6 +16,7 @@
 #include <cuda.h>
 
 #include "la_common.cuh"
+#include "la_scan.cuh"
 #include "la_simt.cuh"
 #include "la_tc.cuh"
 
@@ -83,10 +84,14 @@ la::Plan plan_for(const la_desc* desc, int backend) {
   return la::make_plan(bh, desc->n, la::simt_chunk(desc->dtype), desc->segments, 2 * la::kNumSMs, 4);
 }
 
+size_t acc_bytes(int dtype) { return dtype == LA_F64 ? sizeof(double) : sizeof(float); }
+
+// Workspace: per-segment summaries | per-segment entering states, each [bh][nseg][d][d] in the
+// accumulation type; sized for the plan's segment cap so it does not depend on n.
 size_t ws_bytes_for(const la_desc* desc, int backend, const la::Plan& plan) {
-  const int64_t bh = desc->batch * desc->heads;
-  if (backend == LA_BACKEND_TCGEN05) return la::tc_workspace_bytes(bh, plan.nseg_ws, (int)desc->d);
-  return la::simt_workspace_bytes(desc->dtype, bh, plan.nseg_ws, (int)desc->d);
+  (void)backend;
+  if (plan.nseg_ws <= 1) return 0;
+  return 2 * acc_bytes(desc->dtype) * (size_t)(desc->batch * desc->heads) * plan.nseg_ws * desc->d * desc->d;
 }
 
 la::PassDesc base_pass(const la_desc* desc, const la::Plan& plan, const double* lam) {
@@ -105,20 +110,51 @@ la::PassDesc base_pass(const la_desc* desc, const la::Plan& plan, const double* 
   return p;
 }
 
-cudaError_t run_pass(int backend, int dtype, const la::PassDesc& p, void* ws, cudaStream_t st) {
+cudaError_t launch(int backend, int dtype, const la::PassDesc& p, bool state_only, cudaStream_t st) {
   if (backend == LA_BACKEND_TCGEN05) {
     if (!la::tc_pointers_ok(p)) return cudaErrorMisalignedAddress;  // TMA needs 16-byte aligned bases
-    return la::tc_pass(p, ws, st);
+    return la::tc_launch(p, state_only, st);
   }
-  return la::simt_pass(dtype, p, ws, st);
+  return la::simt_launch(dtype, p, state_only, st);
 }
 
-cudaError_t run_state(int backend, int dtype, const la::PassDesc& p, void* ws, cudaStream_t st) {
-  if (backend == LA_BACKEND_TCGEN05) {
-    if (!la::tc_pointers_ok(p)) return cudaErrorMisalignedAddress;
-    return la::tc_state(p, ws, st);
+// Entering state of every segment of a pass (p.b, p.c, p.rev; p.state_in = the caller's state at the
+// sequence edge, p.state_in_T its orientation): per-segment summaries into `delta`, then the decayed
+// scan into `seg_in` ([bh][nseg][d][d], kernel orientation).
+cudaError_t segment_states(int backend, int dtype, const la::PassDesc& p, void* delta, void* seg_in, cudaStream_t st) {
+  la::PassDesc s = p;
+  s.a = nullptr;
+  s.out = nullptr;
+  s.state_in = nullptr;
+  s.state_out = nullptr;
+  s.delta_out = delta;
+  cudaError_t err = launch(backend, dtype, s, true, st);
+  if (err != cudaSuccess) return err;
+  return la::launch_segment_scan(dtype == LA_F64, delta, seg_in, p.state_in, p.state_in_T, nullptr, 0, p.lam,
+                                 p.batch * p.heads, p.heads, p.d, p.n, p.seg_len, p.nseg, p.rev, st);
+}
+
+// The main pass.  With one segment the caller's edge state is used as is; with several, the entering
+// states `seg_in` (orientation seg_T) must already be computed.
+cudaError_t main_pass(int backend, int dtype, la::PassDesc p, const void* seg_in, int seg_T, cudaStream_t st) {
+  const int64_t dd = (int64_t)p.d * p.d;
+  if (p.nseg > 1) {
+    p.state_in = seg_in;
+    p.state_in_T = seg_T;
+    p.state_in_bh_stride = (int64_t)p.nseg * dd;
+    p.state_in_seg_stride = dd;
+  } else {
+    p.state_in_bh_stride = dd;
+    p.state_in_seg_stride = 0;
   }
-  return la::simt_state(dtype, p, ws, st);
+  return launch(backend, dtype, p, false, st);
+}
+
+// delta / seg_in regions of the workspace
+void* ws_delta(void* ws) { return ws; }
+void* ws_seg_in(void* ws, const la_desc* desc, const la::Plan& plan) {
+  return static_cast<char*>(ws) + acc_bytes(desc->dtype) * (size_t)(desc->batch * desc->heads) * plan.nseg_ws *
+                                      desc->d * desc->d;
 }
 
 // This library carries its own (static) CUDA runtime.  A caller's thread may
@@ -179,8 +215,15 @@ size_t la_workspace_bytes(const la_desc* desc) {
   return ws_bytes_for(desc, backend, plan_for(desc, backend));
 }
 
-int la_fwd(const la_desc* desc, const void* q, const void* k, const void* v, const double* lam,
-           const void* kv_in, void* o, void* kv_out, void* workspace, size_t workspace_bytes, void* stream) {
+int la_segment_count(const la_desc* desc) {
+  if (validate(desc) != LA_OK) return -1;
+  int backend;
+  if (pick_backend(desc, &backend) != LA_OK) return -1;
+  return plan_for(desc, backend).nseg;
+}
+
+int la_fwd(const la_desc* desc, const void* q, const void* k, const void* v, const double* lam, const void* kv_in,
+           void* o, void* kv_out, void* seg_states_out, void* workspace, size_t workspace_bytes, void* stream) {
   Prepared pr;
   int rc = prepare(desc, workspace_bytes, workspace, &pr);
   if (rc != LA_OK) return rc;
@@ -195,14 +238,20 @@ int la_fwd(const la_desc* desc, const void* q, const void* k, const void* v, con
   p.rev = 0;
   p.state_in = kv_in;
   p.state_out = kv_out;
-  cudaError_t err = run_pass(pr.backend, desc->dtype, p, workspace, st);
+  cudaError_t err = cudaSuccess;
+  void* seg_in = nullptr;
+  if (pr.plan.nseg > 1) {
+    seg_in = seg_states_out != nullptr ? seg_states_out : ws_seg_in(workspace, desc, pr.plan);
+    err = segment_states(pr.backend, desc->dtype, p, ws_delta(workspace), seg_in, st);
+  }
+  if (err == cudaSuccess) err = main_pass(pr.backend, desc->dtype, p, seg_in, 0, st);
   if (err != cudaSuccess) return cuda_fail(err, "la_fwd");
   return LA_OK;
 }
 
 int la_bwd(const la_desc* desc, const void* q, const void* k, const void* v, const void* dout, const double* lam,
-           const void* kv_in, const void* dkv_in, void* dq, void* dk, void* dv, void* dkv_out, void* workspace,
-           size_t workspace_bytes, void* stream) {
+           const void* kv_in, const void* dkv_in, const void* fwd_seg_states, void* dq, void* dk, void* dv,
+           void* dkv_out, void* workspace, size_t workspace_bytes, void* stream) {
   Prepared pr;
   int rc = prepare(desc, workspace_bytes, workspace, &pr);
   if (rc != LA_OK) return rc;
@@ -211,8 +260,12 @@ int la_bwd(const la_desc* desc, const void* q, const void* k, const void* v, con
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   bind_stream_context(st);
   const la::PassDesc base = base_pass(desc, pr.plan, lam);
-  cudaError_t err;
-  // sweep 1 (kernels.py:309-318): dq = fwd(do, v, k), state kv^T
+  const bool split = pr.plan.nseg > 1;
+  void* delta = split ? ws_delta(workspace) : nullptr;
+  void* seg_in = split ? ws_seg_in(workspace, desc, pr.plan) : nullptr;
+  cudaError_t err = cudaSuccess;
+  // sweep 1 (kernels.py:309-318): dq = fwd(do, v, k); its state is kv^T, so the forward's segment
+  // states serve it transposed when the caller kept them
   la::PassDesc p = base;
   p.a = dout;
   p.b = v;
@@ -221,8 +274,22 @@ int la_bwd(const la_desc* desc, const void* q, const void* k, const void* v, con
   p.rev = 0;
   p.state_in = kv_in;
   p.state_in_T = 1;
-  if ((err = run_pass(pr.backend, desc->dtype, p, workspace, st)) != cudaSuccess) return cuda_fail(err, "la_bwd dq");
-  // sweep 2 (kernels.py:320-333): dk = rev(v, do, q), state dkv^T
+  if (split && fwd_seg_states != nullptr) {
+    err = main_pass(pr.backend, desc->dtype, p, fwd_seg_states, 1, st);
+  } else {
+    if (split) err = segment_states(pr.backend, desc->dtype, p, delta, seg_in, st);
+    if (err == cudaSuccess) err = main_pass(pr.backend, desc->dtype, p, seg_in, 0, st);
+  }
+  if (err != cudaSuccess) return cuda_fail(err, "la_bwd dq");
+  // sweep 2 (kernels.py:320-333): dk = rev(v, do, q) carries dkv^T, dv = rev(k, q, do) carries dkv --
+  // one set of segment states (over q, do) serves both passes
+  la::PassDesc pd = base;
+  pd.b = q;
+  pd.c = dout;
+  pd.rev = 1;
+  pd.state_in = dkv_in;
+  if (split && (err = segment_states(pr.backend, desc->dtype, pd, delta, seg_in, st)) != cudaSuccess)
+    return cuda_fail(err, "la_bwd dkv states");
   p = base;
   p.a = v;
   p.b = dout;
@@ -231,8 +298,7 @@ int la_bwd(const la_desc* desc, const void* q, const void* k, const void* v, con
   p.rev = 1;
   p.state_in = dkv_in;
   p.state_in_T = 1;
-  if ((err = run_pass(pr.backend, desc->dtype, p, workspace, st)) != cudaSuccess) return cuda_fail(err, "la_bwd dk");
-  //                              dv = rev(k, q, do), state dkv (written out as R(0))
+  if ((err = main_pass(pr.backend, desc->dtype, p, seg_in, 1, st)) != cudaSuccess) return cuda_fail(err, "la_bwd dk");
   p = base;
   p.a = k;
   p.b = q;
@@ -241,42 +307,45 @@ int la_bwd(const la_desc* desc, const void* q, const void* k, const void* v, con
   p.rev = 1;
   p.state_in = dkv_in;
   p.state_out = dkv_out;
-  if ((err = run_pass(pr.backend, desc->dtype, p, workspace, st)) != cudaSuccess) return cuda_fail(err, "la_bwd dv");
+  if ((err = main_pass(pr.backend, desc->dtype, p, seg_in, 0, st)) != cudaSuccess) return cuda_fail(err, "la_bwd dv");
+  return LA_OK;
+}
+
+static int state_entry(const la_desc* desc, const void* b, const void* c, int rev, const double* lam, void* out,
+                       void* workspace, size_t workspace_bytes, void* stream, const char* who) {
+  Prepared pr;
+  int rc = prepare(desc, workspace_bytes, workspace, &pr);
+  if (rc != LA_OK) return rc;
+  if (!b || !c || !lam || !out) return fail(LA_ERR_SHAPE, "%s: null operand", who);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  bind_stream_context(st);
+  la::PassDesc p = base_pass(desc, pr.plan, lam);
+  p.b = b;
+  p.c = c;
+  p.rev = rev;
+  cudaError_t err;
+  if (pr.plan.nseg == 1) {
+    p.delta_out = out;  // one segment: its summary is the answer
+    err = launch(pr.backend, desc->dtype, p, true, st);
+  } else {
+    p.delta_out = ws_delta(workspace);
+    err = launch(pr.backend, desc->dtype, p, true, st);
+    if (err == cudaSuccess)
+      err = la::launch_segment_scan(desc->dtype == LA_F64, p.delta_out, nullptr, nullptr, 0, out, 0, lam,
+                                    p.batch * p.heads, p.heads, p.d, p.n, p.seg_len, p.nseg, rev, st);
+  }
+  if (err != cudaSuccess) return cuda_fail(err, who);
   return LA_OK;
 }
 
 int la_fwd_state(const la_desc* desc, const void* k, const void* v, const double* lam, void* kv_delta,
                  void* workspace, size_t workspace_bytes, void* stream) {
-  Prepared pr;
-  int rc = prepare(desc, workspace_bytes, workspace, &pr);
-  if (rc != LA_OK) return rc;
-  if (!k || !v || !lam || !kv_delta) return fail(LA_ERR_SHAPE, "la_fwd_state: null k/v/lam/kv_delta");
-  bind_stream_context(reinterpret_cast<cudaStream_t>(stream));
-  la::PassDesc p = base_pass(desc, pr.plan, lam);
-  p.b = k;
-  p.c = v;
-  p.rev = 0;
-  p.state_out = kv_delta;
-  cudaError_t err = run_state(pr.backend, desc->dtype, p, workspace, reinterpret_cast<cudaStream_t>(stream));
-  if (err != cudaSuccess) return cuda_fail(err, "la_fwd_state");
-  return LA_OK;
+  return state_entry(desc, k, v, 0, lam, kv_delta, workspace, workspace_bytes, stream, "la_fwd_state");
 }
 
 int la_bwd_state(const la_desc* desc, const void* q, const void* dout, const double* lam, void* dkv_delta,
                  void* workspace, size_t workspace_bytes, void* stream) {
-  Prepared pr;
-  int rc = prepare(desc, workspace_bytes, workspace, &pr);
-  if (rc != LA_OK) return rc;
-  if (!q || !dout || !lam || !dkv_delta) return fail(LA_ERR_SHAPE, "la_bwd_state: null q/do/lam/dkv_delta");
-  bind_stream_context(reinterpret_cast<cudaStream_t>(stream));
-  la::PassDesc p = base_pass(desc, pr.plan, lam);
-  p.b = q;
-  p.c = dout;
-  p.rev = 1;
-  p.state_out = dkv_delta;
-  cudaError_t err = run_state(pr.backend, desc->dtype, p, workspace, reinterpret_cast<cudaStream_t>(stream));
-  if (err != cudaSuccess) return cuda_fail(err, "la_bwd_state");
-  return LA_OK;
+  return state_entry(desc, q, dout, 1, lam, dkv_delta, workspace, workspace_bytes, stream, "la_bwd_state");
 }
 
 int la_launch_count(const la_desc* desc, int which) {
@@ -284,8 +353,10 @@ int la_launch_count(const la_desc* desc, int which) {
   int backend;
   if (pick_backend(desc, &backend) != LA_OK) return -1;
   const la::Plan plan = plan_for(desc, backend);
-  const int per_pass = plan.nseg > 1 ? 3 : 1;  // summaries + scan + main, or main only
-  return (which == 0 ? 1 : 3) * per_pass;
+  if (plan.nseg == 1) return which == 0 ? 1 : 3;
+  // fwd: summaries + scan + main.  bwd: dq main (+ its summaries and scan unless the forward's segment
+  // states are passed, which = 2) + one dkv summaries + scan + the dk and dv mains
+  return which == 0 ? 3 : (which == 2 ? 5 : 7);
 }
 
 const char* la_last_error(void) { return g_last_error.c_str(); }

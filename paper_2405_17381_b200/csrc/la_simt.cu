@@ -167,76 +167,21 @@ template <> struct SimtTraits<float> { using Acc = float; static constexpr int C
 template <> struct SimtTraits<__nv_bfloat16> { using Acc = float; static constexpr int C = 32; };
 
 template <typename Tin>
-cudaError_t simt_pass_t(PassDesc p, void* ws, cudaStream_t st) {
+cudaError_t simt_launch_t(const PassDesc& p, bool state_only, cudaStream_t st) {
   using Acc = typename SimtTraits<Tin>::Acc;
   constexpr int C = SimtTraits<Tin>::C;
-  const int bh = p.batch * p.heads;
-  const size_t dd = (size_t)p.d * p.d;
-  if (p.nseg > 1) {
-    Acc* delta = reinterpret_cast<Acc*>(ws);
-    Acc* seg_in = delta + (size_t)bh * p.nseg * dd;
-    PassDesc s = p;
-    s.out = nullptr;
-    s.state_in = nullptr;
-    s.state_out = nullptr;
-    s.delta_out = delta;
-    cudaError_t err = launch_simt<Tin, Acc, C, true>(s, st);
-    if (err != cudaSuccess) return err;
-    err = launch_segment_scan(sizeof(Acc) == 8, delta, seg_in, p.state_in, p.state_in_T, nullptr, 0, p.lam, bh,
-                              p.heads, p.d, p.n, p.seg_len, p.nseg, p.rev, st);
-    if (err != cudaSuccess) return err;
-    p.state_in = seg_in;
-    p.state_in_T = 0;
-    p.state_in_bh_stride = (int64_t)p.nseg * dd;
-    p.state_in_seg_stride = (int64_t)dd;
-  } else {
-    p.state_in_bh_stride = (int64_t)dd;
-    p.state_in_seg_stride = 0;
-  }
-  return launch_simt<Tin, Acc, C, false>(p, st);
-}
-
-template <typename Tin>
-cudaError_t simt_state_t(PassDesc p, void* ws, cudaStream_t st) {
-  using Acc = typename SimtTraits<Tin>::Acc;
-  constexpr int C = SimtTraits<Tin>::C;
-  const int bh = p.batch * p.heads;
-  if (p.nseg == 1) {
-    p.delta_out = p.state_out;  // single segment: its summary is the answer
-    return launch_simt<Tin, Acc, C, true>(p, st);
-  }
-  Acc* delta = reinterpret_cast<Acc*>(ws);
-  p.delta_out = delta;
-  cudaError_t err = launch_simt<Tin, Acc, C, true>(p, st);
-  if (err != cudaSuccess) return err;
-  return launch_segment_scan(sizeof(Acc) == 8, delta, nullptr, nullptr, 0, p.state_out, p.state_out_T, p.lam, bh,
-                             p.heads, p.d, p.n, p.seg_len, p.nseg, p.rev, st);
+  return state_only ? launch_simt<Tin, Acc, C, true>(p, st) : launch_simt<Tin, Acc, C, false>(p, st);
 }
 
 }  // namespace
 
 int simt_chunk(int dtype) { return dtype == LA_F64 ? SimtTraits<double>::C : SimtTraits<float>::C; }
 
-size_t simt_workspace_bytes(int dtype, int64_t bh, int nseg, int d) {
-  if (nseg <= 1) return 0;
-  const size_t acc = dtype == LA_F64 ? sizeof(double) : sizeof(float);
-  return 2 * acc * (size_t)bh * nseg * d * d;
-}
-
-cudaError_t simt_pass(int dtype, const PassDesc& p, void* ws, cudaStream_t st) {
+cudaError_t simt_launch(int dtype, const PassDesc& p, bool state_only, cudaStream_t st) {
   switch (dtype) {
-    case LA_F64: return simt_pass_t<double>(p, ws, st);
-    case LA_F32: return simt_pass_t<float>(p, ws, st);
-    case LA_BF16: return simt_pass_t<__nv_bfloat16>(p, ws, st);
-  }
-  return cudaErrorInvalidValue;
-}
-
-cudaError_t simt_state(int dtype, const PassDesc& p, void* ws, cudaStream_t st) {
-  switch (dtype) {
-    case LA_F64: return simt_state_t<double>(p, ws, st);
-    case LA_F32: return simt_state_t<float>(p, ws, st);
-    case LA_BF16: return simt_state_t<__nv_bfloat16>(p, ws, st);
+    case LA_F64: return simt_launch_t<double>(p, state_only, st);
+    case LA_F32: return simt_launch_t<float>(p, state_only, st);
+    case LA_BF16: return simt_launch_t<__nv_bfloat16>(p, state_only, st);
   }
   return cudaErrorInvalidValue;
 }

@@ -4,7 +4,6 @@
 
 namespace la {
 int simt_chunk(int dtype);
-size_t simt_workspace_bytes(int dtype, int64_t bh, int nseg, int d);
-cudaError_t simt_pass(int dtype, const PassDesc& p, void* ws, cudaStream_t st);
-cudaError_t simt_state(int dtype, const PassDesc& p, void* ws, cudaStream_t st);
+// one launch of the main pass kernel (state_only = false) or of the per-segment summary kernel
+cudaError_t simt_launch(int dtype, const PassDesc& p, bool state_only, cudaStream_t st);
 }  // namespace la

@@ -730,51 +730,8 @@ Plan tc_plan(int64_t bh, int64_t n, int d, int64_t want_segments) {
   return p;
 }
 
-size_t tc_workspace_bytes(int64_t bh, int nseg, int d) {
-  if (nseg <= 1) return 0;
-  return 2 * sizeof(float) * (size_t)bh * nseg * d * d;
-}
-
-cudaError_t tc_pass(PassDesc p, void* ws, cudaStream_t st) {
-  const int bh = p.batch * p.heads;
-  const size_t dd = (size_t)p.d * p.d;
-  if (p.nseg > 1) {
-    float* delta = reinterpret_cast<float*>(ws);
-    float* seg_in = delta + (size_t)bh * p.nseg * dd;
-    PassDesc s = p;
-    s.a = nullptr;
-    s.out = nullptr;
-    s.state_in = nullptr;
-    s.state_out = nullptr;
-    s.delta_out = delta;
-    cudaError_t err = launch_tc<true>(s, st);
-    if (err != cudaSuccess) return err;
-    err = launch_segment_scan(false, delta, seg_in, p.state_in, p.state_in_T, nullptr, 0, p.lam, bh, p.heads, p.d,
-                              p.n, p.seg_len, p.nseg, p.rev, st);
-    if (err != cudaSuccess) return err;
-    p.state_in = seg_in;
-    p.state_in_T = 0;
-    p.state_in_bh_stride = (int64_t)p.nseg * dd;
-    p.state_in_seg_stride = (int64_t)dd;
-  } else {
-    p.state_in_bh_stride = (int64_t)dd;
-    p.state_in_seg_stride = 0;
-  }
-  return launch_tc<false>(p, st);
-}
-
-cudaError_t tc_state(PassDesc p, void* ws, cudaStream_t st) {
-  const int bh = p.batch * p.heads;
-  if (p.nseg == 1) {
-    p.delta_out = p.state_out;
-    return launch_tc<true>(p, st);
-  }
-  float* delta = reinterpret_cast<float*>(ws);
-  p.delta_out = delta;
-  cudaError_t err = launch_tc<true>(p, st);
-  if (err != cudaSuccess) return err;
-  return launch_segment_scan(false, delta, nullptr, nullptr, 0, p.state_out, p.state_out_T, p.lam, bh, p.heads, p.d,
-                             p.n, p.seg_len, p.nseg, p.rev, st);
+cudaError_t tc_launch(const PassDesc& p, bool state_only, cudaStream_t st) {
+  return state_only ? launch_tc<true>(p, st) : launch_tc<false>(p, st);
 }
 
 }  // namespace la

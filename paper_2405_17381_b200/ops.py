@@ -131,9 +131,17 @@ def _stream(device) -> ctypes.c_void_p:
     return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
 
 
+def segment_count(desc) -> int:
+    return int(_lib.load().la_segment_count(ctypes.byref(desc)))
+
+
 def la_forward(q, k, v, lam, *, block=None, kv_in=None, want_state=False, layout="bhnd",
-               backend="auto", segments=0, lam_dev=None):
-    """o (and kv_out) for batched q, k, v.  ``lam``: float or one value per head."""
+               backend="auto", segments=0, lam_dev=None, want_seg_states=False):
+    """o (and kv_out) for batched q, k, v.  ``lam``: float or one value per head.
+
+    ``want_seg_states``: also return the state entering every sequence segment (or None when the
+    library does not split the sequence) -- pass it to ``la_backward(fwd_seg_states=...)``.
+    """
     (q, k, v), g = _prep([q, k, v], "QKV", layout)
     lib = _lib.load()
     desc = _desc(g, q.dtype, block, backend, segments)
@@ -142,15 +150,24 @@ def la_forward(q, k, v, lam, *, block=None, kv_in=None, want_state=False, layout
     o = torch.empty_like(q)
     kv_out = torch.empty((g.batch, g.heads, g.d, g.d), dtype=state_dtype(q.dtype), device=q.device) \
         if want_state else None
+    seg = None
+    if want_seg_states:
+        nseg = segment_count(desc)
+        if nseg > 1:
+            seg = torch.empty((g.batch, g.heads, nseg, g.d, g.d), dtype=state_dtype(q.dtype), device=q.device)
     ws, nbytes = _workspace(lib, desc, q.device)
     _lib.check(lib.la_fwd(ctypes.byref(desc), _ptr(q), _ptr(k), _ptr(v), _lam_ptr(lam_dev), _ptr(kv_in),
-                          _ptr(o), _ptr(kv_out), _ptr(ws), nbytes, _stream(q.device)))
-    return (o, kv_out) if want_state else o
+                          _ptr(o), _ptr(kv_out), _ptr(seg), _ptr(ws), nbytes, _stream(q.device)))
+    out = (o, kv_out) if want_state else o
+    return (out, seg) if want_seg_states else out
 
 
 def la_backward(q, k, v, do, lam, *, block=None, kv_in=None, dkv_in=None, want_state=False, layout="bhnd",
-                backend="auto", segments=0, lam_dev=None):
-    """(dq, dk, dv) (and dkv_out = R(0)) of <LA(q, k, v), do>."""
+                backend="auto", segments=0, lam_dev=None, fwd_seg_states=None):
+    """(dq, dk, dv) (and dkv_out = R(0)) of <LA(q, k, v), do>.
+
+    ``fwd_seg_states``: the forward's segment states for the same problem and kv_in (optional).
+    """
     (q, k, v, do), g = _prep([q, k, v, do], ["Q", "K", "V", "dO"], layout)
     lib = _lib.load()
     desc = _desc(g, q.dtype, block, backend, segments)
@@ -161,9 +178,12 @@ def la_backward(q, k, v, do, lam, *, block=None, kv_in=None, dkv_in=None, want_s
     dkv_out = torch.empty((g.batch, g.heads, g.d, g.d), dtype=state_dtype(q.dtype), device=q.device) \
         if want_state else None
     ws, nbytes = _workspace(lib, desc, q.device)
+    if fwd_seg_states is not None and fwd_seg_states.shape[2] != segment_count(desc):
+        raise ShapeError(f"fwd_seg_states holds {fwd_seg_states.shape[2]} segments, the plan has "
+                         f"{segment_count(desc)}")
     _lib.check(lib.la_bwd(ctypes.byref(desc), _ptr(q), _ptr(k), _ptr(v), _ptr(do), _lam_ptr(lam_dev),
-                          _ptr(kv_in), _ptr(dkv_in), _ptr(dq), _ptr(dk), _ptr(dv), _ptr(dkv_out), _ptr(ws),
-                          nbytes, _stream(q.device)))
+                          _ptr(kv_in), _ptr(dkv_in), _ptr(fwd_seg_states), _ptr(dq), _ptr(dk), _ptr(dv),
+                          _ptr(dkv_out), _ptr(ws), nbytes, _stream(q.device)))
     return (dq, dk, dv, dkv_out) if want_state else (dq, dk, dv)
 
 
@@ -206,7 +226,8 @@ def workspace_bytes(shape, dtype=torch.bfloat16, *, layout="bhnd", backend="auto
 
 
 def launch_count(shape, dtype=torch.bfloat16, *, which="fwd", layout="bhnd", backend="auto", segments=0) -> int:
-    """Kernels one la_fwd / la_bwd call launches for this problem (la_launch_count)."""
+    """Kernels one call launches for this problem (la_launch_count): which = "fwd", "bwd", or
+    "bwd_saved" (backward given the forward's segment states)."""
     if layout == "bhnd":
         b, h, n, d = shape
         strides = (h * n * d, n * d, d)
@@ -214,4 +235,4 @@ def launch_count(shape, dtype=torch.bfloat16, *, which="fwd", layout="bhnd", bac
         b, n, h, d = shape
         strides = (n * h * d, d, h * d)
     desc = _desc(Geometry(b, h, n, d, strides), dtype, None, backend, segments)
-    return int(_lib.load().la_launch_count(ctypes.byref(desc), 0 if which == "fwd" else 1))
+    return int(_lib.load().la_launch_count(ctypes.byref(desc), {"fwd": 0, "bwd": 1, "bwd_saved": 2}[which]))

@@ -48,7 +48,7 @@ def _fwd(desc):
     lib = _lib.load()
     dummy = ctypes.c_void_p(16)
     lam = ctypes.cast(ctypes.c_void_p(16), ctypes.POINTER(ctypes.c_double))
-    return lib.la_fwd(ctypes.byref(desc), dummy, dummy, dummy, lam, None, dummy, None, None, 0, None)
+    return lib.la_fwd(ctypes.byref(desc), dummy, dummy, dummy, lam, None, dummy, None, None, None, 0, None)
 
 
 @pytest.mark.parametrize("kw,code", [
@@ -82,3 +82,14 @@ def test_workspace_is_bounded_in_n():
         sizes.add(lib.la_workspace_bytes(ctypes.byref(_desc(n=n, d=128, heads=16, dtype=_lib.LA_BF16))))
     assert len(sizes) == 1, sizes
     assert lib.la_workspace_bytes(ctypes.byref(_desc(n=0))) == 0
+
+
+def test_segment_count_and_launches_follow_the_plan():
+    lib = _lib.load()
+    short = _desc(batch=64, heads=16, n=1024, d=128, dtype=_lib.LA_BF16)
+    long_ = _desc(batch=1, heads=16, n=1 << 17, d=128, dtype=_lib.LA_BF16)
+    assert lib.la_segment_count(ctypes.byref(short)) == 1
+    assert lib.la_launch_count(ctypes.byref(short), 0) == 1 and lib.la_launch_count(ctypes.byref(short), 1) == 3
+    assert lib.la_segment_count(ctypes.byref(long_)) > 1
+    assert [lib.la_launch_count(ctypes.byref(long_), w) for w in (0, 1, 2)] == [3, 7, 5]
+    assert lib.la_segment_count(ctypes.byref(_desc(n=0))) == -1
