@@ -23,6 +23,8 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 BUILD = ROOT / "build"
 LIB = PKG / "libla_b200.so"
+# fault-injection build (reverse-pass state update sign-flipped) used only by tests/test_gpu_mutation.py
+MUTANT_LIB = BUILD / "mutant" / "libla_b200_mutant.so"
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + [
@@ -51,6 +53,22 @@ def _compile(src: Path, verbose: bool) -> tuple[Path, str]:
         raise RuntimeError(f"nvcc failed for {src.name}:\n{' '.join(cmd)}\n{proc.stdout}\n{proc.stderr}")
     log = proc.stderr if verbose else ""
     return obj, log
+
+
+def build_mutant(force: bool = False) -> Path:
+    """The whole library compiled with -DLA_MUTATE_DKV (test infrastructure, never loaded by the package)."""
+    MUTANT_LIB.parent.mkdir(parents=True, exist_ok=True)
+    sources = sorted(CSRC.glob("*.cu"))
+    newest = max([_newest_dep()] + [s.stat().st_mtime for s in sources])
+    if not force and MUTANT_LIB.exists() and MUTANT_LIB.stat().st_mtime >= newest:
+        return MUTANT_LIB
+    flags = NVCC_FLAGS[:-2]  # without "-Xptxas -v"
+    cmd = [nvcc(), *flags, "-DLA_MUTATE_DKV", "-shared", "-cudart", "static", "-o", str(MUTANT_LIB),
+           *map(str, sources)]
+    proc = subprocess.run(cmd, capture_output=True, text=True)
+    if proc.returncode != 0:
+        raise RuntimeError(f"mutant build failed:\n{proc.stderr}")
+    return MUTANT_LIB
 
 
 def build(force: bool = False, verbose: bool = False) -> Path:
@@ -83,6 +101,7 @@ def main() -> None:
     ap.add_argument("--verbose", action="store_true")
     args = ap.parse_args()
     print(build(force=args.force, verbose=args.verbose))
+    print(build_mutant(force=args.force))
 
 
 if __name__ == "__main__":

@@ -125,6 +125,9 @@ __global__ void __launch_bounds__(kThreads) simt_pass_kernel(PassDesc p) {
         const Tacc isc = pw[p.rev ? (j + 1) : (b - 1 - j)];
         acc += isc * sB[j * ld + k] * sC[j * ld + col];
       }
+#ifdef LA_MUTATE_DKV
+      if (p.rev) acc = -acc;  // fault injection: the reference's `_dkv_step` sign flip (test_kernels.py:249-268)
+#endif
       sKV[e] = decay * sKV[e] + acc;
     }
     __syncthreads();

@@ -461,6 +461,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           // or lam^(s-p0+1) (rev), so chunks accumulate without decaying the running state
           isc *= (float)pow(s_lam, (double)(rev ? (r0 - p0) : (p1 - r0 - b)));
         }
+#ifdef LA_MUTATE_DKV
+        if (rev) isc = -isc;  // fault injection: the reference's `_dkv_step` sign flip (test_kernels.py:249-268)
+#endif
         const uint32_t isc2 = pack_bf16x2(isc, isc);
         const uint32_t base = tile_b(s) + hh * HALF + i * 128;
         uint4 x[8];
