@@ -290,6 +290,31 @@ int la_bwd(const la_desc* desc, const void* q, const void* k, const void* v, con
   pd.state_in = dkv_in;
   if (split && (err = segment_states(pr.backend, desc->dtype, pd, delta, seg_in, st)) != cudaSuccess)
     return cuda_fail(err, "la_bwd dkv states");
+  if (pr.backend == LA_BACKEND_TCGEN05) {
+    // one fused sweep for dk and dv (la_tc_bwd.cu): q, k, v, do read once, one state update
+    p = base;
+    p.rev = 1;
+    p.b = q;
+    p.c = dout;
+    p.a = k;
+    p.out = dv;
+    p.state_out = dkv_out;
+    const int64_t dd = (int64_t)p.d * p.d;
+    if (split) {
+      p.state_in = seg_in;
+      p.state_in_bh_stride = (int64_t)p.nseg * dd;
+      p.state_in_seg_stride = dd;
+    } else {
+      p.state_in = dkv_in;
+      p.state_in_bh_stride = dd;
+      p.state_in_seg_stride = 0;
+    }
+    if (!la::tc_pointers_ok(p) || (reinterpret_cast<uintptr_t>(v) & 15) || (reinterpret_cast<uintptr_t>(dk) & 15))
+      return cuda_fail(cudaErrorMisalignedAddress, "la_bwd dkdv");
+    if ((err = la::tc_dkdv_launch(p, q, k, v, dout, dq, dk, dv, st)) != cudaSuccess)
+      return cuda_fail(err, "la_bwd dkdv");
+    return LA_OK;
+  }
   p = base;
   p.a = v;
   p.b = dout;
@@ -353,10 +378,12 @@ int la_launch_count(const la_desc* desc, int which) {
   int backend;
   if (pick_backend(desc, &backend) != LA_OK) return -1;
   const la::Plan plan = plan_for(desc, backend);
-  if (plan.nseg == 1) return which == 0 ? 1 : 3;
+  // bwd sweep 2 is one fused dk/dv kernel on the tcgen05 backend, two passes on SIMT
+  const int sweep2 = backend == LA_BACKEND_TCGEN05 ? 1 : 2;
+  if (plan.nseg == 1) return which == 0 ? 1 : 1 + sweep2;
   // fwd: summaries + scan + main.  bwd: dq main (+ its summaries and scan unless the forward's segment
-  // states are passed, which = 2) + one dkv summaries + scan + the dk and dv mains
-  return which == 0 ? 3 : (which == 2 ? 5 : 7);
+  // states are passed, which = 2) + one dkv summaries + scan + sweep 2
+  return which == 0 ? 3 : (which == 2 ? 3 : 5) + sweep2;
 }
 
 const char* la_last_error(void) { return g_last_error.c_str(); }

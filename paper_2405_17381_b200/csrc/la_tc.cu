@@ -91,7 +91,8 @@ struct Bars {
   uint64_t y_done[2];      // MMA: O(t) done, per S buffer     -> MMA (before S(t+2) reuses the buffer)
   uint64_t o_full;         // MMA: O done                      -> output warps
   uint64_t o_free;         // output warps read O              -> MMA
-  uint64_t o_staged;       // bf16 O(t) staged in C's slot     -> store lane (TMA store, then C slot free)
+  uint64_t o_staged[2];    // bf16 O(t) staged in C's slot t%2 -> store lane (per slot: the output warps
+                           // may stage a chunk ahead of the store lane)
   uint64_t b_scaled;       // B~ in SMEM                       -> MMA
   uint64_t ds_full;        // MMA: state += B~^T C done        -> state warps
   uint64_t st_ready;       // bf16 state in SMEM, TMEM state pre-scaled -> MMA
@@ -156,7 +157,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
     mbar_init(&bars.o_full, 1);
     mbar_init(&bars.o_free, NUM_O);
-    mbar_init(&bars.o_staged, NUM_O);
+    mbar_init(&bars.o_staged[0], NUM_O);
+    mbar_init(&bars.o_staged[1], NUM_O);
     mbar_init(&bars.b_scaled, NUM_KV);
     mbar_init(&bars.ds_full, 1);
     mbar_init(&bars.x_done, 1);
@@ -210,7 +212,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       // and hand the slot back to the C ring once the store has read it
       for (int t = 0; t < nchunks; ++t) {
         const int s = t % NSTAGE;
-        mbar_wait(&bars.o_staged, t & 1);
+        mbar_wait(&bars.o_staged[s], (t / NSTAGE) & 1);
         uint8_t* g = smem_gen + (s * 3 + 2) * TILE;
         const int r0 = chunk_row0(t);
         tma_store_4d(&map_o, g, 0, r0, hi, bi);
@@ -502,7 +504,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
       fence_proxy_async_smem();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&bars.o_staged);
+      if (lane == 0) mbar_arrive(&bars.o_staged[s]);
       if (warp == WARP_O && lane == 0) LA_TR(t, 9);
     }
   } else {
@@ -625,7 +627,9 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 thread_local char g_detail[256];
 
-bool make_map(CUtensorMap* map, const void* base, const PassDesc& p) {
+}  // namespace
+
+bool tc_make_map(CUtensorMap* map, const void* base, const PassDesc& p) {
   auto enc = encode_fn();
   if (enc == nullptr) {
     snprintf(g_detail, sizeof(g_detail), "cuTensorMapEncodeTiled entry point unavailable");
@@ -649,13 +653,15 @@ bool make_map(CUtensorMap* map, const void* base, const PassDesc& p) {
   return r == CUDA_SUCCESS;
 }
 
+namespace {
+
 template <bool STATE_ONLY>
 cudaError_t launch_tc(const PassDesc& p, cudaStream_t st) {
   CUtensorMap ma, mb, mc, mo;
   std::memset(&ma, 0, sizeof(ma));
   std::memset(&mo, 0, sizeof(mo));
-  if (!make_map(&mb, p.b, p) || !make_map(&mc, p.c, p)) return cudaErrorInvalidValue;
-  if (!STATE_ONLY && (!make_map(&ma, p.a, p) || !make_map(&mo, p.out, p))) return cudaErrorInvalidValue;
+  if (!tc_make_map(&mb, p.b, p) || !tc_make_map(&mc, p.c, p)) return cudaErrorInvalidValue;
+  if (!STATE_ONLY && (!tc_make_map(&ma, p.a, p) || !tc_make_map(&mo, p.out, p))) return cudaErrorInvalidValue;
   TcArgs a;
   a.out = reinterpret_cast<uint16_t*>(p.out);
   a.sb = p.sb;

@@ -1,12 +1,21 @@
 // la_tc.cuh -- host-side entry points of the TMA + tcgen05 backend (la_tc.cu).
 #pragma once
+#include <cuda.h>
+
 #include "la_common.cuh"
 
 namespace la {
 bool tc_supported(int dtype, int d, const int64_t* strides);
 bool tc_pointers_ok(const PassDesc& p);
 const char* tc_detail();  // thread-local detail of the last host-side failure
+// 4-D TMA descriptor (d, n, heads, batch) over a bf16 [.., .., .., 128] tensor with the desc's strides,
+// box 64 x 128, 128-byte swizzle
+bool tc_make_map(CUtensorMap* map, const void* base, const PassDesc& p);
 Plan tc_plan(int64_t bh, int64_t n, int d, int64_t want_segments);
+// the fused reverse sweep of the backward: dK and dV in one pass over q, k, v, do (p.state_in = the
+// entering adjoint state in dkv orientation; p.state_out = dkv_out, written by segment 0)
+cudaError_t tc_dkdv_launch(const PassDesc& p, const void* q, const void* k, const void* v, const void* dout,
+                           void* dq_unused, void* dk, void* dv, cudaStream_t st);
 // one launch of the main pass kernel (state_only = false) or of the per-segment summary kernel
 cudaError_t tc_launch(const PassDesc& p, bool state_only, cudaStream_t st);
 }  // namespace la

@@ -89,7 +89,8 @@ def test_segment_count_and_launches_follow_the_plan():
     short = _desc(batch=64, heads=16, n=1024, d=128, dtype=_lib.LA_BF16)
     long_ = _desc(batch=1, heads=16, n=1 << 17, d=128, dtype=_lib.LA_BF16)
     assert lib.la_segment_count(ctypes.byref(short)) == 1
-    assert lib.la_launch_count(ctypes.byref(short), 0) == 1 and lib.la_launch_count(ctypes.byref(short), 1) == 3
+    # tcgen05 backend: bwd = dq pass + one fused dk/dv sweep
+    assert lib.la_launch_count(ctypes.byref(short), 0) == 1 and lib.la_launch_count(ctypes.byref(short), 1) == 2
     assert lib.la_segment_count(ctypes.byref(long_)) > 1
-    assert [lib.la_launch_count(ctypes.byref(long_), w) for w in (0, 1, 2)] == [3, 7, 5]
+    assert [lib.la_launch_count(ctypes.byref(long_), w) for w in (0, 1, 2)] == [3, 6, 4]
     assert lib.la_segment_count(ctypes.byref(_desc(n=0))) == -1
