@@ -712,30 +712,20 @@ bool tc_pointers_ok(const PassDesc& p) {
          (p.out == nullptr || aligned16(p.out));
 }
 
-// Segment count from a small cost model in units of one chunk-time of the main pass: waves of CTAs
-// times chunks per segment (+ a per-CTA pipeline fill), plus, when the sequence is split, the
-// state-only pre-pass over K and V (~0.45 chunk-time per chunk) and the scan.  Segments are capped so
-// the workspace does not depend on n (4 waves' worth of CTAs).
+// Segment count: when batch*heads fill >= 60% of the SMs, no split (a split costs a summary pass over
+// two operands); otherwise the largest count that keeps all CTAs in ONE wave, which measured best on
+// B200 at every long-n bench shape (profiles/r01_seg_sweep.txt: multi-wave splits lose to per-CTA
+// pipeline fill and partial last waves).  Segments keep >= 2 chunks; the workspace is sized for the
+// one-wave cap so it does not depend on n.
 Plan tc_plan(int64_t bh, int64_t n, int d, int64_t want_segments) {
   (void)d;
   if (want_segments > 0) return make_plan(bh, n, C, want_segments, kNumSMs, 1);
   const int64_t nchunks = (n + C - 1) / C;
-  const int64_t cap = (4 * kNumSMs + bh - 1) / bh;
-  double best = 1e300;
-  int64_t best_nseg = 1;
-  for (int64_t want = 1; want <= std::min<int64_t>(nchunks, cap); ++want) {
-    const int64_t cps = (nchunks + want - 1) / want;
-    const int64_t nseg = (nchunks + cps - 1) / cps;
-    const int64_t waves = (bh * nseg + kNumSMs - 1) / kNumSMs;
-    double cost = (double)waves * (cps + 1.5);
-    if (nseg > 1) cost += (double)waves * (0.45 * cps + 1.0) + 1.0;
-    if (cost < best * 0.98) {
-      best = cost;
-      best_nseg = nseg;
-    }
-  }
-  Plan p = make_plan(bh, n, C, best_nseg, kNumSMs, 1);
-  p.nseg_ws = (int)std::max<int64_t>(1, cap);
+  const int64_t cap = std::max<int64_t>(1, kNumSMs / bh);
+  int64_t nseg = 1;
+  if (bh * 10 < kNumSMs * 6) nseg = std::min<int64_t>(cap, std::max<int64_t>(1, nchunks / 2));
+  Plan p = make_plan(bh, n, C, nseg, kNumSMs, 1);
+  p.nseg_ws = (int)cap;
   return p;
 }
 
