@@ -91,7 +91,8 @@ size_t acc_bytes(int dtype) { return dtype == LA_F64 ? sizeof(double) : sizeof(f
 size_t ws_bytes_for(const la_desc* desc, int backend, const la::Plan& plan) {
   (void)backend;
   if (plan.nseg_ws <= 1) return 0;
-  return 2 * acc_bytes(desc->dtype) * (size_t)(desc->batch * desc->heads) * plan.nseg_ws * desc->d * desc->d;
+  return acc_bytes(desc->dtype) * (size_t)(desc->batch * desc->heads) * (plan.nsub_ws + plan.nseg_ws) * desc->d *
+         desc->d;
 }
 
 la::PassDesc base_pass(const la_desc* desc, const la::Plan& plan, const double* lam) {
@@ -107,6 +108,10 @@ la::PassDesc base_pass(const la_desc* desc, const la::Plan& plan, const double* 
   p.lam = lam;
   p.seg_len = plan.seg_len;
   p.nseg = plan.nseg;
+  p.sub_len = plan.sub_len;
+  p.sub_per_seg = plan.sub_per_seg;
+  p.g_lo = 0;
+  p.g_hi = plan.nseg - 1;
   return p;
 }
 
@@ -119,8 +124,9 @@ cudaError_t launch(int backend, int dtype, const la::PassDesc& p, bool state_onl
 }
 
 // Entering state of every segment of a pass (p.b, p.c, p.rev; p.state_in = the caller's state at the
-// sequence edge, p.state_in_T its orientation): per-segment summaries into `delta`, then the decayed
-// scan into `seg_in` ([bh][nseg][d][d], kernel orientation).
+// sequence edge, p.state_in_T its orientation): sub-segment summaries into `delta`, then the decayed
+// scan into `seg_in` ([bh][nseg][d][d], kernel orientation).  The segment at the far end of the pass
+// (fwd: the last, rev: the first) feeds no entering state, so it is not summarised.
 cudaError_t segment_states(int backend, int dtype, const la::PassDesc& p, void* delta, void* seg_in, cudaStream_t st) {
   la::PassDesc s = p;
   s.a = nullptr;
@@ -128,10 +134,12 @@ cudaError_t segment_states(int backend, int dtype, const la::PassDesc& p, void* 
   s.state_in = nullptr;
   s.state_out = nullptr;
   s.delta_out = delta;
+  s.g_lo = p.rev ? 1 : 0;
+  s.g_hi = p.rev ? p.nseg - 1 : p.nseg - 2;
   cudaError_t err = launch(backend, dtype, s, true, st);
   if (err != cudaSuccess) return err;
   return la::launch_segment_scan(dtype == LA_F64, delta, seg_in, p.state_in, p.state_in_T, nullptr, 0, p.lam,
-                                 p.batch * p.heads, p.heads, p.d, p.n, p.seg_len, p.nseg, p.rev, st);
+                                 p.batch * p.heads, p.heads, p.d, s, st);
 }
 
 // The main pass.  With one segment the caller's edge state is used as is; with several, the entering
@@ -153,7 +161,7 @@ cudaError_t main_pass(int backend, int dtype, la::PassDesc p, const void* seg_in
 // delta / seg_in regions of the workspace
 void* ws_delta(void* ws) { return ws; }
 void* ws_seg_in(void* ws, const la_desc* desc, const la::Plan& plan) {
-  return static_cast<char*>(ws) + acc_bytes(desc->dtype) * (size_t)(desc->batch * desc->heads) * plan.nseg_ws *
+  return static_cast<char*>(ws) + acc_bytes(desc->dtype) * (size_t)(desc->batch * desc->heads) * plan.nsub_ws *
                                       desc->d * desc->d;
 }
 
@@ -357,7 +365,7 @@ static int state_entry(const la_desc* desc, const void* b, const void* c, int re
     err = launch(pr.backend, desc->dtype, p, true, st);
     if (err == cudaSuccess)
       err = la::launch_segment_scan(desc->dtype == LA_F64, p.delta_out, nullptr, nullptr, 0, out, 0, lam,
-                                    p.batch * p.heads, p.heads, p.d, p.n, p.seg_len, p.nseg, rev, st);
+                                    p.batch * p.heads, p.heads, p.d, p, st);
   }
   if (err != cudaSuccess) return cuda_fail(err, who);
   return LA_OK;

@@ -65,16 +65,23 @@ struct PassDesc {
   // final state of the pass (fwd: F(n), rev: R(0)), written by the last segment processed
   void* state_out;        // nullable
   int state_out_T;
-  // state-only mode: per-segment local summaries [bh][nseg][d][d]
+  // state-only mode: local summaries of sub-segments, [bh][nseg * sub_per_seg][d][d].  Sub-segment j of
+  // segment g covers [g seg_len + j sub_len, min(.. + sub_len, (g + 1) seg_len, n)); only segments
+  // g_lo..g_hi are summarised (the forward never needs the last segment's, the reverse pass never the
+  // first's), so the summary work spreads over all SMs and covers only the rows a scan needs.
   void* delta_out;
+  int sub_len, sub_per_seg, g_lo, g_hi;
 };
 
 // Segment plan shared by host code of every backend.
 struct Plan {
-  int chunk;    // rows per chunk in the kernel
-  int nseg;     // segments per (b, h)
-  int seg_len;  // positions per segment (multiple of chunk)
-  int nseg_ws;  // segments the workspace is sized for: independent of n (kernels.py:342-368 c05)
+  int chunk;        // rows per chunk in the kernel
+  int nseg;         // segments per (b, h)
+  int seg_len;      // positions per segment (multiple of chunk)
+  int nseg_ws;      // segments the workspace is sized for: independent of n (kernels.py:342-368 c05)
+  int sub_per_seg;  // summary sub-segments per segment (1: one summary per segment)
+  int sub_len;      // positions per summary sub-segment (multiple of chunk)
+  int nsub_ws;      // summary slots per (b, h) the workspace is sized for (>= nseg * sub_per_seg)
 };
 
 inline Plan make_plan(int64_t bh, int64_t n, int chunk, int64_t want_segments, int64_t target_ctas,
@@ -96,7 +103,28 @@ inline Plan make_plan(int64_t bh, int64_t n, int chunk, int64_t want_segments, i
   int64_t chunks_per_seg = (nchunks + nseg - 1) / nseg;
   p.seg_len = (int)(chunks_per_seg * chunk);
   p.nseg = (int)((n + p.seg_len - 1) / p.seg_len);
+  p.sub_per_seg = 1;
+  p.sub_len = p.seg_len;
+  p.nsub_ws = p.nseg_ws;
   return p;
+}
+
+// Split each segment into summary sub-segments so that one summary launch over the segments a scan
+// needs (all but one) puts about `target_ctas` CTAs of >= `min_chunks` chunks each on the GPU.
+// `nsub_cap` bounds nseg * sub_per_seg (the workspace's summary slots).
+inline void plan_subsegments(Plan& p, int64_t bh, int64_t target_ctas, int64_t min_chunks, int64_t nsub_cap) {
+  p.sub_per_seg = 1;
+  p.sub_len = p.seg_len;
+  if (p.nseg <= 1) return;
+  const int64_t cps = p.seg_len / p.chunk;
+  int64_t sps = target_ctas / (bh * (p.nseg - 1));
+  const int64_t max_sps = cps / (min_chunks > 0 ? min_chunks : 1);
+  if (sps > max_sps) sps = max_sps;
+  if (sps * p.nseg > nsub_cap) sps = nsub_cap / p.nseg;
+  if (sps < 1) sps = 1;
+  const int64_t sub_chunks = (cps + sps - 1) / sps;
+  p.sub_len = (int)(sub_chunks * p.chunk);
+  p.sub_per_seg = (int)((cps + sub_chunks - 1) / sub_chunks);
 }
 
 }  // namespace la

@@ -43,18 +43,18 @@ namespace {
 using namespace ptx;
 
 #ifdef LA_TRACE
-// debug build only: cycle stamps of pipeline events of CTA (0, 0), [chunk][event]
+// debug build only: cycle stamps of pipeline events of CTA (0, 0), [chunk][event].  The buffer pointer is
+// read once into `la_trp` at kernel entry (a global load per stamp would distort the timeline).
 __device__ unsigned long long* g_la_trace = nullptr;
-#define LA_TR(t, ev)                                                             \
-  do {                                                                           \
-    if (g_la_trace != nullptr && blockIdx.x == 0 && blockIdx.y == 0 && (t) < 32) \
-      g_la_trace[(t) * 16 + (ev)] = clock64();                                   \
+#define LA_TR(t, ev)                                                          \
+  do {                                                                        \
+    if (la_trp != nullptr && (t) < 32) la_trp[(t) * 32 + (ev)] = clock64(); \
   } while (0)
-// per-P-warp stamps: [chunk][p warp][event 0..3] after the 512 slots above
-#define LA_TRP(t, pw_, ev)                                                                              \
-  do {                                                                                                  \
-    if (g_la_trace != nullptr && blockIdx.x == 0 && blockIdx.y == 0 && (t) < 32 && (threadIdx.x & 31) == 0) \
-      g_la_trace[512 + ((t) * 8 + (pw_)) * 4 + (ev)] = clock64();                                       \
+// per-P-warp stamps: [chunk][p warp][event 0..7] after the 1024 slots above
+#define LA_TRP(t, pw_, ev)                                                                          \
+  do {                                                                                              \
+    if (la_trp != nullptr && (t) < 32 && (threadIdx.x & 31) == 0)                                   \
+      la_trp[1024 + ((t) * 8 + (pw_)) * 8 + (ev)] = clock64();                                       \
   } while (0)
 #else
 #define LA_TR(t, ev) \
@@ -105,6 +105,7 @@ constexpr size_t SMEM_BYTES = SMEM_TILES + 1024 /*align slack*/;
 
 struct TcArgs {
   int heads, n, seg_len, nseg, rev;
+  int sub_len, sub_per_seg, g_lo;  // state-only mode: blockIdx.x -> sub-segment (g_lo + x / sub_per_seg, x % ..)
   const double* lam;
   uint16_t* out;  // bf16 output (full mode)
   int64_t sb, sh, sn;
@@ -137,11 +138,24 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const uint32_t st_bf16 = smem + (uint32_t)(NSTAGE * 3 * TILE);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int seg = blockIdx.x, bh = blockIdx.y;
+#ifdef LA_TRACE
+  unsigned long long* const la_trp = (blockIdx.x == 0 && blockIdx.y == 0) ? g_la_trace : nullptr;
+#endif
+  const int bh = blockIdx.y;
   const int bi = bh / args.heads, hi = bh % args.heads;
-  const int p0 = seg * args.seg_len;
-  const int p1 = min(args.n, p0 + args.seg_len);
-  const int nchunks = (p1 - p0 + C - 1) / C;
+  // main pass: CTA = segment.  State-only: CTA = summary sub-segment, `seg` = its summary slot.
+  int seg, p0, p1;
+  if (STATE_ONLY) {
+    const int g = args.g_lo + (int)blockIdx.x / args.sub_per_seg, j = (int)blockIdx.x % args.sub_per_seg;
+    seg = g * args.sub_per_seg + j;
+    p0 = g * args.seg_len + j * args.sub_len;
+    p1 = min(min(args.n, (g + 1) * args.seg_len), p0 + args.sub_len);
+  } else {
+    seg = blockIdx.x;
+    p0 = seg * args.seg_len;
+    p1 = min(args.n, p0 + args.seg_len);
+  }
+  const int nchunks = p1 > p0 ? (p1 - p0 + C - 1) / C : 0;
   const int rev = args.rev;
 
   if (threadIdx.x == 0) {
@@ -203,6 +217,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const int r0 = chunk_row0(t);
         mbar_arrive_expect_tx(&bars.full[x][s], TILE);
         if (x == 0) LA_TR(t, 0);
+        if (x == 1) LA_TR(t, 16);
+        if (x == 2) LA_TR(t, 17);
         uint8_t* g = smem_gen + (s * 3 + x) * TILE;
         tma_load_4d(map, &bars.full[x][s], g, 0, r0, hi, bi);
         tma_load_4d(map, &bars.full[x][s], g + HALF, 64, r0, hi, bi);
@@ -584,7 +600,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       float* dst = nullptr;
       int T = 0;
       if (STATE_ONLY) {
-        dst = args.delta_out + ((int64_t)bh * args.nseg + seg) * D * D;
+        dst = args.delta_out + ((int64_t)bh * args.nseg * args.sub_per_seg + seg) * D * D;
       } else if (args.state_out != nullptr && (rev ? seg == 0 : seg == args.nseg - 1)) {
         dst = args.state_out + (int64_t)bh * D * D;
         T = args.out_T;
@@ -680,10 +696,13 @@ cudaError_t launch_tc(const PassDesc& p, cudaStream_t st) {
   a.state_out = reinterpret_cast<float*>(p.state_out);
   a.out_T = p.state_out_T;
   a.delta_out = reinterpret_cast<float*>(p.delta_out);
+  a.sub_len = p.sub_len;
+  a.sub_per_seg = p.sub_per_seg;
+  a.g_lo = p.g_lo;
   auto kern = tc_pass_kernel<STATE_ONLY>;
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
   if (err != cudaSuccess) return err;
-  dim3 grid(p.nseg, p.batch * p.heads);
+  dim3 grid(STATE_ONLY ? (p.g_hi - p.g_lo + 1) * p.sub_per_seg : p.nseg, p.batch * p.heads);
   kern<<<grid, NUM_THREADS, SMEM_BYTES, st>>>(ma, mb, mc, mo, a);
   return cudaGetLastError();
 }
@@ -719,13 +738,21 @@ bool tc_pointers_ok(const PassDesc& p) {
 // one-wave cap so it does not depend on n.
 Plan tc_plan(int64_t bh, int64_t n, int d, int64_t want_segments) {
   (void)d;
-  if (want_segments > 0) return make_plan(bh, n, C, want_segments, kNumSMs, 1);
+  if (want_segments > 0) {
+    Plan p = make_plan(bh, n, C, want_segments, kNumSMs, 1);
+    p.nsub_ws = (int)(2 * std::max<int64_t>(p.nseg_ws, kNumSMs / bh) + 2);
+    plan_subsegments(p, bh, kNumSMs, 2, p.nsub_ws);
+    return p;
+  }
   const int64_t nchunks = (n + C - 1) / C;
   const int64_t cap = std::max<int64_t>(1, kNumSMs / bh);
   int64_t nseg = 1;
   if (bh * 10 < kNumSMs * 6) nseg = std::min<int64_t>(cap, std::max<int64_t>(1, nchunks / 2));
   Plan p = make_plan(bh, n, C, nseg, kNumSMs, 1);
   p.nseg_ws = (int)cap;
+  p.nsub_ws = (int)(2 * cap + 2);
+  // summaries: one wave over the segments a scan needs, sub-segments of >= 2 chunks
+  plan_subsegments(p, bh, kNumSMs, 2, p.nsub_ws);
   return p;
 }
 

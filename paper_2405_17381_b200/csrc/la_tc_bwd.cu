@@ -33,6 +33,10 @@ namespace {
 
 using namespace ptx;
 
+#ifndef LA_PF
+#define LA_PF 0  // L2 prefetch distance in chunks (0: off)
+#endif
+
 constexpr int C = 128;
 constexpr int D = 128;
 constexpr int TILE = C * D * 2;
@@ -158,8 +162,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     if (lane < 4) {
       const CUtensorMap* map = lane == 0 ? &map_q : lane == 1 ? &map_do : lane == 2 ? &map_k : &map_v;
       const int nslot = lane < 2 ? 2 : 1;
+#if LA_PF > 0
+      for (int t = nslot; t < min(nchunks, LA_PF); ++t) {
+        tma_prefetch_l2_4d(map, 0, chunk_row0(t), hi, bi);
+        tma_prefetch_l2_4d(map, 64, chunk_row0(t), hi, bi);
+      }
+#endif
       for (int t = 0; t < nchunks; ++t) {
         const int s = nslot == 2 ? (t & 1) : 0;
+#if LA_PF > 0
+        if (t + LA_PF < nchunks && t + LA_PF >= nslot) {
+          tma_prefetch_l2_4d(map, 0, chunk_row0(t + LA_PF), hi, bi);
+          tma_prefetch_l2_4d(map, 64, chunk_row0(t + LA_PF), hi, bi);
+        }
+#endif
         uint64_t* full = lane == 0 ? &bars.full_q[s] : lane == 1 ? &bars.full_d[s] : lane == 2 ? &bars.full_k
                                                                                                   : &bars.full_v;
         uint64_t* empty = lane == 0 ? &bars.empty_q[s] : lane == 1 ? &bars.empty_d[s] : lane == 2 ? &bars.empty_k
