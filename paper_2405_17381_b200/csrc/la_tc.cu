@@ -81,9 +81,12 @@ constexpr uint32_t IDESC_KK = idesc_bf16(128, 128, 0, 0);    // A K-major, B K-m
 constexpr uint32_t IDESC_KMN = idesc_bf16(128, 128, 0, 1);   // A K-major (or TMEM), B MN-major
 constexpr uint32_t IDESC_MNMN = idesc_bf16(128, 128, 1, 1);  // A MN-major, B MN-major
 
+constexpr int NSTAGE_S = 3;  // state-only (summary) mode: no A / state tiles, so three stages of {B, C}
+constexpr int NSTAGE_MAX = 3;
+
 struct Bars {
-  uint64_t full[3][NSTAGE];   // TMA -> consumers, one ring per operand tile A, B, C (tx bytes)
-  uint64_t empty[3][NSTAGE];  // MMA commit after the tile's last reader -> TMA
+  uint64_t full[3][NSTAGE_MAX];   // TMA -> consumers, one ring per operand tile A, B, C (tx bytes)
+  uint64_t empty[3][NSTAGE_MAX];  // MMA commit after the tile's last reader -> TMA
   uint64_t s_full[2];      // MMA: S[t%2] done                 -> P warps, state warps
   uint64_t a_full[2];      // A~(t) in TMEM                    -> MMA (per buffer: P warps run a chunk ahead)
   uint64_t p_full[2];      // P(t) in TMEM                     -> MMA
@@ -93,7 +96,8 @@ struct Bars {
   uint64_t o_free;         // output warps read O              -> MMA
   uint64_t o_staged[2];    // bf16 O(t) staged in C's slot t%2 -> store lane (per slot: the output warps
                            // may stage a chunk ahead of the store lane)
-  uint64_t b_scaled;       // B~ in SMEM                       -> MMA
+  uint64_t b_scaled[NSTAGE_MAX];  // B~ in SMEM (per stage: in state-only mode the B warps are gated by
+                                 // the TMA only and may run a stage ahead) -> MMA
   uint64_t ds_full;        // MMA: state += B~^T C done        -> state warps
   uint64_t st_ready;       // bf16 state in SMEM, TMEM state pre-scaled -> MMA
   uint64_t ds_last;        // MMA: last chunk accumulated      -> state warps (state-only mode)
@@ -102,6 +106,7 @@ struct Bars {
 
 constexpr size_t SMEM_TILES = (size_t)NSTAGE * 3 * TILE + TILE;  // 224 KB
 constexpr size_t SMEM_BYTES = SMEM_TILES + 1024 /*align slack*/;
+constexpr size_t SMEM_BYTES_S = (size_t)NSTAGE_S * 2 * TILE + 1024;  // 193 KB
 
 struct TcArgs {
   int heads, n, seg_len, nseg, rev;
@@ -132,10 +137,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   __shared__ double s_lam;
   const uint32_t smem = (smem_u32(smem_raw) + 1023u) & ~1023u;
   uint8_t* smem_gen = smem_raw + (smem - smem_u32(smem_raw));
-  auto tile_a = [smem](int s) { return smem + (uint32_t)(s * 3 * TILE); };
-  auto tile_b = [smem](int s) { return smem + (uint32_t)(s * 3 * TILE + TILE); };
-  auto tile_c = [smem](int s) { return smem + (uint32_t)(s * 3 * TILE + 2 * TILE); };
-  const uint32_t st_bf16 = smem + (uint32_t)(NSTAGE * 3 * TILE);
+  constexpr int NS = STATE_ONLY ? NSTAGE_S : NSTAGE;  // ring depth
+  constexpr int NT = STATE_ONLY ? 2 : 3;              // tiles per stage: {A,} B, C
+  auto tile_a = [smem](int s) { return smem + (uint32_t)(s * NT * TILE); };
+  auto tile_b = [smem](int s) { return smem + (uint32_t)(s * NT * TILE + (NT - 2) * TILE); };
+  auto tile_c = [smem](int s) { return smem + (uint32_t)(s * NT * TILE + (NT - 1) * TILE); };
+  const uint32_t st_bf16 = smem + (uint32_t)(NSTAGE * 3 * TILE);  // main mode only
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #ifdef LA_TRACE
@@ -159,11 +166,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const int rev = args.rev;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < NSTAGE; ++s) {
+    for (int s = 0; s < NS; ++s) {
       for (int x = 0; x < 3; ++x) {
         mbar_init(&bars.full[x][s], 1);
         mbar_init(&bars.empty[x][s], 1);
       }
+      mbar_init(&bars.b_scaled[s], NUM_KV);
+    }
+    for (int s = 0; s < NSTAGE; ++s) {
       mbar_init(&bars.s_full[s], 1);
       mbar_init(&bars.p_full[s], NUM_P);
       mbar_init(&bars.a_full[s], NUM_P);
@@ -173,7 +183,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     mbar_init(&bars.o_free, NUM_O);
     mbar_init(&bars.o_staged[0], NUM_O);
     mbar_init(&bars.o_staged[1], NUM_O);
-    mbar_init(&bars.b_scaled, NUM_KV);
     mbar_init(&bars.ds_full, 1);
     mbar_init(&bars.x_done, 1);
     mbar_init(&bars.st_ready, NUM_KV);
@@ -212,14 +221,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     if (x < 3 && !(STATE_ONLY && x == 0)) {
       const CUtensorMap* map = x == 0 ? &map_a : (x == 1 ? &map_b : &map_c);
       for (int t = 0; t < nchunks; ++t) {
-        const int s = t % NSTAGE;
-        if (t >= NSTAGE) mbar_wait(&bars.empty[x][s], ((t / NSTAGE) - 1) & 1);
+        const int s = t % NS;
+        if (t >= NS) mbar_wait(&bars.empty[x][s], ((t / NS) - 1) & 1);
         const int r0 = chunk_row0(t);
         mbar_arrive_expect_tx(&bars.full[x][s], TILE);
         if (x == 0) LA_TR(t, 0);
         if (x == 1) LA_TR(t, 16);
         if (x == 2) LA_TR(t, 17);
-        uint8_t* g = smem_gen + (s * 3 + x) * TILE;
+        uint8_t* g = smem_gen + (s * NT + x - (3 - NT)) * TILE;
         tma_load_4d(map, &bars.full[x][s], g, 0, r0, hi, bi);
         tma_load_4d(map, &bars.full[x][s], g + HALF, 64, r0, hi, bi);
       }
@@ -266,7 +275,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         s_issued = 1;
       }
       for (int t = 0; t < nchunks; ++t) {
-        const int s = t % NSTAGE;
+        const int s = t % NS;
         const uint32_t b_addr = tile_b(s), c_addr = tile_c(s);
         const uint32_t sbuf = tmem + TM_S0 + (t & 1) * 128;
         if (!STATE_ONLY && s_issued == t + 1 && t + 1 < nchunks &&
@@ -275,7 +284,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           issue_s(t + 1);  // run ahead: S(t+1) as soon as its operands landed
           s_issued = t + 2;
         }
-        if (STATE_ONLY) mbar_wait(&bars.full[1][s], (t / NSTAGE) & 1);
+        if (STATE_ONLY) mbar_wait(&bars.full[1][s], (t / NS) & 1);
         // st_ready(t): bf16 state_{t-1} in SMEM and the TMEM state pre-scaled by lam^b.  State-only
         // mode folds the decay into B~ instead and accumulates straight onto the zeroed state.
         if (!STATE_ONLY || t == 0) mbar_wait(&bars.st_ready, t & 1);
@@ -293,8 +302,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           mma_commit(&bars.empty[0][s]);  // A's readers (S(t), the A~ build) are done
         }
         // state += B~^T C
-        mbar_wait(&bars.b_scaled, t & 1);
-        mbar_wait(&bars.full[2][s], (t / NSTAGE) & 1);
+        mbar_wait(&bars.b_scaled[s], (t / NS) & 1);
+        mbar_wait(&bars.full[2][s], (t / NS) & 1);
         LA_TR(t, 4);
         tc_fence_after();
 #pragma unroll
@@ -331,8 +340,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
       // Drain: every asynchronous tcgen05.commit arrival must land before this CTA retires, or it
       // would hit the barriers of the next CTA scheduled onto this SM's shared memory.
-      for (int t = max(0, nchunks - NSTAGE); t < nchunks; ++t) {
-        for (int x = STATE_ONLY ? 1 : 0; x < 3; ++x) mbar_wait(&bars.empty[x][t % NSTAGE], (t / NSTAGE) & 1);
+      for (int t = max(0, nchunks - NS); t < nchunks; ++t) {
+        for (int x = STATE_ONLY ? 1 : 0; x < 3; ++x) mbar_wait(&bars.empty[x][t % NS], (t / NS) & 1);
         if (STATE_ONLY && t == nchunks - 1) mbar_wait(&bars.ds_last, 0);
         if (!STATE_ONLY) mbar_wait(&bars.y_done[t & 1], (t >> 1) & 1);
       }
@@ -461,11 +470,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const int i = quad * 32 + lane;       // chunk row == TMEM lane
     const uint32_t o_cols = tmem + ((uint32_t)(quad * 32) << 16) + TM_O + hh * 64;
     for (int t = 0; t < nchunks; ++t) {
-      const int s = t % NSTAGE;
+      const int s = t % NS;
       const int r0 = chunk_row0(t);
       const int b = chunk_len(t);
       if (STATE_ONLY)
-        mbar_wait(&bars.full[1][s], (t / NSTAGE) & 1);
+        mbar_wait(&bars.full[1][s], (t / NS) & 1);
       else
         mbar_wait(&bars.s_full[t & 1], (t >> 1) & 1);
       if (warp == WARP_O && lane == 0) LA_TR(t, 11);
@@ -484,15 +493,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #endif
         const uint32_t isc2 = pack_bf16x2(isc, isc);
         const uint32_t base = tile_b(s) + hh * HALF + i * 128;
+#ifndef LA_KO_B
         uint4 x[8];
 #pragma unroll
         for (int m = 0; m < 8; ++m) x[m] = lds128(base + ((m ^ (i & 7)) << 4));
 #pragma unroll
         for (int m = 0; m < 8; ++m) sts128(base + ((m ^ (i & 7)) << 4), mul_bf16x2(x[m], isc2));
+#else
+        (void)isc2; (void)base;
+#endif
       }
       fence_proxy_async_smem();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&bars.b_scaled);
+      if (lane == 0) mbar_arrive(&bars.b_scaled[s]);
       if (warp == WARP_O && lane == 0) LA_TR(t, 12);
       if (STATE_ONLY) continue;
       // out = bf16(O): TMEM -> registers (then O's columns are released) -> C's SMEM slot -> TMA store
@@ -501,6 +514,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       if (warp == WARP_O && lane == 0) LA_TR(t, 8);
       tc_fence_after();
       uint32_t pk[32];
+#ifndef LA_KO_O
 #pragma unroll
       for (int cb = 0; cb < 2; ++cb) {
         float y[32];
@@ -509,15 +523,22 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
         for (int e = 0; e < 16; ++e) pk[cb * 16 + e] = pack_bf16x2(y[2 * e], y[2 * e + 1]);
       }
+#else
+      (void)o_cols;
+#pragma unroll
+      for (int e = 0; e < 32; ++e) pk[e] = 0u;
+#endif
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars.o_free);  // O's TMEM is free; the stores proceed from registers
+#ifndef LA_KO_O
       {
         const uint32_t base = tile_c(s) + hh * HALF;
 #pragma unroll
         for (int m = 0; m < 8; ++m)
           sts128(base + sw128(i, m), make_uint4(pk[4 * m], pk[4 * m + 1], pk[4 * m + 2], pk[4 * m + 3]));
       }
+#endif
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars.o_staged[s]);
@@ -581,6 +602,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       tc_fence_after();
       if (t + 1 < nchunks) {
         const float next_decay = pw[chunk_len(t + 1)];
+#ifndef LA_KO_ST
 #pragma unroll 1
         for (int q4 = 0; q4 < 4; ++q4) {
           float x[16];
@@ -588,6 +610,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           tmem_ld_wait();
           publish(x, q4, next_decay);
         }
+#else
+        (void)next_decay;
+#endif
         signal_ready();
       }
       if (warp == WARP_KV && lane == 0) LA_TR(t, 14);
@@ -700,10 +725,11 @@ cudaError_t launch_tc(const PassDesc& p, cudaStream_t st) {
   a.sub_per_seg = p.sub_per_seg;
   a.g_lo = p.g_lo;
   auto kern = tc_pass_kernel<STATE_ONLY>;
-  cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
+  const size_t smem_bytes = STATE_ONLY ? SMEM_BYTES_S : SMEM_BYTES;
+  cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes);
   if (err != cudaSuccess) return err;
   dim3 grid(STATE_ONLY ? (p.g_hi - p.g_lo + 1) * p.sub_per_seg : p.nseg, p.batch * p.heads);
-  kern<<<grid, NUM_THREADS, SMEM_BYTES, st>>>(ma, mb, mc, mo, a);
+  kern<<<grid, NUM_THREADS, smem_bytes, st>>>(ma, mb, mc, mo, a);
   return cudaGetLastError();
 }
 
