@@ -46,7 +46,7 @@
 extern "C" {
 #endif
 
-#define LA_ABI_VERSION 1
+#define LA_ABI_VERSION 2
 
 #if defined(__GNUC__)
 #define LA_API __attribute__((visibility("default")))
@@ -122,6 +122,58 @@ LA_API int la_fwd_state(const la_desc* desc, const void* k, const void* v,
 LA_API int la_bwd_state(const la_desc* desc, const void* q, const void* dout,
                  const double* lam, void* dkv_delta,
                  void* workspace, size_t workspace_bytes, void* stream);
+
+/* Recurrent decode, one token per sequence (replaces the per-(layer, head) update of
+ * decode_step, model.py:697-701):
+ *   kv <- lam * kv + k v^T      in place, [batch, heads, d, d] in the state dtype
+ *   o   = q . kv                after the update (the token attends to itself, as in la_fwd)
+ * desc->n must be 1; q, k, v, o are addressed with the desc's batch / head strides.  A prefill
+ * by la_fwd with kv_out, followed by la_decode steps, reproduces la_fwd over the whole sequence. */
+LA_API int la_decode(const la_desc* desc, const void* q, const void* k, const void* v,
+              const double* lam, void* kv, void* o, void* stream);
+
+/* ---- GLA layer stages around the attention core (model.py:365-453) -------------------------
+ * The GLA layer is  y = [srmsnorm(LA(rot(act(x Wq)), rot(act(x Wk)), x Wv)) * (x Wu)] Wo.
+ * The five projections stay library GEMMs; these entry points are the element-wise stages
+ * between them, on the model-native [batch, n, heads, d] layout (contiguous, width = heads * d)
+ * that la_fwd / la_bwd read directly:
+ *   la_gla_prologue      q = rot(act(qp)), k = rot(act(kp))        model.py:381-392,
+ *                        act (model.py:60-99), LRPE rot (positional.py:126-150) when theta != NULL
+ *   la_gla_prologue_bwd  dqp = act'(qp) rot^-1(dq), dkp likewise; dtheta += the angle gradient
+ *                        of q and k (positional.py:153-182, model.py:434-441); workspace sized by
+ *                        la_gla_workspace_bytes
+ *   la_gla_epilogue      gated = srmsnorm(a) * u (u NULL: no gate), rawnorm[row] = |a_row|
+ *                        (model.py:106-116, 402-404)
+ *   la_gla_epilogue_bwd  (da, du) from dgated, a, u, rawnorm (model.py:118-129, 417-426)
+ * theta: device doubles [d/2]; dtheta: device doubles [d/2], accumulated; rawnorm: [batch * n]
+ * in the accumulation type. */
+typedef enum la_act {
+  LA_ACT_NONE = 0,
+  LA_ACT_SWISH = 1,          /* x * sigmoid(x), the reference default gla_act (model.py:215) */
+  LA_ACT_ONE_PLUS_ELU = 2
+} la_act;
+
+typedef struct la_gla_desc {
+  int64_t batch;    /* >= 1                                                          */
+  int64_t n;        /* positions per sequence >= 1                                   */
+  int64_t heads;    /* >= 1                                                          */
+  int64_t d;        /* head dim >= 1 (even when theta is given)                      */
+  int32_t dtype;    /* la_dtype                                                      */
+  int32_t act;      /* la_act                                                        */
+  int64_t offset;   /* LRPE position of each sequence's first row (decode resumes)   */
+  double eps;       /* srmsnorm eps, the reference's SRMS_EPS = 1e-8 (model.py:48)   */
+} la_gla_desc;
+
+LA_API size_t la_gla_workspace_bytes(const la_gla_desc* desc);
+LA_API int la_gla_prologue(const la_gla_desc* desc, const void* qp, const void* kp, const double* theta,
+                    void* q, void* k, void* stream);
+LA_API int la_gla_prologue_bwd(const la_gla_desc* desc, const void* qp, const void* kp, const double* theta,
+                        const void* dq, const void* dk, void* dqp, void* dkp, double* dtheta,
+                        void* workspace, size_t workspace_bytes, void* stream);
+LA_API int la_gla_epilogue(const la_gla_desc* desc, const void* a, const void* u, void* gated,
+                    void* rawnorm, void* stream);
+LA_API int la_gla_epilogue_bwd(const la_gla_desc* desc, const void* dgated, const void* a, const void* u,
+                        const void* rawnorm, void* da, void* du, void* stream);
 
 /* Number of kernels la_fwd (which = 0), la_bwd (which = 1) or la_bwd given the
  * forward's segment states (which = 2) launches for this descriptor; -1 on a

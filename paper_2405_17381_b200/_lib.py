@@ -23,7 +23,11 @@ BACKENDS = {"auto": LA_BACKEND_AUTO, "simt": LA_BACKEND_SIMT, "tcgen05": LA_BACK
 
 # every symbol include/lightning_attn.h declares
 EXPORTS = ("la_workspace_bytes", "la_segment_count", "la_fwd", "la_bwd", "la_fwd_state", "la_bwd_state",
-           "la_launch_count", "la_last_error", "la_abi_version", "la_build_info")
+           "la_decode", "la_gla_workspace_bytes", "la_gla_prologue", "la_gla_prologue_bwd", "la_gla_epilogue",
+           "la_gla_epilogue_bwd", "la_launch_count", "la_last_error", "la_abi_version", "la_build_info")
+ABI_VERSION = 2
+LA_ACT_NONE, LA_ACT_SWISH, LA_ACT_ONE_PLUS_ELU = 0, 1, 2
+ACTS = {"none": LA_ACT_NONE, "swish": LA_ACT_SWISH, "one_plus_elu": LA_ACT_ONE_PLUS_ELU}
 
 
 class LaDesc(ctypes.Structure):
@@ -39,6 +43,21 @@ class LaDesc(ctypes.Structure):
         ("backend", c_int32),
         ("stride", c_int64 * 3),
         ("segments", c_int64),
+    ]
+
+
+class LaGlaDesc(ctypes.Structure):
+    """Mirror of ``la_gla_desc``."""
+
+    _fields_ = [
+        ("batch", c_int64),
+        ("n", c_int64),
+        ("heads", c_int64),
+        ("d", c_int64),
+        ("dtype", ctypes.c_int32),
+        ("act", ctypes.c_int32),
+        ("offset", c_int64),
+        ("eps", c_double),
     ]
 
 
@@ -84,6 +103,20 @@ def load() -> ctypes.CDLL:
     lib.la_fwd_state.restype = c_int
     lib.la_bwd_state.argtypes = [P, c_void_p, c_void_p, POINTER(c_double), c_void_p, c_void_p, c_size_t, c_void_p]
     lib.la_bwd_state.restype = c_int
+    lib.la_decode.argtypes = [P, c_void_p, c_void_p, c_void_p, POINTER(c_double), c_void_p, c_void_p, c_void_p]
+    lib.la_decode.restype = c_int
+    G = POINTER(LaGlaDesc)
+    lib.la_gla_workspace_bytes.argtypes = [G]
+    lib.la_gla_workspace_bytes.restype = c_size_t
+    lib.la_gla_prologue.argtypes = [G, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]
+    lib.la_gla_prologue.restype = c_int
+    lib.la_gla_prologue_bwd.argtypes = [G, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                        c_void_p, c_void_p, c_size_t, c_void_p]
+    lib.la_gla_prologue_bwd.restype = c_int
+    lib.la_gla_epilogue.argtypes = [G, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]
+    lib.la_gla_epilogue.restype = c_int
+    lib.la_gla_epilogue_bwd.argtypes = [G, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]
+    lib.la_gla_epilogue_bwd.restype = c_int
     lib.la_launch_count.argtypes = [P, c_int]
     lib.la_launch_count.restype = c_int
     lib.la_last_error.argtypes = []

@@ -16,6 +16,8 @@
 #include <cuda.h>
 
 #include "la_common.cuh"
+#include "la_decode.cuh"
+#include "la_gla.cuh"
 #include "la_scan.cuh"
 #include "la_simt.cuh"
 #include "la_tc.cuh"
@@ -381,6 +383,106 @@ int la_bwd_state(const la_desc* desc, const void* q, const void* dout, const dou
   return state_entry(desc, q, dout, 1, lam, dkv_delta, workspace, workspace_bytes, stream, "la_bwd_state");
 }
 
+int la_decode(const la_desc* desc, const void* q, const void* k, const void* v, const double* lam, void* kv,
+              void* o, void* stream) {
+  int rc = validate(desc);
+  if (rc != LA_OK) return rc;
+  if (desc->n != 1) return fail(LA_ERR_SHAPE, "la_decode advances one token per sequence: need n == 1, got n=%lld",
+                                (long long)desc->n);
+  if (!q || !k || !v || !kv || !o || !lam) return fail(LA_ERR_SHAPE, "la_decode: null q/k/v/kv/o/lam");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  bind_stream_context(st);
+  cudaError_t err = la::decode_launch(desc->dtype, (int)desc->batch, (int)desc->heads, (int)desc->d, desc->stride[0],
+                                      desc->stride[1], q, k, v, lam, kv, o, st);
+  if (err != cudaSuccess) return cuda_fail(err, "la_decode");
+  return LA_OK;
+}
+
+static int gla_prepare(const la_gla_desc* desc, bool need_even_d, la::GlaRows* g) {
+  if (desc == nullptr) return fail(LA_ERR_SHAPE, "null GLA descriptor");
+  if (desc->batch < 1 || desc->n < 1 || desc->heads < 1 || desc->d < 1)
+    return fail(LA_ERR_DOMAIN, "GLA stages need batch, n, heads, d >= 1");
+  if (desc->dtype != LA_F32 && desc->dtype != LA_F64 && desc->dtype != LA_BF16)
+    return fail(LA_ERR_DOMAIN, "dtype must be LA_F32, LA_F64 or LA_BF16, got %d", desc->dtype);
+  if (desc->act < LA_ACT_NONE || desc->act > LA_ACT_ONE_PLUS_ELU) return fail(LA_ERR_DOMAIN, "unknown act %d", desc->act);
+  if (desc->offset < 0) return fail(LA_ERR_DOMAIN, "position offset must be >= 0, got %lld", (long long)desc->offset);
+  if (!(desc->eps >= 0.0)) return fail(LA_ERR_DOMAIN, "eps must be >= 0");
+  if (need_even_d && desc->d % 2) return fail(LA_ERR_SHAPE, "rotation needs an even head dim, got d=%lld", (long long)desc->d);
+  if (desc->heads * desc->d > (int64_t)1 << 30 || desc->batch * desc->n > (int64_t)1 << 40)
+    return fail(LA_ERR_UNSUPPORTED, "GLA rows / width beyond this build's limits");
+  g->rows = desc->batch * desc->n;
+  g->n = (int)desc->n;
+  g->width = (int)(desc->heads * desc->d);
+  g->d = (int)desc->d;
+  g->dtype = desc->dtype;
+  g->act = desc->act;
+  g->offset = desc->offset;
+  return LA_OK;
+}
+
+size_t la_gla_workspace_bytes(const la_gla_desc* desc) {
+  la::GlaRows g;
+  if (gla_prepare(desc, false, &g) != LA_OK) return 0;
+  return la::gla_prologue_bwd_partial_bytes(g);
+}
+
+int la_gla_prologue(const la_gla_desc* desc, const void* qp, const void* kp, const double* theta, void* q, void* k,
+                    void* stream) {
+  la::GlaRows g;
+  int rc = gla_prepare(desc, theta != nullptr, &g);
+  if (rc != LA_OK) return rc;
+  if (!qp || !kp || !q || !k) return fail(LA_ERR_SHAPE, "la_gla_prologue: null qp/kp/q/k");
+  if (g.width % 2) return fail(LA_ERR_SHAPE, "la_gla_prologue: heads * d must be even");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  bind_stream_context(st);
+  cudaError_t err = la::gla_prologue(g, qp, kp, theta, q, k, st);
+  return err == cudaSuccess ? LA_OK : cuda_fail(err, "la_gla_prologue");
+}
+
+int la_gla_prologue_bwd(const la_gla_desc* desc, const void* qp, const void* kp, const double* theta, const void* dq,
+                        const void* dk, void* dqp, void* dkp, double* dtheta, void* workspace, size_t workspace_bytes,
+                        void* stream) {
+  la::GlaRows g;
+  int rc = gla_prepare(desc, theta != nullptr, &g);
+  if (rc != LA_OK) return rc;
+  if (!qp || !kp || !dq || !dk || !dqp || !dkp) return fail(LA_ERR_SHAPE, "la_gla_prologue_bwd: null operand");
+  if (g.width % 2) return fail(LA_ERR_SHAPE, "la_gla_prologue_bwd: heads * d must be even");
+  if (theta != nullptr) {
+    if (dtheta == nullptr) return fail(LA_ERR_SHAPE, "la_gla_prologue_bwd: theta given without dtheta");
+    const size_t need = la::gla_prologue_bwd_partial_bytes(g);
+    if (workspace == nullptr || workspace_bytes < need)
+      return fail(LA_ERR_SHAPE, "workspace too small: need %zu bytes, got %zu", need, workspace_bytes);
+  }
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  bind_stream_context(st);
+  cudaError_t err = la::gla_prologue_bwd(g, qp, kp, theta, dq, dk, dqp, dkp, workspace, dtheta, st);
+  return err == cudaSuccess ? LA_OK : cuda_fail(err, "la_gla_prologue_bwd");
+}
+
+int la_gla_epilogue(const la_gla_desc* desc, const void* a, const void* u, void* gated, void* rawnorm, void* stream) {
+  la::GlaRows g;
+  int rc = gla_prepare(desc, false, &g);
+  if (rc != LA_OK) return rc;
+  if (!a || !gated || !rawnorm) return fail(LA_ERR_SHAPE, "la_gla_epilogue: null a/gated/rawnorm");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  bind_stream_context(st);
+  cudaError_t err = la::gla_epilogue(g, a, u, gated, rawnorm, desc->eps, st);
+  return err == cudaSuccess ? LA_OK : cuda_fail(err, "la_gla_epilogue");
+}
+
+int la_gla_epilogue_bwd(const la_gla_desc* desc, const void* dgated, const void* a, const void* u, const void* rawnorm,
+                        void* da, void* du, void* stream) {
+  la::GlaRows g;
+  int rc = gla_prepare(desc, false, &g);
+  if (rc != LA_OK) return rc;
+  if (!dgated || !a || !rawnorm || !da || (u != nullptr && du == nullptr))
+    return fail(LA_ERR_SHAPE, "la_gla_epilogue_bwd: null operand");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  bind_stream_context(st);
+  cudaError_t err = la::gla_epilogue_bwd(g, dgated, a, u, rawnorm, da, du, desc->eps, st);
+  return err == cudaSuccess ? LA_OK : cuda_fail(err, "la_gla_epilogue_bwd");
+}
+
 int la_launch_count(const la_desc* desc, int which) {
   if (validate(desc) != LA_OK) return -1;
   int backend;
@@ -399,7 +501,7 @@ const char* la_last_error(void) { return g_last_error.c_str(); }
 int la_abi_version(void) { return LA_ABI_VERSION; }
 
 const char* la_build_info(void) {
-  return "lightning-attn b200: sm_100a, backends simt(f64/f32/bf16) + tcgen05(bf16)";
+  return "lightning-attn b200: sm_100a, backends simt(f64/f32/bf16) + tcgen05(bf16); decode; GLA stages";
 }
 
 }  // extern "C"

@@ -1,0 +1,93 @@
+// la_decode.cu -- one recurrent decode step over every (batch, head) state (model.py:669-709).
+//
+// The reference's decode_step updates each (layer, head) summary in place and reads the output
+// through it (model.py:697-701):
+//     kv <- lam * kv + k v^T        (d x d, state dtype)
+//     o   = q . kv                  (after the update: the token attends to itself, as in la_fwd)
+// so after a prefill of n tokens with kv_out = F(n) the decode continues exactly where la_fwd
+// stopped.  The step is bound by the state traffic (d^2 reads + d^2 writes per head), so one CTA per
+// (batch, head) streams its state once: a warp covers 32 consecutive columns of a row (coalesced
+// 128-byte accesses), eight warps split the rows, and the per-column partial dot products meet in
+// shared memory.
+#include "la_common.cuh"
+#include "la_decode.cuh"
+
+namespace la {
+
+namespace {
+
+constexpr int kDecThreads = 256;  // 8 warps: warp w owns rows w, w + 8, ...
+
+template <typename T, typename Tacc>
+__global__ void __launch_bounds__(kDecThreads) decode_kernel(const T* __restrict__ q, const T* __restrict__ k,
+                                                             const T* __restrict__ v, const double* __restrict__ lam,
+                                                             Tacc* __restrict__ kv, T* __restrict__ o, int heads,
+                                                             int d, int64_t sb, int64_t sh) {
+  __shared__ Tacc sq[128], sk[128], sv[128];
+  __shared__ Tacc part[kDecThreads / 32][128];
+  const int bh = blockIdx.x;
+  const int bi = bh / heads, hi = bh % heads;
+  const int64_t base = (int64_t)bi * sb + (int64_t)hi * sh;
+  for (int e = threadIdx.x; e < d; e += kDecThreads) {
+    sq[e] = (Tacc)Cvt<T>::to_f(q[base + e]);
+    sk[e] = (Tacc)Cvt<T>::to_f(k[base + e]);
+    sv[e] = (Tacc)Cvt<T>::to_f(v[base + e]);
+  }
+  __syncthreads();
+  const Tacc l = (Tacc)lam[hi];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  Tacc* st = kv + (int64_t)bh * d * d;
+  Tacc acc[4] = {0, 0, 0, 0};
+  for (int i = warp; i < d; i += kDecThreads / 32) {
+    const Tacc qi = sq[i], ki = sk[i];
+    Tacc* row = st + (int64_t)i * d;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int j = lane + 32 * c;
+      if (j < d) {
+        const Tacc x = l * row[j] + ki * sv[j];
+        row[j] = x;
+        acc[c] += qi * x;
+      }
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const int j = lane + 32 * c;
+    if (j < d) part[warp][j] = acc[c];
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < d; j += kDecThreads) {
+    Tacc s = 0;
+#pragma unroll
+    for (int w = 0; w < kDecThreads / 32; ++w) s += part[w][j];
+    o[base + j] = Cvt<T>::from_f(s);
+  }
+}
+
+}  // namespace
+
+cudaError_t decode_launch(int dtype, int batch, int heads, int d, int64_t sb, int64_t sh, const void* q,
+                          const void* k, const void* v, const double* lam, void* kv, void* o, cudaStream_t st) {
+  const dim3 grid((unsigned)(batch * heads));
+  switch (dtype) {
+    case LA_F64:
+      decode_kernel<double, double><<<grid, kDecThreads, 0, st>>>(
+          static_cast<const double*>(q), static_cast<const double*>(k), static_cast<const double*>(v), lam,
+          static_cast<double*>(kv), static_cast<double*>(o), heads, d, sb, sh);
+      break;
+    case LA_F32:
+      decode_kernel<float, float><<<grid, kDecThreads, 0, st>>>(
+          static_cast<const float*>(q), static_cast<const float*>(k), static_cast<const float*>(v), lam,
+          static_cast<float*>(kv), static_cast<float*>(o), heads, d, sb, sh);
+      break;
+    default:
+      decode_kernel<__nv_bfloat16, float><<<grid, kDecThreads, 0, st>>>(
+          static_cast<const __nv_bfloat16*>(q), static_cast<const __nv_bfloat16*>(k),
+          static_cast<const __nv_bfloat16*>(v), lam, static_cast<float*>(kv), static_cast<__nv_bfloat16*>(o), heads,
+          d, sb, sh);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace la

@@ -1,0 +1,24 @@
+// la_gla.cuh -- element-wise stages of the GLA layer around the attention core (la_gla.cu).
+#pragma once
+#include "la_common.cuh"
+
+namespace la {
+struct GlaRows {
+  int64_t rows;    // batch * n
+  int n;           // positions per sequence (LRPE position = row % n + offset)
+  int width;       // heads * d
+  int d;           // head dim (LRPE pairs within a head)
+  int dtype;       // la_dtype
+  int act;         // la_act
+  int64_t offset;  // LRPE position of each sequence's first row
+};
+size_t gla_prologue_bwd_partial_bytes(const GlaRows& g);
+cudaError_t gla_prologue(const GlaRows& g, const void* qp, const void* kp, const double* theta, void* q, void* k,
+                         cudaStream_t st);
+cudaError_t gla_prologue_bwd(const GlaRows& g, const void* qp, const void* kp, const double* theta, const void* dq,
+                             const void* dk, void* dqp, void* dkp, void* partial, double* dtheta, cudaStream_t st);
+cudaError_t gla_epilogue(const GlaRows& g, const void* a, const void* u, void* gated, void* rawnorm, double eps,
+                         cudaStream_t st);
+cudaError_t gla_epilogue_bwd(const GlaRows& g, const void* dgated, const void* a, const void* u, const void* rawnorm,
+                             void* da, void* du, double eps, cudaStream_t st);
+}  // namespace la

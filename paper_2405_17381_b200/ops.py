@@ -236,3 +236,126 @@ def launch_count(shape, dtype=torch.bfloat16, *, which="fwd", layout="bhnd", bac
         strides = (n * h * d, d, h * d)
     desc = _desc(Geometry(b, h, n, d, strides), dtype, None, backend, segments)
     return int(_lib.load().la_launch_count(ctypes.byref(desc), {"fwd": 0, "bwd": 1, "bwd_saved": 2}[which]))
+
+
+# ----------------------------------------------------------------------------------------------
+# Recurrent decode (model.py:669-709) and the GLA layer stages around the core (model.py:365-453)
+
+
+def la_decode(q, k, v, lam, kv, *, lam_dev=None):
+    """One decode step for every (batch, head): ``kv <- lam kv + k v^T`` in place, returns
+    ``o = q . kv`` (model.py:697-701).  q, k, v: [batch, heads, d]; kv: [batch, heads, d, d] in the
+    state dtype (fp32, or fp64 for fp64 operands), e.g. la_forward's kv_out after a prefill."""
+    for t, name in ((q, "Q"), (k, "K"), (v, "V")):
+        if not isinstance(t, torch.Tensor) or t.dim() != 3:
+            raise ShapeError(f"{name}: expected a [batch, heads, d] tensor")
+    (q4, k4, v4), g = _prep([q.unsqueeze(2), k.unsqueeze(2), v.unsqueeze(2)], "QKV", "bhnd")
+    if not isinstance(kv, torch.Tensor) or kv.shape != (g.batch, g.heads, g.d, g.d):
+        raise ShapeError(f"kv: expected shape {(g.batch, g.heads, g.d, g.d)}")
+    if kv.dtype != state_dtype(q.dtype) or not kv.is_contiguous() or kv.device != q.device:
+        raise ShapeError(f"kv: expected a contiguous {state_dtype(q.dtype)} tensor on {q.device} (updated in place)")
+    lib = _lib.load()
+    desc = _desc(g, q4.dtype, None, "auto", 0)
+    lam_dev = decay_tensor(lam, g.heads, q.device) if lam_dev is None else lam_dev
+    o = torch.empty_like(q4)
+    _lib.check(lib.la_decode(ctypes.byref(desc), _ptr(q4), _ptr(k4), _ptr(v4), _lam_ptr(lam_dev), _ptr(kv), _ptr(o),
+                             _stream(q.device)))
+    return o.squeeze(2)
+
+
+SRMS_EPS = 1e-8  # model.py:48
+
+
+def _gla_desc(x: torch.Tensor, heads: int, act: str, offset: int, eps: float) -> _lib.LaGlaDesc:
+    if x.dim() != 3:
+        raise ShapeError(f"expected a [batch, n, heads * d] tensor, got shape {tuple(x.shape)}")
+    if x.dtype not in _DTYPES:
+        raise DomainError(f"dtype must be float32, float64 or bfloat16, got {x.dtype}")
+    if not x.is_cuda:
+        raise DomainError("tensors must live on a CUDA device (no CPU path)")
+    if act not in _lib.ACTS:
+        raise DomainError(f"act must be one of {sorted(_lib.ACTS)}, got {act!r}")
+    b, n, w = x.shape
+    if heads < 1 or w % heads:
+        raise ShapeError(f"width {w} not divisible by heads={heads}")
+    desc = _lib.LaGlaDesc()
+    desc.batch, desc.n, desc.heads, desc.d = b, n, heads, w // heads
+    desc.dtype = _DTYPES[x.dtype]
+    desc.act = _lib.ACTS[act]
+    desc.offset = int(offset)
+    desc.eps = float(eps)
+    return desc
+
+
+def _rows(tensors, names):
+    first = tensors[0]
+    out = []
+    for t, name in zip(tensors, names):
+        if t is None:
+            out.append(None)
+            continue
+        if t.shape != first.shape or t.dtype != first.dtype or t.device != first.device:
+            raise ShapeError(f"{name}: shape/dtype/device {tuple(t.shape)}/{t.dtype}/{t.device} do not match "
+                             f"{tuple(first.shape)}/{first.dtype}/{first.device}")
+        out.append(t.contiguous())
+    return out
+
+
+def _theta(theta, d, device):
+    if theta is None:
+        return None
+    th = torch.as_tensor(theta, dtype=torch.float64).to(device).contiguous()
+    if th.shape != (d // 2,):
+        raise ShapeError(f"theta has shape {tuple(th.shape)}, expected ({d // 2},)")
+    return th
+
+
+def gla_prologue(qp, kp, heads, *, act="swish", theta=None, offset=0):
+    """q = rot(act(qp)), k = rot(act(kp)) on [batch, n, heads * d] rows (model.py:381-392)."""
+    qp, kp = _rows([qp, kp], ["qp", "kp"])
+    desc = _gla_desc(qp, heads, act, offset, SRMS_EPS)
+    th = _theta(theta, desc.d, qp.device)
+    q, k = torch.empty_like(qp), torch.empty_like(kp)
+    _lib.check(_lib.load().la_gla_prologue(ctypes.byref(desc), _ptr(qp), _ptr(kp), _ptr(th), _ptr(q), _ptr(k),
+                                           _stream(qp.device)))
+    return q, k
+
+
+def gla_prologue_backward(qp, kp, dq, dk, heads, *, act="swish", theta=None, offset=0, dtheta=None):
+    """(dqp, dkp) of gla_prologue; with theta, the angle gradient is accumulated into ``dtheta``
+    (fp64 [d/2], created when None) and returned as the third value."""
+    qp, kp, dq, dk = _rows([qp, kp, dq, dk], ["qp", "kp", "dq", "dk"])
+    desc = _gla_desc(qp, heads, act, offset, SRMS_EPS)
+    lib = _lib.load()
+    th = _theta(theta, desc.d, qp.device)
+    if th is not None and dtheta is None:
+        dtheta = torch.zeros(desc.d // 2, dtype=torch.float64, device=qp.device)
+    nbytes = lib.la_gla_workspace_bytes(ctypes.byref(desc)) if th is not None else 0
+    ws = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=qp.device)
+    dqp, dkp = torch.empty_like(qp), torch.empty_like(kp)
+    _lib.check(lib.la_gla_prologue_bwd(ctypes.byref(desc), _ptr(qp), _ptr(kp), _ptr(th), _ptr(dq), _ptr(dk),
+                                       _ptr(dqp), _ptr(dkp), _ptr(dtheta if th is not None else None), _ptr(ws),
+                                       nbytes, _stream(qp.device)))
+    return dqp, dkp, (dtheta if th is not None else None)
+
+
+def gla_epilogue(a, u, heads, *, eps=SRMS_EPS):
+    """gated = srmsnorm(a) * u (u None: no gate) over each row; returns (gated, rawnorm)."""
+    a, u = _rows([a, u], ["a", "u"])
+    desc = _gla_desc(a, heads, "none", 0, eps)
+    gated = torch.empty_like(a)
+    rawnorm = torch.empty(a.shape[0] * a.shape[1], dtype=state_dtype(a.dtype), device=a.device)
+    _lib.check(_lib.load().la_gla_epilogue(ctypes.byref(desc), _ptr(a), _ptr(u), _ptr(gated), _ptr(rawnorm),
+                                           _stream(a.device)))
+    return gated, rawnorm
+
+
+def gla_epilogue_backward(dgated, a, u, rawnorm, heads, *, eps=SRMS_EPS):
+    """(da, du) of gla_epilogue (du None when u is None)."""
+    dgated, a, u = _rows([dgated, a, u], ["dgated", "a", "u"])
+    desc = _gla_desc(a, heads, "none", 0, eps)
+    da = torch.empty_like(a)
+    du = torch.empty_like(a) if u is not None else None
+    _lib.check(_lib.load().la_gla_epilogue_bwd(ctypes.byref(desc), _ptr(dgated), _ptr(a), _ptr(u),
+                                               _ptr(rawnorm.contiguous()), _ptr(da), _ptr(du), _stream(a.device)))
+    return da, du

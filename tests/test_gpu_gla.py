@@ -1,0 +1,148 @@
+"""GLA layer stages (model.py:365-453) and recurrent decode (model.py:669-709) on the GPU against
+golden vectors produced by the real reference (tests/golden/make_gla_golden.py).
+
+Tolerances (scaled: max|got - want| / max|want|): fp64 1e-9 and fp32 1e-4 -- these are the parity
+proof.  bf16 (input, weights and every GEMM output rounded to bf16, fp32 accumulation) bounds the
+end-to-end rounding of five chained bf16 GEMMs around the core: 5e-2 on the output, 1.5e-1 on
+gradients (each passes through two more bf16-rounded GEMMs than the output); the LRPE angle
+gradient is not checked in bf16 -- it is a sum over positions of cancelling products of
+bf16-rounded values (positional.py:178-181), meaningful only from fp32 up.
+"""
+
+from pathlib import Path
+
+import numpy as np
+import pytest
+import torch
+
+GOLD = Path(__file__).resolve().parent / "golden" / "gla_golden.npz"
+CASES = ["rot_swish_gate", "norot_swish_gate", "rot_elu_nogate", "norot_none_gate"]
+TOL = {torch.float64: 1e-9, torch.float32: 1e-4, torch.bfloat16: 5e-2}
+GRAD_TOL = {torch.float64: 1e-9, torch.float32: 1e-4, torch.bfloat16: 1.5e-1}
+
+
+def _gold():
+    return np.load(GOLD)
+
+
+def test_gla_golden_fixture_complete():
+    g = _gold()
+    for c in CASES:
+        for key in ("x", "dy", "lam", "theta", "wq", "wk", "wv", "wu", "wo", "y", "dx", "dwq", "dwk", "dwv", "dwu",
+                    "dwo", "dtheta", "kv_prefill", "kv_final", "cfg", "act"):
+            assert f"{c}.{key}" in g.files, (c, key)
+
+
+def _scaled(got, want):
+    want = np.asarray(want)
+    return float(np.max(np.abs(np.asarray(got, dtype=np.float64) - want)) / max(np.max(np.abs(want)), 1e-30))
+
+
+def _case(g, c, dtype, dev):
+    dm, heads, n, layers, layer, rotate, gate, seed, n0 = (int(x) for x in g[f"{c}.cfg"])
+    t = lambda a: torch.tensor(np.asarray(a), dtype=dtype, device=dev)  # noqa: E731
+    from paper_2405_17381_b200.gla import GlaWeights
+    w = GlaWeights(wq=t(g[f"{c}.wq"]), wk=t(g[f"{c}.wk"]), wv=t(g[f"{c}.wv"]), wo=t(g[f"{c}.wo"]),
+                   wu=t(g[f"{c}.wu"]) if gate else None)
+    theta = torch.tensor(g[f"{c}.theta"], dtype=torch.float64, device=dev) if rotate else None
+    return dict(dm=dm, heads=heads, n=n, n0=n0, rotate=rotate, gate=gate, w=w, theta=theta,
+                lam=[float(x) for x in g[f"{c}.lam"]], act=str(g[f"{c}.act"]), t=t)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("case", CASES)
+def test_gla_forward_backward_matches_reference(case, dtype):
+    from paper_2405_17381_b200.gla import gla_forward
+    g = _gold()
+    dev = torch.device("cuda", 0)
+    cs = _case(g, case, dtype, dev)
+    x = cs["t"](g[f"{case}.x"])[None].repeat(2, 1, 1).requires_grad_(True)  # batch 2: two copies
+    params = [cs["w"].wq, cs["w"].wk, cs["w"].wv, cs["w"].wo] + ([cs["w"].wu] if cs["gate"] else [])
+    for p in params:
+        p.requires_grad_(True)
+    theta = cs["theta"].clone().requires_grad_(True) if cs["rotate"] else None
+    y = gla_forward(x, cs["w"], cs["lam"], cs["heads"], act=cs["act"], theta=theta)
+    dy = cs["t"](g[f"{case}.dy"])[None].repeat(2, 1, 1)
+    y.backward(dy)
+    tol = TOL[dtype]
+    errs = {"y": max(_scaled(y[b].detach().double().cpu(), g[f"{case}.y"]) for b in range(2)),
+            # each batch copy carries the same upstream gradient: weight grads are twice the reference's
+            "dx": max(_scaled(x.grad[b].double().cpu(), g[f"{case}.dx"]) for b in range(2))}
+    names = ["wq", "wk", "wv", "wo"] + (["wu"] if cs["gate"] else [])
+    for nm, p in zip(names, params):
+        errs[f"d{nm}"] = _scaled(p.grad.double().cpu() / 2, g[f"{case}.d{nm}"])
+    if cs["rotate"] and dtype != torch.bfloat16:
+        errs["dtheta"] = _scaled(theta.grad.double().cpu() / 2, g[f"{case}.dtheta"])
+    bad = {k: v for k, v in errs.items() if not v <= (tol if k == "y" else GRAD_TOL[dtype])}
+    assert not bad, f"{case} {dtype}: {errs}"
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+@pytest.mark.parametrize("case", CASES)
+def test_gla_prefill_then_decode_matches_reference(case, dtype):
+    """Prefill n0 rows with la_fwd (kv_out), then la_decode the rest one token at a time: outputs
+    equal the reference layer's rows, the summaries equal the reference decode's (model.py:697-701)."""
+    from paper_2405_17381_b200.gla import DecodeState
+    g = _gold()
+    dev = torch.device("cuda", 0)
+    cs = _case(g, case, dtype, dev)
+    x = cs["t"](g[f"{case}.x"])[None]
+    n0, n = cs["n0"], cs["n"]
+    with torch.no_grad():
+        y0, st = DecodeState.from_prefill(x[:, :n0], cs["w"], cs["lam"], cs["heads"], act=cs["act"], theta=cs["theta"])
+        tol = TOL[dtype]
+        assert _scaled(y0[0].double().cpu(), g[f"{case}.y"][:n0]) <= tol
+        assert _scaled(st.kv[0].double().cpu(), g[f"{case}.kv_prefill"]) <= tol
+        ys = [st.step(x[:, t], cs["w"], cs["lam"], cs["heads"], act=cs["act"], theta=cs["theta"]) for t in range(n0, n)]
+        got = torch.stack(ys, 1)[0].double().cpu()
+    assert _scaled(got, g[f"{case}.y"][n0:]) <= tol
+    assert _scaled(st.kv[0].double().cpu(), g[f"{case}.kv_final"]) <= tol
+    assert st.position == n
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32, torch.float64])
+def test_decode_chains_with_forward(dtype):
+    """la_fwd over n tokens == la_fwd over the first n0 (kv_out) + la_decode steps, any dtype / d."""
+    from paper_2405_17381_b200 import ops
+    dev = torch.device("cuda", 0)
+    torch.manual_seed(0)
+    b, h, n, n0 = 3, 4, 40, 25
+    for d in (16, 64, 128, 100):
+        q, k, v = (torch.randn(b, h, n, d, device=dev, dtype=torch.float64).to(dtype) * d ** -0.5 for _ in range(3))
+        lam = [1.0, 0.99, 0.9, 0.3]
+        full, kv_n = ops.la_forward(q, k, v, lam, want_state=True)
+        _, kv = ops.la_forward(q[:, :, :n0], k[:, :, :n0], v[:, :, :n0], lam, want_state=True)
+        outs = [ops.la_decode(q[:, :, t], k[:, :, t], v[:, :, t], lam, kv) for t in range(n0, n)]
+        got = torch.stack(outs, 2)
+        tol = {torch.float64: 1e-10, torch.float32: 1e-4, torch.bfloat16: 2e-2}[dtype]
+        ref = full[:, :, n0:].double()
+        assert float((got.double() - ref).abs().max() / ref.abs().max()) <= tol, d
+        assert float((kv - kv_n).abs().max() / kv_n.abs().max()) <= tol, d
+
+
+@pytest.mark.gpu
+def test_gla_epilogue_zero_rows_and_errors():
+    """srmsnorm's eps branch (rows with |x| < eps are scaled linearly, model.py:106-129) and the
+    reference-class errors of the stage entry points."""
+    from paper_2405_17381_b200 import ops
+    from paper_2405_17381_b200.errors import DomainError, ShapeError
+    dev = torch.device("cuda", 0)
+    a = torch.zeros(1, 3, 8, dtype=torch.float64, device=dev)
+    a[0, 1] = 1e-12
+    a[0, 2] = torch.arange(8, dtype=torch.float64)
+    gated, raw = ops.gla_epilogue(a, None, 2)
+    want = a[0, 2] * (8 ** 0.5) / a[0, 2].norm()
+    assert torch.allclose(gated[0, 2], want) and torch.all(gated[0, 0] == 0)
+    assert torch.allclose(gated[0, 1], a[0, 1] * 8 ** 0.5 / 1e-8)
+    dg = torch.randn_like(a)
+    da, _ = ops.gla_epilogue_backward(dg, a, None, raw, 2)
+    assert torch.allclose(da[0, 1], dg[0, 1] * 8 ** 0.5 / 1e-8)  # below eps: linear, no projection term
+    with pytest.raises(ShapeError):
+        ops.gla_epilogue(a, None, 3)
+    with pytest.raises(DomainError):
+        ops.gla_prologue(a, a, 2, act="gelu")
+    with pytest.raises(ShapeError):
+        ops.gla_prologue(a, a, 2, theta=torch.ones(3))
