@@ -196,6 +196,30 @@ void bind_stream_context(cudaStream_t st) {
   }
 }
 
+// A side stream (+ fork / join events) per device and calling thread, for independent passes that
+// can share the GPU: the backward's adjoint summaries run beside its dq pass.  Stream-ordered
+// fork / join, so it composes with the caller's stream and with CUDA graph capture.
+struct SideStream {
+  cudaStream_t stream = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+
+cudaError_t side_stream(SideStream** out) {
+  thread_local SideStream res[64];
+  int dev = 0;
+  cudaError_t err = cudaGetDevice(&dev);
+  if (err != cudaSuccess) return err;
+  if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+  SideStream& r = res[dev];
+  if (r.stream == nullptr) {
+    if ((err = cudaStreamCreateWithFlags(&r.stream, cudaStreamNonBlocking)) != cudaSuccess) return err;
+    if ((err = cudaEventCreateWithFlags(&r.fork, cudaEventDisableTiming)) != cudaSuccess) return err;
+    if ((err = cudaEventCreateWithFlags(&r.join, cudaEventDisableTiming)) != cudaSuccess) return err;
+  }
+  *out = &r;
+  return cudaSuccess;
+}
+
 struct Prepared {
   int backend;
   la::Plan plan;
@@ -284,13 +308,6 @@ int la_bwd(const la_desc* desc, const void* q, const void* k, const void* v, con
   p.rev = 0;
   p.state_in = kv_in;
   p.state_in_T = 1;
-  if (split && fwd_seg_states != nullptr) {
-    err = main_pass(pr.backend, desc->dtype, p, fwd_seg_states, 1, st);
-  } else {
-    if (split) err = segment_states(pr.backend, desc->dtype, p, delta, seg_in, st);
-    if (err == cudaSuccess) err = main_pass(pr.backend, desc->dtype, p, seg_in, 0, st);
-  }
-  if (err != cudaSuccess) return cuda_fail(err, "la_bwd dq");
   // sweep 2 (kernels.py:320-333): dk = rev(v, do, q) carries dkv^T, dv = rev(k, q, do) carries dkv --
   // one set of segment states (over q, do) serves both passes
   la::PassDesc pd = base;
@@ -298,8 +315,27 @@ int la_bwd(const la_desc* desc, const void* q, const void* k, const void* v, con
   pd.c = dout;
   pd.rev = 1;
   pd.state_in = dkv_in;
-  if (split && (err = segment_states(pr.backend, desc->dtype, pd, delta, seg_in, st)) != cudaSuccess)
-    return cuda_fail(err, "la_bwd dkv states");
+  if (split && fwd_seg_states != nullptr) {
+    // the dq pass needs only the forward's segment states, so the adjoint summaries (the workspace's
+    // only user) run on a side stream beside it: each alone leaves SMs idle
+    SideStream* side = nullptr;
+    if ((err = side_stream(&side)) != cudaSuccess) return cuda_fail(err, "la_bwd side stream");
+    if ((err = cudaEventRecord(side->fork, st)) != cudaSuccess ||
+        (err = cudaStreamWaitEvent(side->stream, side->fork, 0)) != cudaSuccess)
+      return cuda_fail(err, "la_bwd fork");
+    if ((err = segment_states(pr.backend, desc->dtype, pd, delta, seg_in, side->stream)) != cudaSuccess)
+      return cuda_fail(err, "la_bwd dkv states");
+    if ((err = cudaEventRecord(side->join, side->stream)) != cudaSuccess) return cuda_fail(err, "la_bwd join");
+    if ((err = main_pass(pr.backend, desc->dtype, p, fwd_seg_states, 1, st)) != cudaSuccess)
+      return cuda_fail(err, "la_bwd dq");
+    if ((err = cudaStreamWaitEvent(st, side->join, 0)) != cudaSuccess) return cuda_fail(err, "la_bwd join");
+  } else {
+    if (split) err = segment_states(pr.backend, desc->dtype, p, delta, seg_in, st);
+    if (err == cudaSuccess) err = main_pass(pr.backend, desc->dtype, p, seg_in, 0, st);
+    if (err != cudaSuccess) return cuda_fail(err, "la_bwd dq");
+    if (split && (err = segment_states(pr.backend, desc->dtype, pd, delta, seg_in, st)) != cudaSuccess)
+      return cuda_fail(err, "la_bwd dkv states");
+  }
   if (pr.backend == LA_BACKEND_TCGEN05) {
     // one fused sweep for dk and dv (la_tc_bwd.cu): q, k, v, do read once, one state update
     p = base;

@@ -14,8 +14,9 @@ out = {}
 for b, n, seg in cases:
     q, k, v, do = (torch.randn(b, H, n, D, device=dev, dtype=torch.bfloat16) * D ** -0.5 for _ in range(4))
     res = {}
-    for name, fn in (("fwd", lambda: ops.la_forward(q, k, v, lams, segments=seg)),
-                     ("bwd", lambda: ops.la_backward(q, k, v, do, lams, segments=seg))):
+    _, fst = ops.la_forward(q, k, v, lams, segments=seg, want_seg_states=True)
+    for name, fn in (("fwd", lambda: ops.la_forward(q, k, v, lams, segments=seg, want_seg_states=True)),
+                     ("bwd", lambda: ops.la_backward(q, k, v, do, lams, segments=seg, fwd_seg_states=fst))):
         for _ in range(3): fn()
         ts = []
         for _ in range(7):
