@@ -199,6 +199,9 @@ def run_ours(args) -> None:
             dist.destroy_process_group()
         return
     cpu = cpu_baseline(args.cpu_seconds) if (world == 1 and not args.no_cpu) else None
+    del inputs
+    torch.cuda.empty_cache()
+    rows = None if args.no_rows else measure_rows(ops, device, stream, pk)
     flat = sweep[str(seq_lens[-1])]["tokens_per_s"] / sweep[str(seq_lens[0])]["tokens_per_s"]
     line = {
         "metric": METRIC, "value": round(value), "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -217,10 +220,79 @@ def run_ours(args) -> None:
         "e2e": e2e,
         "clocks": clock,
         "cpu_baseline": cpu,
+        "rows": rows,
     }
     print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()
+
+
+def _time_ms(fn, stream, reps=10, warm=3) -> float:
+    import torch
+
+    for _ in range(warm):
+        fn()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+    for a, b in evs:
+        a.record(stream)
+        fn()
+        b.record(stream)
+    torch.cuda.synchronize()
+    return statistics.median(a.elapsed_time(b) for a, b in evs)
+
+
+def measure_rows(ops, device, stream, pk) -> dict:
+    """SURVEY.md §8(f) rows at the TNL-1B shape (d_model 2048 = 16 heads x 128), bf16:
+    recurrent decode (state traffic vs HBM peak), the GLA layer's element-wise stages (bytes moved
+    vs HBM peak), and the whole GLA layer fwd+bwd (cuBLAS projections + these kernels + the core)."""
+    import torch
+
+    from paper_2405_17381_b200 import gla
+    from paper_2405_17381_b200.positional import decay_rate
+
+    out = {}
+    g = torch.Generator(device=device).manual_seed(7)
+    rnd = lambda *shape: (torch.randn(*shape, device=device, generator=g) * 0.5).to(torch.bfloat16)  # noqa: E731
+    lam = [decay_rate(h, 1, H, L_LAYERS) for h in range(1, H + 1)]
+    # decode: 64 sequences x 16 heads, one token each per step; fp32 states read + written once
+    bsz = 64
+    q, k, v = rnd(bsz, H, D), rnd(bsz, H, D), rnd(bsz, H, D)
+    kv = torch.zeros(bsz, H, D, D, device=device, dtype=torch.float32)
+    lam_dev = ops.decay_tensor(lam, H, device)
+    ms = _time_ms(lambda: ops.la_decode(q, k, v, None, kv, lam_dev=lam_dev), stream, reps=50)
+    state_bytes = bsz * H * D * D * 4 * 2
+    out["decode"] = {"batch": bsz, "heads": H, "head_dim": D, "ms_per_step": round(ms, 4),
+                     "tokens_per_s": round(bsz / (ms / 1e3)), "state_gbs": round(state_bytes / (ms / 1e3) / 1e9, 1),
+                     "frac_hbm": round(state_bytes / (ms / 1e3) / 1e9 / pk["hbm_gbs"], 3)}
+    # GLA stages on [8, 8192, 2048] (64K tokens), LRPE on
+    b, n, w = 8, 8192, H * D
+    row_bytes = b * n * w * 2
+    qp, kp, a, u, dgd = (rnd(b, n, w) for _ in range(5))
+    theta = torch.tensor([10000.0 ** (-2.0 * j / D) for j in range(D // 2)], dtype=torch.float64, device=device)
+    stages = {}
+    ms = _time_ms(lambda: ops.gla_prologue(qp, kp, H, theta=theta), stream)
+    stages["prologue"] = (ms, 4 * row_bytes)
+    gated, raw = ops.gla_epilogue(a, u, H)
+    ms = _time_ms(lambda: ops.gla_epilogue(a, u, H), stream)
+    stages["epilogue"] = (ms, 3 * row_bytes)
+    ms = _time_ms(lambda: ops.gla_epilogue_backward(dgd, a, u, raw, H), stream)
+    stages["epilogue_bwd"] = (ms, 5 * row_bytes)
+    ms = _time_ms(lambda: ops.gla_prologue_backward(qp, kp, a, u, H, theta=theta), stream)
+    stages["prologue_bwd"] = (ms, 6 * row_bytes)
+    out["gla_stages"] = {k: {"ms": round(t, 4), "gbs": round(by / (t / 1e3) / 1e9, 1),
+                             "frac_hbm": round(by / (t / 1e3) / 1e9 / pk["hbm_gbs"], 3)} for k, (t, by) in stages.items()}
+    # the whole GLA layer, fwd + bwd through autograd
+    x = rnd(b, n, w).requires_grad_(True)
+    ws = gla.GlaWeights(*(rnd(w, w).mul_(w ** -0.5 * 2).requires_grad_(True) for _ in range(5)))
+
+    def layer():
+        y = gla.gla_forward(x, ws, lam, H, theta=theta)
+        y.backward(dgd)
+
+    ms = _time_ms(layer, stream, reps=5)
+    out["gla_layer"] = {"shape": [b, n, w], "ms_fwd_bwd": round(ms, 3), "tokens_per_s": round(b * n / (ms / 1e3)),
+                        "path": "cuBLAS projections + la_gla_* stages + la_fwd/la_bwd core (LRPE on, gate on)"}
+    return out
 
 
 def pass_roofline(ops, tensors, lam_dev, stream, pk) -> dict:
@@ -250,8 +322,13 @@ def pass_roofline(ops, tensors, lam_dev, stream, pk) -> dict:
             "shape": list(q.shape), "peak_source": pk["source"]}
 
 
-def run_e2e(ops, seq_lens, tokens, lam_dev, device, steps, world) -> dict:
-    """Same metric through the public API with pinned HOST buffers, H2D + D2H inside the timed region."""
+def run_e2e(ops, seq_lens, tokens, lam_dev, device, steps, world, pieces=4) -> dict:
+    """Same metric through the public API with pinned HOST buffers, H2D + D2H inside the timed region.
+
+    Each n's batch is cut into ``pieces`` independent (batch or head) slices, pipelined over three
+    streams: H2D of slice i+1 and D2H of slice i-1 overlap the kernels of slice i (PCIe is full
+    duplex), so the step is bounded by the link, not by copy + compute + copy in series.
+    """
     import torch
 
     maxel = max(tokens.values()) * H * D
@@ -259,33 +336,61 @@ def run_e2e(ops, seq_lens, tokens, lam_dev, device, steps, world) -> dict:
     host_out = [torch.empty(maxel, dtype=torch.bfloat16, pin_memory=True) for _ in range(4)]
     for t in host_in:
         t.normal_(0, D ** -0.5)
-    stream = torch.cuda.current_stream(device)
+    comp = torch.cuda.current_stream(device)
+    h2d_s, d2h_s = torch.cuda.Stream(device), torch.cuda.Stream(device)
+
+    def slices(n):
+        b = tokens[n] // n
+        views = [h[:tokens[n] * H * D].view(b, H, n, D) for h in host_in + host_out]
+        if b > 1:  # batch slices (contiguous in host memory)
+            m = min(pieces, b)
+            cut = [(i * b // m, (i + 1) * b // m) for i in range(m)]
+            return [([v[lo:hi] for v in views], lam_dev) for lo, hi in cut if hi > lo]
+        cut = [(i * H // pieces, (i + 1) * H // pieces) for i in range(pieces)]  # batch 1: head slices (contiguous)
+        return [([v[:, lo:hi] for v in views], lam_dev[lo:hi]) for lo, hi in cut if hi > lo]
 
     def one(n):
-        b = tokens[n] // n
-        el = tokens[n] * H * D
-        dev_in = [h[:el].view(b, H, n, D).to(device, non_blocking=True) for h in host_in]
-        o, seg = ops.la_forward(*dev_in[:3], None, lam_dev=lam_dev, want_seg_states=True)
-        dq, dk, dv = ops.la_backward(*dev_in, None, lam_dev=lam_dev, fwd_seg_states=seg)
-        for h, t in zip(host_out, (o, dq, dk, dv)):
-            h[:el].view(b, H, n, D).copy_(t, non_blocking=True)
-        return 4 * el * 2, 4 * el * 2
+        moved = 0
+        for sl, lam in slices(n):
+            hin, hout = sl[:4], sl[4:]
+            with torch.cuda.stream(h2d_s):
+                dev_in = [h.to(device, non_blocking=True) for h in hin]
+                ready = torch.cuda.Event()
+                ready.record(h2d_s)
+            comp.wait_event(ready)
+            o, seg = ops.la_forward(*dev_in[:3], None, lam_dev=lam, want_seg_states=True)
+            dq, dk, dv = ops.la_backward(*dev_in, None, lam_dev=lam, fwd_seg_states=seg)
+            done = torch.cuda.Event()
+            done.record(comp)
+            with torch.cuda.stream(d2h_s):
+                d2h_s.wait_event(done)
+                for h, t in zip(hout, (o, dq, dk, dv)):
+                    h.copy_(t, non_blocking=True)
+            for t in dev_in:
+                t.record_stream(comp)
+            for t in (o, dq, dk, dv):
+                t.record_stream(d2h_s)
+            moved += sum(t.numel() * 2 for t in hin)
+        return moved, moved
 
-    one(seq_lens[0])
+    for n in seq_lens:  # warm the caching allocator's pools of all three streams at every size
+        one(n)
     torch.cuda.synchronize()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     h2d = d2h = 0
-    a.record(stream)
+    a.record(comp)
     for _ in range(steps):
         for n in seq_lens:
             i, o = one(n)
             h2d, d2h = h2d + i, d2h + o
-    b.record(stream)
+    comp.wait_stream(d2h_s)
+    b.record(comp)
     torch.cuda.synchronize()
     ms = a.elapsed_time(b)
     value = sum(tokens.values()) * steps * world / (ms / 1e3)
     return {"value": round(value), "unit": UNIT, "h2d_bytes_per_step": h2d // steps, "d2h_bytes_per_step": d2h // steps,
-            "steps": steps, "path": "ops.la_forward/la_backward (C ABI) from pinned host buffers"}
+            "steps": steps, "path": "ops.la_forward/la_backward (C ABI) from pinned host buffers, "
+                                    f"{pieces} slices per n pipelined over H2D / compute / D2H streams"}
 
 
 # ----------------------------------------------------------------------------
@@ -390,6 +495,7 @@ def main() -> None:
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-rows", action="store_true", help="skip the decode / GLA-stage / GLA-layer measurements")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")

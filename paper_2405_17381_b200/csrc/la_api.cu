@@ -446,6 +446,10 @@ static int gla_prepare(const la_gla_desc* desc, bool need_even_d, la::GlaRows* g
   if (need_even_d && desc->d % 2) return fail(LA_ERR_SHAPE, "rotation needs an even head dim, got d=%lld", (long long)desc->d);
   if (desc->heads * desc->d > (int64_t)1 << 30 || desc->batch * desc->n > (int64_t)1 << 40)
     return fail(LA_ERR_UNSUPPORTED, "GLA rows / width beyond this build's limits");
+  const int64_t vec = 16 / (desc->dtype == LA_F64 ? 8 : desc->dtype == LA_F32 ? 4 : 2);
+  if ((desc->heads * desc->d) % vec)
+    return fail(LA_ERR_UNSUPPORTED, "GLA stages need heads * d to be a multiple of %lld (16-byte rows), got %lld",
+                (long long)vec, (long long)(desc->heads * desc->d));
   g->rows = desc->batch * desc->n;
   g->n = (int)desc->n;
   g->width = (int)(desc->heads * desc->d);

@@ -18,7 +18,8 @@ namespace {
 
 constexpr int kDecThreads = 256;  // 8 warps: warp w owns rows w, w + 8, ...
 
-template <typename T, typename Tacc>
+// VW state columns per thread (16-byte accesses when the head dim allows, else 1)
+template <typename T, typename Tacc, int VW>
 __global__ void __launch_bounds__(kDecThreads) decode_kernel(const T* __restrict__ q, const T* __restrict__ k,
                                                              const T* __restrict__ v, const double* __restrict__ lam,
                                                              Tacc* __restrict__ kv, T* __restrict__ o, int heads,
@@ -37,24 +38,45 @@ __global__ void __launch_bounds__(kDecThreads) decode_kernel(const T* __restrict
   const Tacc l = (Tacc)lam[hi];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   Tacc* st = kv + (int64_t)bh * d * d;
-  Tacc acc[4] = {0, 0, 0, 0};
+  constexpr int NC = VW == 1 ? 4 : 1;  // column groups per lane: 4 x 32 scalars, or one 32 x VW vector
+  Tacc acc[NC][VW];
+#pragma unroll
+  for (int c = 0; c < NC; ++c)
+#pragma unroll
+    for (int e = 0; e < VW; ++e) acc[c][e] = 0;
+#pragma unroll 4
   for (int i = warp; i < d; i += kDecThreads / 32) {
     const Tacc qi = sq[i], ki = sk[i];
     Tacc* row = st + (int64_t)i * d;
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const int j = lane + 32 * c;
-      if (j < d) {
-        const Tacc x = l * row[j] + ki * sv[j];
-        row[j] = x;
-        acc[c] += qi * x;
+    for (int c = 0; c < NC; ++c) {
+      const int j0 = VW == 1 ? lane + 32 * c : lane * VW;
+      if (j0 < d) {
+        Tacc x[VW];
+        if (VW > 1) {
+          *reinterpret_cast<uint4*>(x) = *reinterpret_cast<const uint4*>(row + j0);
+        } else {
+          x[0] = row[j0];
+        }
+#pragma unroll
+        for (int e = 0; e < VW; ++e) {
+          x[e] = l * x[e] + ki * sv[j0 + e];
+          acc[c][e] += qi * x[e];
+        }
+        if (VW > 1) {
+          *reinterpret_cast<uint4*>(row + j0) = *reinterpret_cast<const uint4*>(x);
+        } else {
+          row[j0] = x[0];
+        }
       }
     }
   }
 #pragma unroll
-  for (int c = 0; c < 4; ++c) {
-    const int j = lane + 32 * c;
-    if (j < d) part[warp][j] = acc[c];
+  for (int c = 0; c < NC; ++c) {
+    const int j0 = VW == 1 ? lane + 32 * c : lane * VW;
+#pragma unroll
+    for (int e = 0; e < VW; ++e)
+      if (j0 + e < d) part[warp][j0 + e] = acc[c][e];
   }
   __syncthreads();
   for (int j = threadIdx.x; j < d; j += kDecThreads) {
@@ -70,22 +92,39 @@ __global__ void __launch_bounds__(kDecThreads) decode_kernel(const T* __restrict
 cudaError_t decode_launch(int dtype, int batch, int heads, int d, int64_t sb, int64_t sh, const void* q,
                           const void* k, const void* v, const double* lam, void* kv, void* o, cudaStream_t st) {
   const dim3 grid((unsigned)(batch * heads));
+  // 16-byte state accesses when a warp's 32 vectors span exactly one row (d = 128 fp32, d = 64 fp64)
   switch (dtype) {
     case LA_F64:
-      decode_kernel<double, double><<<grid, kDecThreads, 0, st>>>(
-          static_cast<const double*>(q), static_cast<const double*>(k), static_cast<const double*>(v), lam,
-          static_cast<double*>(kv), static_cast<double*>(o), heads, d, sb, sh);
+      if (d == 64)
+        decode_kernel<double, double, 2><<<grid, kDecThreads, 0, st>>>(
+            static_cast<const double*>(q), static_cast<const double*>(k), static_cast<const double*>(v), lam,
+            static_cast<double*>(kv), static_cast<double*>(o), heads, d, sb, sh);
+      else
+        decode_kernel<double, double, 1><<<grid, kDecThreads, 0, st>>>(
+            static_cast<const double*>(q), static_cast<const double*>(k), static_cast<const double*>(v), lam,
+            static_cast<double*>(kv), static_cast<double*>(o), heads, d, sb, sh);
       break;
     case LA_F32:
-      decode_kernel<float, float><<<grid, kDecThreads, 0, st>>>(
-          static_cast<const float*>(q), static_cast<const float*>(k), static_cast<const float*>(v), lam,
-          static_cast<float*>(kv), static_cast<float*>(o), heads, d, sb, sh);
+      if (d == 128)
+        decode_kernel<float, float, 4><<<grid, kDecThreads, 0, st>>>(
+            static_cast<const float*>(q), static_cast<const float*>(k), static_cast<const float*>(v), lam,
+            static_cast<float*>(kv), static_cast<float*>(o), heads, d, sb, sh);
+      else
+        decode_kernel<float, float, 1><<<grid, kDecThreads, 0, st>>>(
+            static_cast<const float*>(q), static_cast<const float*>(k), static_cast<const float*>(v), lam,
+            static_cast<float*>(kv), static_cast<float*>(o), heads, d, sb, sh);
       break;
     default:
-      decode_kernel<__nv_bfloat16, float><<<grid, kDecThreads, 0, st>>>(
-          static_cast<const __nv_bfloat16*>(q), static_cast<const __nv_bfloat16*>(k),
-          static_cast<const __nv_bfloat16*>(v), lam, static_cast<float*>(kv), static_cast<__nv_bfloat16*>(o), heads,
-          d, sb, sh);
+      if (d == 128)
+        decode_kernel<__nv_bfloat16, float, 4><<<grid, kDecThreads, 0, st>>>(
+            static_cast<const __nv_bfloat16*>(q), static_cast<const __nv_bfloat16*>(k),
+            static_cast<const __nv_bfloat16*>(v), lam, static_cast<float*>(kv), static_cast<__nv_bfloat16*>(o), heads,
+            d, sb, sh);
+      else
+        decode_kernel<__nv_bfloat16, float, 1><<<grid, kDecThreads, 0, st>>>(
+            static_cast<const __nv_bfloat16*>(q), static_cast<const __nv_bfloat16*>(k),
+            static_cast<const __nv_bfloat16*>(v), lam, static_cast<float*>(kv), static_cast<__nv_bfloat16*>(o), heads,
+            d, sb, sh);
   }
   return cudaGetLastError();
 }

@@ -44,7 +44,7 @@ __device__ __forceinline__ Tacc act_grad(Tacc x, int act) {
 template <typename Tacc>
 __device__ __forceinline__ void rot_cs(double theta, int64_t pos, Tacc* c, Tacc* s) {
   double ang = theta * (double)pos;
-  ang = remainder(ang, 6.283185307179586476925286766559);
+  ang = fma(-6.283185307179586476925286766559, rint(ang * 0.15915494309189533576888376337251), ang);
   if (sizeof(Tacc) == 8) {
     double cc, ss;
     sincos(ang, &ss, &cc);
@@ -58,36 +58,62 @@ __device__ __forceinline__ void rot_cs(double theta, int64_t pos, Tacc* c, Tacc*
   }
 }
 
-// one thread per feature pair of one row
+// 16-byte vectors of the operand type (8 bf16, 4 fp32, 2 fp64 = 4, 2, 1 feature pairs)
+template <typename T> struct Vec {
+  static constexpr int N = 16 / sizeof(T);
+  T v[N];
+};
+template <typename T>
+__device__ __forceinline__ Vec<T> ldv(const T* p) {
+  Vec<T> r;
+  *reinterpret_cast<uint4*>(r.v) = __ldg(reinterpret_cast<const uint4*>(p));
+  return r;
+}
+template <typename T>
+__device__ __forceinline__ void stv(T* p, const Vec<T>& r) {
+  *reinterpret_cast<uint4*>(p) = *reinterpret_cast<const uint4*>(r.v);
+}
+
+// one thread per 16-byte vector of one row (its feature pairs share the row's position)
 template <typename T, typename Tacc>
 __global__ void prologue_kernel(const T* __restrict__ qp, const T* __restrict__ kp, const double* __restrict__ theta,
                                 T* __restrict__ q, T* __restrict__ k, int64_t rows, int n, int width, int d,
                                 int64_t offset, int act) {
+  constexpr int V = Vec<T>::N;
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int half_w = width >> 1;
-  if (idx >= rows * half_w) return;
-  const int64_t row = idx / half_w;
-  const int pc = (int)(idx % half_w);  // pair column within the row
-  const int64_t e = row * width + 2 * pc;
-  Tacc q1 = act_fwd<Tacc>((Tacc)Cvt<T>::to_f(qp[e]), act), q2 = act_fwd<Tacc>((Tacc)Cvt<T>::to_f(qp[e + 1]), act);
-  Tacc k1 = act_fwd<Tacc>((Tacc)Cvt<T>::to_f(kp[e]), act), k2 = act_fwd<Tacc>((Tacc)Cvt<T>::to_f(kp[e + 1]), act);
-  if (theta != nullptr) {
-    Tacc c, s;
-    rot_cs<Tacc>(theta[pc % (d >> 1)], row % n + offset, &c, &s);
-    const Tacc a1 = q1 * c - q2 * s, a2 = q1 * s + q2 * c;
-    const Tacc b1 = k1 * c - k2 * s, b2 = k1 * s + k2 * c;
-    q1 = a1, q2 = a2, k1 = b1, k2 = b2;
+  const int vw = width / V;
+  if (idx >= rows * vw) return;
+  const int64_t row = idx / vw;
+  const int c0 = (int)(idx % vw) * V;
+  const int64_t e = row * width + c0;
+  const Vec<T> xq = ldv(qp + e), xk = ldv(kp + e);
+  Vec<T> oq, ok;
+  const int64_t pos = row % n + offset;
+#pragma unroll
+  for (int pr = 0; pr < V / 2; ++pr) {
+    Tacc q1 = act_fwd<Tacc>((Tacc)Cvt<T>::to_f(xq.v[2 * pr]), act), q2 = act_fwd<Tacc>((Tacc)Cvt<T>::to_f(xq.v[2 * pr + 1]), act);
+    Tacc k1 = act_fwd<Tacc>((Tacc)Cvt<T>::to_f(xk.v[2 * pr]), act), k2 = act_fwd<Tacc>((Tacc)Cvt<T>::to_f(xk.v[2 * pr + 1]), act);
+    if (theta != nullptr) {
+      Tacc c, s;
+      rot_cs<Tacc>(theta[((c0 >> 1) + pr) % (d >> 1)], pos, &c, &s);
+      const Tacc a1 = q1 * c - q2 * s, a2 = q1 * s + q2 * c;
+      const Tacc b1 = k1 * c - k2 * s, b2 = k1 * s + k2 * c;
+      q1 = a1, q2 = a2, k1 = b1, k2 = b2;
+    }
+    oq.v[2 * pr] = Cvt<T>::from_f(q1);
+    oq.v[2 * pr + 1] = Cvt<T>::from_f(q2);
+    ok.v[2 * pr] = Cvt<T>::from_f(k1);
+    ok.v[2 * pr + 1] = Cvt<T>::from_f(k2);
   }
-  q[e] = Cvt<T>::from_f(q1);
-  q[e + 1] = Cvt<T>::from_f(q2);
-  k[e] = Cvt<T>::from_f(k1);
-  k[e + 1] = Cvt<T>::from_f(k2);
+  stv(q + e, oq);
+  stv(k + e, ok);
 }
 
 constexpr int kRowsPerBlock = 64;
 
-// grid (ceil(width/2 / 256), ceil(rows / 64)); dtheta partials per (row block, x block) land in
-// `partial` [gridDim.y * gridDim.x][d/2] (deterministic; summed by reduce_theta_kernel)
+// grid (ceil(width/V / 256), ceil(rows / 64)); a thread owns one 16-byte column vector and walks 64
+// rows.  dtheta partials per (row block, x block) land in `partial` [gridDim.y * gridDim.x][d/2]
+// (deterministic; summed by reduce_theta_kernel)
 template <typename T, typename Tacc>
 __global__ void __launch_bounds__(256) prologue_bwd_kernel(const T* __restrict__ qp, const T* __restrict__ kp,
                                                            const double* __restrict__ theta, const T* __restrict__ dq,
@@ -95,47 +121,63 @@ __global__ void __launch_bounds__(256) prologue_bwd_kernel(const T* __restrict__
                                                            T* __restrict__ dkp, double* __restrict__ partial,
                                                            int64_t rows, int n, int width, int d, int64_t offset,
                                                            int act) {
+  constexpr int V = Vec<T>::N;
   extern __shared__ double sdt[];  // [d/2]
-  const int half_w = width >> 1, hd = d >> 1;
-  const int pc = blockIdx.x * blockDim.x + threadIdx.x;
+  const int vw = width / V, hd = d >> 1;
+  const int vc = blockIdx.x * blockDim.x + threadIdx.x;
   if (theta != nullptr) {
     for (int j = threadIdx.x; j < hd; j += blockDim.x) sdt[j] = 0.0;
     __syncthreads();
   }
-  Tacc acc = 0;
-  if (pc < half_w) {
-    const double th = theta != nullptr ? theta[pc % hd] : 0.0;
+  Tacc acc[V / 2];
+#pragma unroll
+  for (int pr = 0; pr < V / 2; ++pr) acc[pr] = 0;
+  const int c0 = vc * V;
+  if (vc < vw) {
+    double th[V / 2];
+#pragma unroll
+    for (int pr = 0; pr < V / 2; ++pr) th[pr] = theta != nullptr ? theta[((c0 >> 1) + pr) % hd] : 0.0;
     const int64_t r0 = (int64_t)blockIdx.y * kRowsPerBlock;
     const int64_t r1 = r0 + kRowsPerBlock < rows ? r0 + kRowsPerBlock : rows;
     for (int64_t row = r0; row < r1; ++row) {
-      const int64_t e = row * width + 2 * pc;
-      const Tacc xq1 = (Tacc)Cvt<T>::to_f(qp[e]), xq2 = (Tacc)Cvt<T>::to_f(qp[e + 1]);
-      const Tacc xk1 = (Tacc)Cvt<T>::to_f(kp[e]), xk2 = (Tacc)Cvt<T>::to_f(kp[e + 1]);
-      Tacc gq1 = (Tacc)Cvt<T>::to_f(dq[e]), gq2 = (Tacc)Cvt<T>::to_f(dq[e + 1]);
-      Tacc gk1 = (Tacc)Cvt<T>::to_f(dk[e]), gk2 = (Tacc)Cvt<T>::to_f(dk[e + 1]);
-      if (theta != nullptr) {
-        Tacc c, s;
-        const int64_t pos = row % n + offset;
-        rot_cs<Tacc>(th, pos, &c, &s);
-        // rotated activations y (recomputed) for the angle gradient
-        const Tacc aq1 = act_fwd<Tacc>(xq1, act), aq2 = act_fwd<Tacc>(xq2, act);
-        const Tacc ak1 = act_fwd<Tacc>(xk1, act), ak2 = act_fwd<Tacc>(xk2, act);
-        const Tacc yq1 = aq1 * c - aq2 * s, yq2 = aq1 * s + aq2 * c;
-        const Tacc yk1 = ak1 * c - ak2 * s, yk2 = ak1 * s + ak2 * c;
-        acc += (Tacc)pos * ((gq2 * yq1 - gq1 * yq2) + (gk2 * yk1 - gk1 * yk2));
-        // dx = rot^-1 dy
-        const Tacc rq1 = gq1 * c + gq2 * s, rq2 = -gq1 * s + gq2 * c;
-        const Tacc rk1 = gk1 * c + gk2 * s, rk2 = -gk1 * s + gk2 * c;
-        gq1 = rq1, gq2 = rq2, gk1 = rk1, gk2 = rk2;
+      const int64_t e = row * width + c0;
+      const Vec<T> xq = ldv(qp + e), xk = ldv(kp + e), gq = ldv(dq + e), gk = ldv(dk + e);
+      Vec<T> oq, ok;
+      const int64_t pos = row % n + offset;
+#pragma unroll
+      for (int pr = 0; pr < V / 2; ++pr) {
+        const Tacc xq1 = (Tacc)Cvt<T>::to_f(xq.v[2 * pr]), xq2 = (Tacc)Cvt<T>::to_f(xq.v[2 * pr + 1]);
+        const Tacc xk1 = (Tacc)Cvt<T>::to_f(xk.v[2 * pr]), xk2 = (Tacc)Cvt<T>::to_f(xk.v[2 * pr + 1]);
+        Tacc gq1 = (Tacc)Cvt<T>::to_f(gq.v[2 * pr]), gq2 = (Tacc)Cvt<T>::to_f(gq.v[2 * pr + 1]);
+        Tacc gk1 = (Tacc)Cvt<T>::to_f(gk.v[2 * pr]), gk2 = (Tacc)Cvt<T>::to_f(gk.v[2 * pr + 1]);
+        if (theta != nullptr) {
+          Tacc c, s;
+          rot_cs<Tacc>(th[pr], pos, &c, &s);
+          // rotated activations y (recomputed) for the angle gradient
+          const Tacc aq1 = act_fwd<Tacc>(xq1, act), aq2 = act_fwd<Tacc>(xq2, act);
+          const Tacc ak1 = act_fwd<Tacc>(xk1, act), ak2 = act_fwd<Tacc>(xk2, act);
+          const Tacc yq1 = aq1 * c - aq2 * s, yq2 = aq1 * s + aq2 * c;
+          const Tacc yk1 = ak1 * c - ak2 * s, yk2 = ak1 * s + ak2 * c;
+          acc[pr] += (Tacc)pos * ((gq2 * yq1 - gq1 * yq2) + (gk2 * yk1 - gk1 * yk2));
+          // dx = rot^-1 dy
+          const Tacc rq1 = gq1 * c + gq2 * s, rq2 = -gq1 * s + gq2 * c;
+          const Tacc rk1 = gk1 * c + gk2 * s, rk2 = -gk1 * s + gk2 * c;
+          gq1 = rq1, gq2 = rq2, gk1 = rk1, gk2 = rk2;
+        }
+        oq.v[2 * pr] = Cvt<T>::from_f(gq1 * act_grad<Tacc>(xq1, act));
+        oq.v[2 * pr + 1] = Cvt<T>::from_f(gq2 * act_grad<Tacc>(xq2, act));
+        ok.v[2 * pr] = Cvt<T>::from_f(gk1 * act_grad<Tacc>(xk1, act));
+        ok.v[2 * pr + 1] = Cvt<T>::from_f(gk2 * act_grad<Tacc>(xk2, act));
       }
-      dqp[e] = Cvt<T>::from_f(gq1 * act_grad<Tacc>(xq1, act));
-      dqp[e + 1] = Cvt<T>::from_f(gq2 * act_grad<Tacc>(xq2, act));
-      dkp[e] = Cvt<T>::from_f(gk1 * act_grad<Tacc>(xk1, act));
-      dkp[e + 1] = Cvt<T>::from_f(gk2 * act_grad<Tacc>(xk2, act));
+      stv(dqp + e, oq);
+      stv(dkp + e, ok);
     }
   }
   if (theta == nullptr) return;
-  if (pc < half_w) atomicAdd(&sdt[pc % hd], (double)acc);  // shared-memory reduction over the heads
+  if (vc < vw) {
+#pragma unroll
+    for (int pr = 0; pr < V / 2; ++pr) atomicAdd(&sdt[((c0 >> 1) + pr) % hd], (double)acc[pr]);  // over heads
+  }
   __syncthreads();
   double* dst = partial + ((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * hd;
   for (int j = threadIdx.x; j < hd; j += blockDim.x) dst[j] = sdt[j];
@@ -157,82 +199,113 @@ __global__ void reduce_theta_kernel(const double* __restrict__ partial, int64_t 
 }
 
 template <typename Tacc>
-__device__ __forceinline__ Tacc block_sum(Tacc v, Tacc* red) {
+__device__ __forceinline__ Tacc warp_sum(Tacc v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  __syncthreads();  // red reused across calls
-  if (lane == 0) red[warp] = v;
-  __syncthreads();
-  Tacc t = 0;
-  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
-  return t;
+  return v;
 }
 
-// one CTA per row
+constexpr int kEpiWarps = 8;  // rows per CTA, one warp each
+
+// one warp per row; 16-byte vectors; the second sweep over the row hits L1
 template <typename T, typename Tacc>
-__global__ void __launch_bounds__(256) epilogue_kernel(const T* __restrict__ a, const T* __restrict__ u,
-                                                       T* __restrict__ gated, Tacc* __restrict__ rawnorm, int width,
-                                                       double eps) {
-  __shared__ Tacc red[32];
-  const int64_t row = blockIdx.x;
-  const T* ar = a + row * width;
+__global__ void __launch_bounds__(32 * kEpiWarps) epilogue_kernel(const T* __restrict__ a, const T* __restrict__ u,
+                                                                  T* __restrict__ gated, Tacc* __restrict__ rawnorm,
+                                                                  int64_t rows, int width, double eps) {
+  constexpr int V = Vec<T>::N;
+  const int64_t row = (int64_t)blockIdx.x * kEpiWarps + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const int64_t off = row * width;
   Tacc ss = 0;
-  for (int c = threadIdx.x; c < width; c += blockDim.x) {
-    const Tacc x = (Tacc)Cvt<T>::to_f(ar[c]);
-    ss += x * x;
+  for (int c = lane * V; c < width; c += 32 * V) {
+    const Vec<T> x = ldv(a + off + c);
+#pragma unroll
+    for (int e = 0; e < V; ++e) {
+      const Tacc f = (Tacc)Cvt<T>::to_f(x.v[e]);
+      ss += f * f;
+    }
   }
-  ss = block_sum<Tacc>(ss, red);
+  ss = warp_sum(ss);
   const Tacc raw = sqrt(ss);
   const Tacc scale = sqrt((Tacc)width) / (raw > (Tacc)eps ? raw : (Tacc)eps);
-  if (threadIdx.x == 0) rawnorm[row] = raw;
-  for (int c = threadIdx.x; c < width; c += blockDim.x) {
-    Tacc y = (Tacc)Cvt<T>::to_f(ar[c]) * scale;
-    if (u != nullptr) y *= (Tacc)Cvt<T>::to_f(u[row * width + c]);
-    gated[row * width + c] = Cvt<T>::from_f(y);
+  if (lane == 0) rawnorm[row] = raw;
+  for (int c = lane * V; c < width; c += 32 * V) {
+    const Vec<T> x = ldv(a + off + c);
+    Vec<T> y;
+    if (u != nullptr) {
+      const Vec<T> g = ldv(u + off + c);
+#pragma unroll
+      for (int e = 0; e < V; ++e)
+        y.v[e] = Cvt<T>::from_f((Tacc)Cvt<T>::to_f(x.v[e]) * scale * (Tacc)Cvt<T>::to_f(g.v[e]));
+    } else {
+#pragma unroll
+      for (int e = 0; e < V; ++e) y.v[e] = Cvt<T>::from_f((Tacc)Cvt<T>::to_f(x.v[e]) * scale);
+    }
+    stv(gated + off + c, y);
   }
 }
 
 template <typename T, typename Tacc>
-__global__ void __launch_bounds__(256) epilogue_bwd_kernel(const T* __restrict__ dgated, const T* __restrict__ a,
-                                                           const T* __restrict__ u, const Tacc* __restrict__ rawnorm,
-                                                           T* __restrict__ da, T* __restrict__ du, int width,
-                                                           double eps) {
-  __shared__ Tacc red[32];
-  const int64_t row = blockIdx.x;
+__global__ void __launch_bounds__(32 * kEpiWarps) epilogue_bwd_kernel(const T* __restrict__ dgated,
+                                                                      const T* __restrict__ a, const T* __restrict__ u,
+                                                                      const Tacc* __restrict__ rawnorm,
+                                                                      T* __restrict__ da, T* __restrict__ du,
+                                                                      int64_t rows, int width, double eps) {
+  constexpr int V = Vec<T>::N;
+  const int64_t row = (int64_t)blockIdx.x * kEpiWarps + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
   const int64_t off = row * width;
   const Tacc raw = rawnorm[row];
   const Tacc r = raw > (Tacc)eps ? raw : (Tacc)eps;
   const Tacc scale = sqrt((Tacc)width) / r;
   Tacc dot = 0;  // sum_c a_c * dan_c
-  for (int c = threadIdx.x; c < width; c += blockDim.x) {
-    const Tacc x = (Tacc)Cvt<T>::to_f(a[off + c]);
-    const Tacc g = (Tacc)Cvt<T>::to_f(dgated[off + c]);
-    Tacc dan = g;
+  for (int c = lane * V; c < width; c += 32 * V) {
+    const Vec<T> x = ldv(a + off + c), g = ldv(dgated + off + c);
     if (u != nullptr) {
-      const Tacc uu = (Tacc)Cvt<T>::to_f(u[off + c]);
-      dan = g * uu;
-      du[off + c] = Cvt<T>::from_f(g * x * scale);  // du = dgated * an
+      const Vec<T> uu = ldv(u + off + c);
+      Vec<T> o;
+#pragma unroll
+      for (int e = 0; e < V; ++e) {
+        const Tacc xf = (Tacc)Cvt<T>::to_f(x.v[e]), gf = (Tacc)Cvt<T>::to_f(g.v[e]);
+        dot += xf * gf * (Tacc)Cvt<T>::to_f(uu.v[e]);
+        o.v[e] = Cvt<T>::from_f(gf * xf * scale);  // du = dgated * an
+      }
+      stv(du + off + c, o);
+    } else {
+#pragma unroll
+      for (int e = 0; e < V; ++e) dot += (Tacc)Cvt<T>::to_f(x.v[e]) * (Tacc)Cvt<T>::to_f(g.v[e]);
     }
-    dot += x * dan;
   }
-  dot = block_sum<Tacc>(dot, red);
+  dot = warp_sum(dot);
   // srmsnorm_backward: dx = dan sqrt(W)/r - [raw >= eps] x (x.dan / r^2) sqrt(W)/r
   const Tacc proj = raw >= (Tacc)eps ? dot / (r * r) : (Tacc)0;
-  for (int c = threadIdx.x; c < width; c += blockDim.x) {
-    const Tacc x = (Tacc)Cvt<T>::to_f(a[off + c]);
-    Tacc dan = (Tacc)Cvt<T>::to_f(dgated[off + c]);
-    if (u != nullptr) dan *= (Tacc)Cvt<T>::to_f(u[off + c]);
-    da[off + c] = Cvt<T>::from_f((dan - x * proj) * scale);
+  for (int c = lane * V; c < width; c += 32 * V) {
+    const Vec<T> x = ldv(a + off + c), g = ldv(dgated + off + c);
+    Vec<T> o;
+    if (u != nullptr) {
+      const Vec<T> uu = ldv(u + off + c);
+#pragma unroll
+      for (int e = 0; e < V; ++e) {
+        const Tacc dan = (Tacc)Cvt<T>::to_f(g.v[e]) * (Tacc)Cvt<T>::to_f(uu.v[e]);
+        o.v[e] = Cvt<T>::from_f((dan - (Tacc)Cvt<T>::to_f(x.v[e]) * proj) * scale);
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < V; ++e)
+        o.v[e] = Cvt<T>::from_f(((Tacc)Cvt<T>::to_f(g.v[e]) - (Tacc)Cvt<T>::to_f(x.v[e]) * proj) * scale);
+    }
+    stv(da + off + c, o);
   }
 }
 
 template <typename T, typename Tacc>
 cudaError_t prologue_t(const GlaRows& g, const void* qp, const void* kp, const double* theta, void* q, void* k,
                        cudaStream_t st) {
-  const int64_t pairs = g.rows * (g.width / 2);
+  const int64_t vecs = g.rows * (g.width / Vec<T>::N);
   const int threads = 256;
-  const int64_t blocks = (pairs + threads - 1) / threads;
+  const int64_t blocks = (vecs + threads - 1) / threads;
   prologue_kernel<T, Tacc><<<(unsigned)blocks, threads, 0, st>>>(
       static_cast<const T*>(qp), static_cast<const T*>(kp), theta, static_cast<T*>(q), static_cast<T*>(k), g.rows,
       g.n, g.width, g.d, g.offset, g.act);
@@ -242,8 +315,8 @@ cudaError_t prologue_t(const GlaRows& g, const void* qp, const void* kp, const d
 template <typename T, typename Tacc>
 cudaError_t prologue_bwd_t(const GlaRows& g, const void* qp, const void* kp, const double* theta, const void* dq,
                            const void* dk, void* dqp, void* dkp, double* partial, double* dtheta, cudaStream_t st) {
-  const int half_w = g.width / 2, hd = g.d / 2;
-  const dim3 grid((unsigned)((half_w + 255) / 256), (unsigned)((g.rows + kRowsPerBlock - 1) / kRowsPerBlock));
+  const int vw = g.width / Vec<T>::N, hd = g.d / 2;
+  const dim3 grid((unsigned)((vw + 255) / 256), (unsigned)((g.rows + kRowsPerBlock - 1) / kRowsPerBlock));
   const size_t smem = theta != nullptr ? (size_t)hd * sizeof(double) : 0;
   prologue_bwd_kernel<T, Tacc><<<grid, 256, smem, st>>>(
       static_cast<const T*>(qp), static_cast<const T*>(kp), theta, static_cast<const T*>(dq),
@@ -258,24 +331,25 @@ cudaError_t prologue_bwd_t(const GlaRows& g, const void* qp, const void* kp, con
 template <typename T, typename Tacc>
 cudaError_t epilogue_t(const GlaRows& g, const void* a, const void* u, void* gated, void* rawnorm, double eps,
                        cudaStream_t st) {
-  epilogue_kernel<T, Tacc><<<(unsigned)g.rows, 256, 0, st>>>(static_cast<const T*>(a), static_cast<const T*>(u),
-                                                              static_cast<T*>(gated), static_cast<Tacc*>(rawnorm),
-                                                              g.width, eps);
+  epilogue_kernel<T, Tacc><<<(unsigned)((g.rows + kEpiWarps - 1) / kEpiWarps), 32 * kEpiWarps, 0, st>>>(
+      static_cast<const T*>(a), static_cast<const T*>(u), static_cast<T*>(gated), static_cast<Tacc*>(rawnorm), g.rows,
+      g.width, eps);
   return cudaGetLastError();
 }
 
 template <typename T, typename Tacc>
 cudaError_t epilogue_bwd_t(const GlaRows& g, const void* dgated, const void* a, const void* u, const void* rawnorm,
                            void* da, void* du, double eps, cudaStream_t st) {
-  epilogue_bwd_kernel<T, Tacc><<<(unsigned)g.rows, 256, 0, st>>>(
+  epilogue_bwd_kernel<T, Tacc><<<(unsigned)((g.rows + kEpiWarps - 1) / kEpiWarps), 32 * kEpiWarps, 0, st>>>(
       static_cast<const T*>(dgated), static_cast<const T*>(a), static_cast<const T*>(u),
-      static_cast<const Tacc*>(rawnorm), static_cast<T*>(da), static_cast<T*>(du), g.width, eps);
+      static_cast<const Tacc*>(rawnorm), static_cast<T*>(da), static_cast<T*>(du), g.rows, g.width, eps);
   return cudaGetLastError();
 }
 
 }  // namespace
 
 size_t gla_prologue_bwd_partial_bytes(const GlaRows& g) {
+  // sized for the narrowest vector (fp64: one pair per thread), so it covers every dtype
   const int64_t gx = (g.width / 2 + 255) / 256, gy = (g.rows + kRowsPerBlock - 1) / kRowsPerBlock;
   return (size_t)(gx * gy) * (size_t)(g.d / 2) * sizeof(double);
 }
