@@ -14,9 +14,11 @@ for b in txt.split('=== ')[1:]:
         if not v or not v[0].isdigit():
             break
         rows.append([int(x) for x in v[1:]])
-    print("chunk " + " ".join(f"{n:>6s}" for n in order) + "  period")
+    # events this build does not stamp print as 0 in the raw table: drop them
+    live = [n for n in order if any(r[names.index(n)] != -1 for r in rows)]  # -1: not stamped by this build
+    print("chunk " + " ".join(f"{n:>6s}" for n in live) + "  period")
     for c in range(4, min(len(rows), 20)):
         r = rows[c]
         base = r[names.index("S_iss")]
-        print(f"{c:5d} " + " ".join(f"{r[names.index(n)] - base:6d}" for n in order) +
+        print(f"{c:5d} " + " ".join(f"{r[names.index(n)] - base:6d}" for n in live) +
               f"  {base - rows[c - 1][names.index('S_iss')]:6d}")
