@@ -175,6 +175,17 @@ LA_API int la_gla_epilogue(const la_gla_desc* desc, const void* a, const void* u
 LA_API int la_gla_epilogue_bwd(const la_gla_desc* desc, const void* dgated, const void* a, const void* u,
                         const void* rawnorm, void* da, void* du, void* stream);
 
+/* Tensor-parallel GLA (gla_parallel_forward, parallel.py:138-178): each rank runs its heads and
+ * gates without the norm, the ONE all-reduce carries [partial output | row sum of squares]:
+ *   la_gla_gate_rowsq  gated = a * u (u NULL: a), rowsq[row * rowsq_stride] = sum_c a[row, c]^2
+ *                      (accumulation dtype; point rowsq at column out_w of the augmented buffer)
+ *   la_gla_rowscale    y[r, :] = red[r, :out_w] sqrt(out_w) / max(sqrt(red[r, out_w]), eps) on the
+ *                      reduced [rows, out_w + 1] buffer (accumulation dtype in and out) */
+LA_API int la_gla_gate_rowsq(const la_gla_desc* desc, const void* a, const void* u, void* gated,
+                      void* rowsq, int64_t rowsq_stride, void* stream);
+LA_API int la_gla_rowscale(int dtype, int64_t rows, int64_t out_width, double eps, const void* red,
+                    void* y, void* stream);
+
 /* Number of kernels la_fwd (which = 0), la_bwd (which = 1) or la_bwd given the
  * forward's segment states (which = 2) launches for this descriptor; -1 on a
  * bad descriptor. */

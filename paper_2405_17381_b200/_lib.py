@@ -24,7 +24,7 @@ BACKENDS = {"auto": LA_BACKEND_AUTO, "simt": LA_BACKEND_SIMT, "tcgen05": LA_BACK
 # every symbol include/lightning_attn.h declares
 EXPORTS = ("la_workspace_bytes", "la_segment_count", "la_fwd", "la_bwd", "la_fwd_state", "la_bwd_state",
            "la_decode", "la_gla_workspace_bytes", "la_gla_prologue", "la_gla_prologue_bwd", "la_gla_epilogue",
-           "la_gla_epilogue_bwd", "la_launch_count", "la_last_error", "la_abi_version", "la_build_info")
+           "la_gla_epilogue_bwd", "la_gla_gate_rowsq", "la_gla_rowscale", "la_launch_count", "la_last_error", "la_abi_version", "la_build_info")
 ABI_VERSION = 2
 LA_ACT_NONE, LA_ACT_SWISH, LA_ACT_ONE_PLUS_ELU = 0, 1, 2
 ACTS = {"none": LA_ACT_NONE, "swish": LA_ACT_SWISH, "one_plus_elu": LA_ACT_ONE_PLUS_ELU}
@@ -117,6 +117,10 @@ def load() -> ctypes.CDLL:
     lib.la_gla_epilogue.restype = c_int
     lib.la_gla_epilogue_bwd.argtypes = [G, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]
     lib.la_gla_epilogue_bwd.restype = c_int
+    lib.la_gla_gate_rowsq.argtypes = [G, c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_void_p]
+    lib.la_gla_gate_rowsq.restype = c_int
+    lib.la_gla_rowscale.argtypes = [c_int, c_int64, c_int64, c_double, c_void_p, c_void_p, c_void_p]
+    lib.la_gla_rowscale.restype = c_int
     lib.la_launch_count.argtypes = [P, c_int]
     lib.la_launch_count.restype = c_int
     lib.la_last_error.argtypes = []

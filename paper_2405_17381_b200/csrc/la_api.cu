@@ -523,6 +523,28 @@ int la_gla_epilogue_bwd(const la_gla_desc* desc, const void* dgated, const void*
   return err == cudaSuccess ? LA_OK : cuda_fail(err, "la_gla_epilogue_bwd");
 }
 
+int la_gla_gate_rowsq(const la_gla_desc* desc, const void* a, const void* u, void* gated, void* rowsq,
+                      int64_t rowsq_stride, void* stream) {
+  la::GlaRows g;
+  int rc = gla_prepare(desc, false, &g);
+  if (rc != LA_OK) return rc;
+  if (!a || !gated || !rowsq || rowsq_stride < 1) return fail(LA_ERR_SHAPE, "la_gla_gate_rowsq: null operand / bad stride");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  bind_stream_context(st);
+  cudaError_t err = la::gla_gate_rowsq(g, a, u, gated, rowsq, rowsq_stride, st);
+  return err == cudaSuccess ? LA_OK : cuda_fail(err, "la_gla_gate_rowsq");
+}
+
+int la_gla_rowscale(int dtype, int64_t rows, int64_t out_width, double eps, const void* red, void* y, void* stream) {
+  if (dtype != LA_F32 && dtype != LA_F64 && dtype != LA_BF16) return fail(LA_ERR_DOMAIN, "bad dtype %d", dtype);
+  if (rows < 1 || out_width < 1 || out_width > (int64_t)1 << 30) return fail(LA_ERR_SHAPE, "bad rows / out_width");
+  if (!red || !y) return fail(LA_ERR_SHAPE, "la_gla_rowscale: null red / y");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  bind_stream_context(st);
+  cudaError_t err = la::gla_rowscale(dtype == LA_F64, red, y, rows, (int)out_width, eps, st);
+  return err == cudaSuccess ? LA_OK : cuda_fail(err, "la_gla_rowscale");
+}
+
 int la_launch_count(const la_desc* desc, int which) {
   if (validate(desc) != LA_OK) return -1;
   int backend;

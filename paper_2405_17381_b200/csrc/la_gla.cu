@@ -300,6 +300,56 @@ __global__ void __launch_bounds__(32 * kEpiWarps) epilogue_bwd_kernel(const T* _
   }
 }
 
+// tensor-parallel GLA (parallel.py:138-178): gated = a * u (no norm) and the row's sum of squares
+// of this shard's attention output, written as the last column of an augmented [rows, out_w + 1]
+// buffer row (the all-reduce payload); the output projection fills columns [0, out_w)
+template <typename T, typename Tacc>
+__global__ void __launch_bounds__(32 * kEpiWarps) gate_rowsq_kernel(const T* __restrict__ a, const T* __restrict__ u,
+                                                                    T* __restrict__ gated, Tacc* __restrict__ rowsq,
+                                                                    int64_t rowsq_stride, int64_t rows, int width) {
+  constexpr int V = Vec<T>::N;
+  const int64_t row = (int64_t)blockIdx.x * kEpiWarps + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const int64_t off = row * width;
+  Tacc ss = 0;
+  for (int c = lane * V; c < width; c += 32 * V) {
+    const Vec<T> x = ldv(a + off + c);
+    Vec<T> y;
+    if (u != nullptr) {
+      const Vec<T> g = ldv(u + off + c);
+#pragma unroll
+      for (int e = 0; e < V; ++e) {
+        const Tacc f = (Tacc)Cvt<T>::to_f(x.v[e]);
+        ss += f * f;
+        y.v[e] = Cvt<T>::from_f(f * (Tacc)Cvt<T>::to_f(g.v[e]));
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < V; ++e) {
+        const Tacc f = (Tacc)Cvt<T>::to_f(x.v[e]);
+        ss += f * f;
+        y.v[e] = x.v[e];
+      }
+    }
+    stv(gated + off + c, y);
+  }
+  ss = warp_sum(ss);
+  if (lane == 0) rowsq[row * rowsq_stride] = ss;
+}
+
+// y[row, :] = red[row, :out_w] * sqrt(out_w) / max(sqrt(red[row, out_w]), eps)   (parallel.py:176-178)
+template <typename Tacc>
+__global__ void __launch_bounds__(256) rowscale_kernel(const Tacc* __restrict__ red, Tacc* __restrict__ y,
+                                                       int64_t rows, int out_w, double eps) {
+  const int64_t row = blockIdx.x;
+  if (row >= rows) return;
+  const Tacc* r = red + row * (int64_t)(out_w + 1);
+  const Tacc raw = sqrt(r[out_w]);
+  const Tacc scale = sqrt((Tacc)out_w) / (raw > (Tacc)eps ? raw : (Tacc)eps);
+  for (int c = threadIdx.x; c < out_w; c += blockDim.x) y[row * out_w + c] = r[c] * scale;
+}
+
 template <typename T, typename Tacc>
 cudaError_t prologue_t(const GlaRows& g, const void* qp, const void* kp, const double* theta, void* q, void* k,
                        cudaStream_t st) {
@@ -346,6 +396,15 @@ cudaError_t epilogue_bwd_t(const GlaRows& g, const void* dgated, const void* a, 
   return cudaGetLastError();
 }
 
+template <typename T, typename Tacc>
+cudaError_t gate_rowsq_t(const GlaRows& g, const void* a, const void* u, void* gated, void* rowsq,
+                         int64_t rowsq_stride, cudaStream_t st) {
+  gate_rowsq_kernel<T, Tacc><<<(unsigned)((g.rows + kEpiWarps - 1) / kEpiWarps), 32 * kEpiWarps, 0, st>>>(
+      static_cast<const T*>(a), static_cast<const T*>(u), static_cast<T*>(gated), static_cast<Tacc*>(rowsq),
+      rowsq_stride, g.rows, g.width);
+  return cudaGetLastError();
+}
+
 }  // namespace
 
 size_t gla_prologue_bwd_partial_bytes(const GlaRows& g) {
@@ -378,5 +437,25 @@ cudaError_t gla_epilogue_bwd(const GlaRows& g, const void* dgated, const void* a
   LA_DISPATCH(epilogue_bwd_t, dgated, a, u, rawnorm, da, du, eps, st)
 }
 #undef LA_DISPATCH
+
+cudaError_t gla_gate_rowsq(const GlaRows& g, const void* a, const void* u, void* gated, void* rowsq,
+                           int64_t rowsq_stride, cudaStream_t st) {
+  switch (g.dtype) {
+    case LA_F64: return gate_rowsq_t<double, double>(g, a, u, gated, rowsq, rowsq_stride, st);
+    case LA_F32: return gate_rowsq_t<float, float>(g, a, u, gated, rowsq, rowsq_stride, st);
+    default: return gate_rowsq_t<__nv_bfloat16, float>(g, a, u, gated, rowsq, rowsq_stride, st);
+  }
+}
+
+cudaError_t gla_rowscale(bool acc_double, const void* red, void* y, int64_t rows, int out_w, double eps,
+                         cudaStream_t st) {
+  if (acc_double)
+    rowscale_kernel<double><<<(unsigned)rows, 256, 0, st>>>(static_cast<const double*>(red), static_cast<double*>(y),
+                                                             rows, out_w, eps);
+  else
+    rowscale_kernel<float><<<(unsigned)rows, 256, 0, st>>>(static_cast<const float*>(red), static_cast<float*>(y),
+                                                            rows, out_w, eps);
+  return cudaGetLastError();
+}
 
 }  // namespace la

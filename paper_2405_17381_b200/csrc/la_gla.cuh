@@ -21,4 +21,10 @@ cudaError_t gla_epilogue(const GlaRows& g, const void* a, const void* u, void* g
                          cudaStream_t st);
 cudaError_t gla_epilogue_bwd(const GlaRows& g, const void* dgated, const void* a, const void* u, const void* rawnorm,
                              void* da, void* du, double eps, cudaStream_t st);
+// tensor-parallel GLA: gated = a * u (u nullable) + per-row sum of squares of a at rowsq[row * stride]
+cudaError_t gla_gate_rowsq(const GlaRows& g, const void* a, const void* u, void* gated, void* rowsq,
+                           int64_t rowsq_stride, cudaStream_t st);
+// y[r, :] = red[r, :out_w] sqrt(out_w) / max(sqrt(red[r, out_w]), eps); red / y in the accumulation type
+cudaError_t gla_rowscale(bool acc_double, const void* red, void* y, int64_t rows, int out_w, double eps,
+                         cudaStream_t st);
 }  // namespace la

@@ -359,3 +359,29 @@ def gla_epilogue_backward(dgated, a, u, rawnorm, heads, *, eps=SRMS_EPS):
     _lib.check(_lib.load().la_gla_epilogue_bwd(ctypes.byref(desc), _ptr(dgated), _ptr(a), _ptr(u),
                                                _ptr(rawnorm.contiguous()), _ptr(da), _ptr(du), _stream(a.device)))
     return da, du
+
+
+def gla_gate_rowsq(a, u, heads, rowsq, *, rowsq_stride=1):
+    """Tensor-parallel stage: gated = a * u (u None: a copy of a) and rowsq[r * stride] = |a_r|^2
+    written into ``rowsq`` (a view into the all-reduce buffer, accumulation dtype)."""
+    a, u = _rows([a, u], ["a", "u"])
+    desc = _gla_desc(a, heads, "none", 0, SRMS_EPS)
+    if rowsq.dtype != state_dtype(a.dtype) or rowsq.device != a.device:
+        raise ShapeError(f"rowsq must be {state_dtype(a.dtype)} on {a.device}")
+    gated = torch.empty_like(a)
+    _lib.check(_lib.load().la_gla_gate_rowsq(ctypes.byref(desc), _ptr(a), _ptr(u), _ptr(gated), _ptr(rowsq),
+                                             int(rowsq_stride), _stream(a.device)))
+    return gated
+
+
+def gla_rowscale(red, out_width, *, eps=SRMS_EPS, dtype=torch.float32):
+    """y[r, :] = red[r, :W] sqrt(W) / max(sqrt(red[r, W]), eps) on the reduced [rows, W + 1] buffer."""
+    if red.dim() != 2 or red.shape[1] != out_width + 1 or red.dtype not in (torch.float32, torch.float64):
+        raise ShapeError(f"red must be a float32/float64 [rows, {out_width + 1}] tensor, got {tuple(red.shape)} "
+                         f"{red.dtype}")
+    red = red.contiguous()
+    y = torch.empty(red.shape[0], out_width, dtype=red.dtype, device=red.device)
+    code = _lib.LA_F64 if red.dtype == torch.float64 else _lib.LA_F32
+    _lib.check(_lib.load().la_gla_rowscale(code, red.shape[0], out_width, float(eps), _ptr(red), _ptr(y),
+                                           _stream(red.device)))
+    return y
