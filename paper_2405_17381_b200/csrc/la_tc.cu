@@ -743,6 +743,11 @@ const char* tc_detail() { return g_detail; }
 extern "C" __attribute__((visibility("default"))) int la_debug_set_trace(void* dev_ptr) {
   return (int)cudaMemcpyToSymbol(g_la_trace, &dev_ptr, sizeof(dev_ptr));
 }
+void la_debug_set_trace_bwd(void* dev_ptr);
+extern "C" __attribute__((visibility("default"))) int la_debug_set_trace_bwd_c(void* dev_ptr) {
+  la_debug_set_trace_bwd(dev_ptr);
+  return (int)cudaGetLastError();
+}
 #endif
 
 bool tc_supported(int dtype, int d, const int64_t* strides) {

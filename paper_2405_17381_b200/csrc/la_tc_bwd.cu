@@ -37,6 +37,19 @@ using namespace ptx;
 #define LA_PF 0  // L2 prefetch distance in chunks (0: off)
 #endif
 
+#ifdef LA_TRACE
+// debug build only: cycle stamps of CTA (0, 0), [chunk][event] (tests/tc_trace_bwd.py)
+__device__ unsigned long long* g_la_trace_bwd = nullptr;
+#define LB_TR(t, ev)                                                         \
+  do {                                                                       \
+    if (lb_trp != nullptr && (t) < 32) lb_trp[(t) * 32 + (ev)] = clock64(); \
+  } while (0)
+#else
+#define LB_TR(t, ev) \
+  do {               \
+  } while (0)
+#endif
+
 constexpr int C = 128;
 constexpr int D = 128;
 constexpr int TILE = C * D * 2;
@@ -96,6 +109,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const uint32_t st_bf16 = slot(SLOT_ST);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#ifdef LA_TRACE
+  unsigned long long* const lb_trp = (blockIdx.x == 0 && blockIdx.y == 0) ? g_la_trace_bwd : nullptr;
+#endif
   const int seg = blockIdx.x, bh = blockIdx.y;
   const int bi = bh / args.heads, hi = bh % args.heads;
   const int p0 = seg * args.seg_len;
@@ -181,6 +197,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         uint64_t* empty = lane == 0 ? &bars.empty_q[s] : lane == 1 ? &bars.empty_d[s] : lane == 2 ? &bars.empty_k
                                                                                                      : &bars.empty_v;
         if (t >= nslot) mbar_wait(empty, ((t / nslot) - 1) & 1);
+        LB_TR(t, lane);
         const int r0 = chunk_row0(t);
         mbar_arrive_expect_tx(full, TILE);
         uint8_t* g = slot_gen(lane == 0 ? SLOT_Q + s : lane == 1 ? SLOT_D + s : lane == 2 ? SLOT_K : SLOT_V);
@@ -195,11 +212,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         tma_store_4d(&map_dv, slot_gen(SLOT_D + s), 0, r0, hi, bi);
         tma_store_4d(&map_dv, slot_gen(SLOT_D + s) + HALF, 64, r0, hi, bi);
         tma_store_commit();
+        LB_TR(t, 20);
         mbar_wait(&bars.dk_staged[s], (t >> 1) & 1);
         tma_store_4d(&map_dk, slot_gen(SLOT_Q + s), 0, r0, hi, bi);
         tma_store_4d(&map_dk, slot_gen(SLOT_Q + s) + HALF, 64, r0, hi, bi);
         tma_store_commit();
         tma_store_wait_read();
+        LB_TR(t, 21);
         mbar_arrive(&bars.empty_d[s]);
         mbar_arrive(&bars.empty_q[s]);
       }
@@ -224,6 +243,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                       IDESC_KK, kk > 0);
         }
         mma_commit(&bars.sv_full);
+        LB_TR(t, 4);
         // Sk = V dO^T
         mbar_wait(&bars.full_d[s], (t >> 1) & 1);
         mbar_wait(&bars.full_v, t & 1);
@@ -236,9 +256,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                       IDESC_KK, kk > 0);
         }
         mma_commit(&bars.sk_full);
+        LB_TR(t, 5);
         // state += Q^T W  (A = Q^T: MN-major Q tile; B = W in K's slot, MN-major)
         mbar_wait(&bars.st_scaled, t & 1);
         mbar_wait(&bars.w_ready, t & 1);
+        LB_TR(t, 6);
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < C / 16; ++kk)
@@ -250,6 +272,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         mbar_wait(&bars.st_pub, t & 1);
         if (t >= 1) mbar_wait(&bars.o_free, (2 * t - 1) & 1);
         mbar_wait(&bars.av_full, t & 1);
+        LB_TR(t, 7);
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk)
@@ -265,9 +288,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                       1);
         }
         mma_commit(&bars.ov_full);
+        LB_TR(t, 8);
         // dK = V~ state^T + Pk Q  (state^T = the same bf16 copy read K-major)
         mbar_wait(&bars.o_free, (2 * t) & 1);
         mbar_wait(&bars.ak_full, t & 1);
+        LB_TR(t, 9);
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
@@ -287,6 +312,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                       1);
         }
         mma_commit(&bars.ok_full);
+        LB_TR(t, 10);
       }
       // drain every asynchronous commit before the CTA retires
       if (nchunks > 0) {
@@ -296,6 +322,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         mbar_wait(&bars.ok_full, t & 1);
         mbar_wait(&bars.x_done, t & 1);
         mbar_wait(&bars.ds_full, t & 1);
+      if (warp == WARP_KV && lane == 0) LB_TR(t, 18);
       }
     }
   } else if (warp < WARP_O) {
@@ -375,11 +402,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     for (int t = 0; t < nchunks; ++t) {
       const float osc = pw[max(chunk_len(t) - 1 - i, 0)];
       mbar_wait(&bars.sv_full, t & 1);
+      if (warp == WARP_P && lane == 0) LB_TR(t, 11);
       tc_fence_after();
       convert(TM_SV, slot(SLOT_K), osc, &bars.av_full, &bars.pv_full);
+      if (warp == WARP_P && lane == 0) LB_TR(t, 12);
       mbar_wait(&bars.sk_full, t & 1);
+      if (warp == WARP_P && lane == 0) LB_TR(t, 13);
       tc_fence_after();
       convert(TM_SK, slot(SLOT_V), osc, &bars.ak_full, &bars.pk_full);
+      if (warp == WARP_P && lane == 0) LB_TR(t, 14);
     }
   } else if (warp < WARP_KV) {
     // ------------------------------------------------------------ W + dV / dK epilogues (warps 10..17)
@@ -431,8 +462,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars.w_ready);
+      if (warp == WARP_O && lane == 0) LB_TR(t, 15);
       epilogue(&bars.ov_full, 2 * t, slot(SLOT_D + s), &bars.dv_staged[s], t);
+      if (warp == WARP_O && lane == 0) LB_TR(t, 16);
       epilogue(&bars.ok_full, 2 * t + 1, slot(SLOT_Q + s), &bars.dk_staged[s], t);
+      if (warp == WARP_O && lane == 0) LB_TR(t, 17);
     }
   } else {
     // ------------------------------------------------------------ state (warps 18..25)
@@ -490,6 +524,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         load_scale(false, pw[chunk_len(t + 1)]);
         mbar_wait(&bars.x_done, t & 1);  // both products of chunk t read the previous copy
         publish();
+        if (warp == WARP_KV && lane == 0) LB_TR(t, 19);
       }
     }
     if (nchunks > 0 && args.state_out != nullptr && seg == 0) {
@@ -514,6 +549,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 }
 
 }  // namespace
+
+#ifdef LA_TRACE
+void la_debug_set_trace_bwd(void* dev_ptr) { cudaMemcpyToSymbol(g_la_trace_bwd, &dev_ptr, sizeof(dev_ptr)); }
+#endif
 
 cudaError_t tc_dkdv_launch(const PassDesc& p, const void* q, const void* k, const void* v, const void* dout,
                            void* dq_unused, void* dk, void* dv, cudaStream_t st) {
