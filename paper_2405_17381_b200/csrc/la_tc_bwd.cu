@@ -175,34 +175,37 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   if (warp == WARP_TMA) {
     // ------------------------------------------------------------ producers (lanes 0-3) + store lane (4)
-    if (lane < 4) {
-      const CUtensorMap* map = lane == 0 ? &map_q : lane == 1 ? &map_do : lane == 2 ? &map_k : &map_v;
-      const int nslot = lane < 2 ? 2 : 1;
-#if LA_PF > 0
-      for (int t = nslot; t < min(nchunks, LA_PF); ++t) {
-        tma_prefetch_l2_4d(map, 0, chunk_row0(t), hi, bi);
-        tma_prefetch_l2_4d(map, 64, chunk_row0(t), hi, bi);
-      }
-#endif
-      for (int t = 0; t < nchunks; ++t) {
-        const int s = nslot == 2 ? (t & 1) : 0;
-#if LA_PF > 0
-        if (t + LA_PF < nchunks && t + LA_PF >= nslot) {
-          tma_prefetch_l2_4d(map, 0, chunk_row0(t + LA_PF), hi, bi);
-          tma_prefetch_l2_4d(map, 64, chunk_row0(t + LA_PF), hi, bi);
+    if (lane == 0) {
+      // One lane serves all four rings from a polling loop, each ring advancing as soon as ITS slot is
+      // free.  (Four lanes running one shared loop reconverge every iteration, so the slowest ring's
+      // release gated the loads of the other three.)
+      const CUtensorMap* maps[4] = {&map_q, &map_do, &map_k, &map_v};
+      int next[4] = {0, 0, 0, 0};
+      long long t0 = 0;
+      for (uint32_t spins = 1; next[0] < nchunks || next[1] < nchunks || next[2] < nchunks || next[3] < nchunks;
+           ++spins) {
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const int t = next[r];
+          if (t >= nchunks) continue;
+          const int nslot = r < 2 ? 2 : 1;
+          const int s = nslot == 2 ? (t & 1) : 0;
+          uint64_t* full = r == 0 ? &bars.full_q[s] : r == 1 ? &bars.full_d[s] : r == 2 ? &bars.full_k : &bars.full_v;
+          uint64_t* empty = r == 0 ? &bars.empty_q[s] : r == 1 ? &bars.empty_d[s] : r == 2 ? &bars.empty_k
+                                                                                            : &bars.empty_v;
+          if (t >= nslot && !mbar_test(smem_u32(empty), ((t / nslot) - 1) & 1)) continue;
+          LB_TR(t, r);
+          const int r0 = chunk_row0(t);
+          mbar_arrive_expect_tx(full, TILE);
+          uint8_t* g = slot_gen(r == 0 ? SLOT_Q + s : r == 1 ? SLOT_D + s : r == 2 ? SLOT_K : SLOT_V);
+          tma_load_4d(maps[r], full, g, 0, r0, hi, bi);
+          tma_load_4d(maps[r], full, g + HALF, 64, r0, hi, bi);
+          next[r] = t + 1;
         }
-#endif
-        uint64_t* full = lane == 0 ? &bars.full_q[s] : lane == 1 ? &bars.full_d[s] : lane == 2 ? &bars.full_k
-                                                                                                  : &bars.full_v;
-        uint64_t* empty = lane == 0 ? &bars.empty_q[s] : lane == 1 ? &bars.empty_d[s] : lane == 2 ? &bars.empty_k
-                                                                                                     : &bars.empty_v;
-        if (t >= nslot) mbar_wait(empty, ((t / nslot) - 1) & 1);
-        LB_TR(t, lane);
-        const int r0 = chunk_row0(t);
-        mbar_arrive_expect_tx(full, TILE);
-        uint8_t* g = slot_gen(lane == 0 ? SLOT_Q + s : lane == 1 ? SLOT_D + s : lane == 2 ? SLOT_K : SLOT_V);
-        tma_load_4d(map, full, g, 0, r0, hi, bi);
-        tma_load_4d(map, full, g + HALF, 64, r0, hi, bi);
+        if ((spins & 0xFFFFF) == 0) {  // watchdog, as mbar_wait
+          if (t0 == 0) t0 = clock64();
+          else if (clock64() - t0 > 40000000000LL) __trap();
+        }
       }
     } else if (lane == 4) {
       for (int t = 0; t < nchunks; ++t) {
