@@ -670,7 +670,7 @@ thread_local char g_detail[256];
 
 }  // namespace
 
-bool tc_make_map(CUtensorMap* map, const void* base, const PassDesc& p) {
+bool tc_make_map(CUtensorMap* map, const void* base, const PassDesc& p, int box_rows) {
   auto enc = encode_fn();
   if (enc == nullptr) {
     snprintf(g_detail, sizeof(g_detail), "cuTensorMapEncodeTiled entry point unavailable");
@@ -678,7 +678,7 @@ bool tc_make_map(CUtensorMap* map, const void* base, const PassDesc& p) {
   }
   cuuint64_t dims[4] = {(cuuint64_t)p.d, (cuuint64_t)p.n, (cuuint64_t)p.heads, (cuuint64_t)p.batch};
   cuuint64_t strides[3] = {(cuuint64_t)p.sn * 2, (cuuint64_t)p.sh * 2, (cuuint64_t)p.sb * 2};
-  cuuint32_t box[4] = {64, (cuuint32_t)C, 1, 1};
+  cuuint32_t box[4] = {64, (cuuint32_t)box_rows, 1, 1};
   cuuint32_t estr[4] = {1, 1, 1, 1};
   // degenerate strides of size-1 dims must still be valid multiples of 16
   if (p.heads == 1) strides[1] = strides[0] * (cuuint64_t)p.n;
@@ -771,8 +771,8 @@ Plan tc_plan(int64_t bh, int64_t n, int d, int64_t want_segments) {
   (void)d;
   if (want_segments > 0) {
     Plan p = make_plan(bh, n, C, want_segments, kNumSMs, 1);
-    p.nsub_ws = (int)(2 * std::max<int64_t>(p.nseg_ws, kNumSMs / bh) + 2);
-    plan_subsegments(p, bh, kNumSMs, 2, p.nsub_ws);
+    p.nsub_ws = (int)(4 * std::max<int64_t>(p.nseg_ws, kNumSMs / bh) + 4);
+    plan_subsegments(p, bh, 2 * kNumSMs, 2, p.nsub_ws);
     return p;
   }
   const int64_t nchunks = (n + C - 1) / C;
@@ -781,14 +781,16 @@ Plan tc_plan(int64_t bh, int64_t n, int d, int64_t want_segments) {
   if (bh * 10 < kNumSMs * 6) nseg = std::min<int64_t>(cap, std::max<int64_t>(1, nchunks / 2));
   Plan p = make_plan(bh, n, C, nseg, kNumSMs, 1);
   p.nseg_ws = (int)cap;
-  p.nsub_ws = (int)(2 * cap + 2);
-  // summaries: one wave over the segments a scan needs, sub-segments of >= 2 chunks
-  plan_subsegments(p, bh, kNumSMs, 2, p.nsub_ws);
+  p.nsub_ws = (int)(4 * cap + 4);
+  // summaries: one wave of the two-CTAs-per-SM summary kernel over the segments a scan needs,
+  // sub-segments of >= 2 chunks
+  plan_subsegments(p, bh, 2 * kNumSMs, 2, p.nsub_ws);
   return p;
 }
 
 cudaError_t tc_launch(const PassDesc& p, bool state_only, cudaStream_t st) {
-  return state_only ? launch_tc<true>(p, st) : launch_tc<false>(p, st);
+  // summaries: the lean two-CTAs-per-SM kernel of la_summary.cu
+  return state_only ? tc_summary_launch(p, st) : launch_tc<false>(p, st);
 }
 
 }  // namespace la

@@ -9,8 +9,10 @@ bool tc_supported(int dtype, int d, const int64_t* strides);
 bool tc_pointers_ok(const PassDesc& p);
 const char* tc_detail();  // thread-local detail of the last host-side failure
 // 4-D TMA descriptor (d, n, heads, batch) over a bf16 [.., .., .., 128] tensor with the desc's strides,
-// box 64 x 128, 128-byte swizzle
-bool tc_make_map(CUtensorMap* map, const void* base, const PassDesc& p);
+// box 64 x box_rows, 128-byte swizzle
+bool tc_make_map(CUtensorMap* map, const void* base, const PassDesc& p, int box_rows = 128);
+// the segment-summary pass (la_summary.cu): p.delta_out, sub-segment geometry, g_lo..g_hi
+cudaError_t tc_summary_launch(const PassDesc& p, cudaStream_t st);
 Plan tc_plan(int64_t bh, int64_t n, int d, int64_t want_segments);
 // the fused reverse sweep of the backward: dK and dV in one pass over q, k, v, do (p.state_in = the
 // entering adjoint state in dkv orientation; p.state_out = dkv_out, written by segment 0)

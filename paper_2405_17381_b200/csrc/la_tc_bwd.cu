@@ -452,7 +452,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       mbar_wait(&bars.full_d[s], (t >> 1) & 1);
       mbar_wait(&bars.av_full, t & 1);
       {
+#ifndef LA_MUTATE_DKV
         const float isc = i < b ? pw[i + 1] : 0.f;
+#else
+        const float isc = i < b ? -pw[i + 1] : 0.f;  // fault injection: `_dkv_step` sign flip (test_kernels.py:249-268)
+#endif
         const uint32_t isc2 = pack_bf16x2(isc, isc);
         const uint32_t src = slot(SLOT_D + s) + hh * HALF + i * 128;
         const uint32_t dst = slot(SLOT_K) + hh * HALF + i * 128;
