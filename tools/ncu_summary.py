@@ -25,10 +25,13 @@ def launch_table(path):
         a[2] += m.get("dram__bytes_read.sum", 0)
         a[3] += m.get("dram__bytes_write.sum", 0)
     tot = sum(a[1] for a in agg.values())
-    lines = ["kernel | launches | total us | share | avg us | DRAM read MB/launch | DRAM write MB/launch",
-             "---|---|---|---|---|---|---"]
+    tot_la = sum(a[1] for n, a in agg.items() if n.startswith("la::"))  # the step's own kernels
+    lines = ["kernel | launches | total us | share | share of the step (la:: only) | avg us | DRAM read MB/launch | "
+             "DRAM write MB/launch",
+             "---|---|---|---|---|---|---|---"]
     for name, a in sorted(agg.items(), key=lambda x: -x[1][1]):
-        lines.append(f"{name} | {a[0]} | {a[1]/1e3:.1f} | {100*a[1]/tot:.1f}% | {a[1]/a[0]/1e3:.1f} | "
+        step = f"{100*a[1]/tot_la:.1f}%" if name.startswith("la::") else "(input setup, outside the step)"
+        lines.append(f"{name} | {a[0]} | {a[1]/1e3:.1f} | {100*a[1]/tot:.1f}% | {step} | {a[1]/a[0]/1e3:.1f} | "
                      f"{a[2]/a[0]/1e6:.1f} | {a[3]/a[0]/1e6:.1f}")
     return lines
 
