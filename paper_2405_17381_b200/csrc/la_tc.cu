@@ -81,8 +81,7 @@ constexpr uint32_t IDESC_KK = idesc_bf16(128, 128, 0, 0);    // A K-major, B K-m
 constexpr uint32_t IDESC_KMN = idesc_bf16(128, 128, 0, 1);   // A K-major (or TMEM), B MN-major
 constexpr uint32_t IDESC_MNMN = idesc_bf16(128, 128, 1, 1);  // A MN-major, B MN-major
 
-constexpr int NSTAGE_S = 3;  // state-only (summary) mode: no A / state tiles, so three stages of {B, C}
-constexpr int NSTAGE_MAX = 3;
+constexpr int NSTAGE_MAX = NSTAGE;
 
 struct Bars {
   uint64_t full[3][NSTAGE_MAX];   // TMA -> consumers, one ring per operand tile A, B, C (tx bytes)
@@ -100,17 +99,14 @@ struct Bars {
                                  // the TMA only and may run a stage ahead) -> MMA
   uint64_t ds_full;        // MMA: state += B~^T C done        -> state warps
   uint64_t st_ready;       // bf16 state in SMEM, TMEM state pre-scaled -> MMA
-  uint64_t ds_last;        // MMA: last chunk accumulated      -> state warps (state-only mode)
   uint32_t tmem_base;
 };
 
 constexpr size_t SMEM_TILES = (size_t)NSTAGE * 3 * TILE + TILE;  // 224 KB
 constexpr size_t SMEM_BYTES = SMEM_TILES + 1024 /*align slack*/;
-constexpr size_t SMEM_BYTES_S = (size_t)NSTAGE_S * 2 * TILE + 1024;  // 193 KB
 
 struct TcArgs {
   int heads, n, seg_len, nseg, rev;
-  int sub_len, sub_per_seg, g_lo;  // state-only mode: blockIdx.x -> sub-segment (g_lo + x / sub_per_seg, x % ..)
   const double* lam;
   uint16_t* out;  // bf16 output (full mode)
   int64_t sb, sh, sn;
@@ -119,14 +115,12 @@ struct TcArgs {
   int in_T;
   float* state_out;
   int out_T;
-  float* delta_out;
 };
 
 // byte offset of 16-byte chunk `c` (0..7) of row `r` inside a [128][64] bf16 block, 128B swizzle
 __device__ __forceinline__ uint32_t sw128(int r, int c) { return (uint32_t)(r * 128 + ((c ^ (r & 7)) << 4)); }
 
 
-template <bool STATE_ONLY>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     tc_pass_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                    const __grid_constant__ CUtensorMap map_c, const __grid_constant__ CUtensorMap map_o,
@@ -134,15 +128,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   extern __shared__ uint8_t smem_raw[];
   __shared__ Bars bars;
   __shared__ __align__(16) float pw[C + 8];  // lam^0 .. lam^128
-  __shared__ double s_lam;
   const uint32_t smem = (smem_u32(smem_raw) + 1023u) & ~1023u;
   uint8_t* smem_gen = smem_raw + (smem - smem_u32(smem_raw));
-  constexpr int NS = STATE_ONLY ? NSTAGE_S : NSTAGE;  // ring depth
-  constexpr int NT = STATE_ONLY ? 2 : 3;              // tiles per stage: {A,} B, C
-  auto tile_a = [smem](int s) { return smem + (uint32_t)(s * NT * TILE); };
-  auto tile_b = [smem](int s) { return smem + (uint32_t)(s * NT * TILE + (NT - 2) * TILE); };
-  auto tile_c = [smem](int s) { return smem + (uint32_t)(s * NT * TILE + (NT - 1) * TILE); };
-  const uint32_t st_bf16 = smem + (uint32_t)(NSTAGE * 3 * TILE);  // main mode only
+  constexpr int NS = NSTAGE;  // ring depth
+  auto tile_a = [smem](int s) { return smem + (uint32_t)(s * 3 * TILE); };
+  auto tile_b = [smem](int s) { return smem + (uint32_t)(s * 3 * TILE + TILE); };
+  auto tile_c = [smem](int s) { return smem + (uint32_t)(s * 3 * TILE + 2 * TILE); };
+  const uint32_t st_bf16 = smem + (uint32_t)(NSTAGE * 3 * TILE);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #ifdef LA_TRACE
@@ -150,18 +142,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #endif
   const int bh = blockIdx.y;
   const int bi = bh / args.heads, hi = bh % args.heads;
-  // main pass: CTA = segment.  State-only: CTA = summary sub-segment, `seg` = its summary slot.
-  int seg, p0, p1;
-  if (STATE_ONLY) {
-    const int g = args.g_lo + (int)blockIdx.x / args.sub_per_seg, j = (int)blockIdx.x % args.sub_per_seg;
-    seg = g * args.sub_per_seg + j;
-    p0 = g * args.seg_len + j * args.sub_len;
-    p1 = min(min(args.n, (g + 1) * args.seg_len), p0 + args.sub_len);
-  } else {
-    seg = blockIdx.x;
-    p0 = seg * args.seg_len;
-    p1 = min(args.n, p0 + args.seg_len);
-  }
+  const int seg = blockIdx.x;  // CTA = one segment of one (batch, head)
+  const int p0 = seg * args.seg_len;
+  const int p1 = min(args.n, p0 + args.seg_len);
   const int nchunks = p1 > p0 ? (p1 - p0 + C - 1) / C : 0;
   const int rev = args.rev;
 
@@ -186,23 +169,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     mbar_init(&bars.ds_full, 1);
     mbar_init(&bars.x_done, 1);
     mbar_init(&bars.st_ready, NUM_KV);
-    mbar_init(&bars.ds_last, 1);
     fence_mbar_init();
     double x = 1.0;
     const double lam = args.lam[hi];
-    s_lam = lam;
     for (int k = 0; k <= C; ++k) {
       pw[k] = (float)x;
       x *= lam;
     }
   }
   if (warp == WARP_TMA && lane == 0) {
+    tma_prefetch(&map_a);
     tma_prefetch(&map_b);
     tma_prefetch(&map_c);
-    if (!STATE_ONLY) {
-      tma_prefetch(&map_a);
-      tma_prefetch(&map_o);
-    }
+    tma_prefetch(&map_o);
   }
   if (warp == WARP_MMA) tmem_alloc(&bars.tmem_base, TM_COLS);
   tc_fence_before();
@@ -218,7 +197,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // Lanes 0/1/2 each run the ring of one operand tile (A, B, C), so a tile is refilled as soon as
     // its own last reader retires: A after X(t), B after the state update, C after Y(t).
     const int x = lane;
-    if (x < 3 && !(STATE_ONLY && x == 0)) {
+    if (x < 3) {
       const CUtensorMap* map = x == 0 ? &map_a : (x == 1 ? &map_b : &map_c);
       for (int t = 0; t < nchunks; ++t) {
         const int s = t % NS;
@@ -228,11 +207,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (x == 0) LA_TR(t, 0);
         if (x == 1) LA_TR(t, 16);
         if (x == 2) LA_TR(t, 17);
-        uint8_t* g = smem_gen + (s * NT + x - (3 - NT)) * TILE;
+        uint8_t* g = smem_gen + (s * 3 + x) * TILE;
         tma_load_4d(map, &bars.full[x][s], g, 0, r0, hi, bi);
         tma_load_4d(map, &bars.full[x][s], g + HALF, 64, r0, hi, bi);
       }
-    } else if (x == 3 && !STATE_ONLY) {
+    } else if (x == 3) {
       // store lane: bf16 O(t) is staged in C(t)'s slot (C's MMA readers are done by then); TMA-store it
       // and hand the slot back to the C ring once the store has read it
       for (int t = 0; t < nchunks; ++t) {
@@ -270,7 +249,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         LA_TR(t, 1);
       };
       int s_issued = 0;  // S issued for chunks < s_issued
-      if (!STATE_ONLY && nchunks > 0) {
+      if (nchunks > 0) {
         issue_s(0);
         s_issued = 1;
       }
@@ -278,17 +257,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const int s = t % NS;
         const uint32_t b_addr = tile_b(s), c_addr = tile_c(s);
         const uint32_t sbuf = tmem + TM_S0 + (t & 1) * 128;
-        if (!STATE_ONLY && s_issued == t + 1 && t + 1 < nchunks &&
+        if (s_issued == t + 1 && t + 1 < nchunks &&
             mbar_try_wait(smem_u32(&bars.full[0][(t + 1) % NSTAGE]), ((t + 1) / NSTAGE) & 1) &&
             mbar_try_wait(smem_u32(&bars.full[1][(t + 1) % NSTAGE]), ((t + 1) / NSTAGE) & 1)) {
           issue_s(t + 1);  // run ahead: S(t+1) as soon as its operands landed
           s_issued = t + 2;
         }
-        if (STATE_ONLY) mbar_wait(&bars.full[1][s], (t / NS) & 1);
         // st_ready(t): bf16 state_{t-1} in SMEM and the TMEM state pre-scaled by lam^b.  State-only
         // mode folds the decay into B~ instead and accumulates straight onto the zeroed state.
-        if (!STATE_ONLY || t == 0) mbar_wait(&bars.st_ready, t & 1);
-        if (!STATE_ONLY) {
+        mbar_wait(&bars.st_ready, t & 1);
+        {
           // X(t) = A~ state_{t-1}  -> O (fresh accumulation)
           if (t >= 1) mbar_wait(&bars.o_free, (t - 1) & 1);
           mbar_wait(&bars.a_full[t & 1], (t >> 1) & 1);
@@ -310,13 +288,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         for (int kk = 0; kk < C / 16; ++kk)
           mma_bf16_ss(tmem + TM_ST, smem_desc_sw128(b_addr + kk * 2048, HALF, 1024),
                       smem_desc_sw128(c_addr + kk * 2048, HALF, 1024), IDESC_MNMN, 1);
-        if (!STATE_ONLY)
-          mma_commit(&bars.ds_full);
-        else if (t == nchunks - 1)
-          mma_commit(&bars.ds_last);
+        mma_commit(&bars.ds_full);
         mma_commit(&bars.empty[1][s]);  // B's last reader
         LA_TR(t, 5);
-        if (!STATE_ONLY) {
+        {
           // Y(t) = P C  -> O (accumulate)
           mbar_wait(&bars.p_full[t & 1], (t >> 1) & 1);
           LA_TR(t, 2);
@@ -332,8 +307,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           mma_commit(&bars.y_done[t & 1]);
           LA_TR(t, 3);
         }
-        if (STATE_ONLY) mma_commit(&bars.empty[2][s]);  // C's last reader (else: the store lane frees it)
-        if (!STATE_ONLY && s_issued == t + 1 && t + 1 < nchunks) {
+        if (s_issued == t + 1 && t + 1 < nchunks) {
           issue_s(t + 1);
           s_issued = t + 2;
         }
@@ -341,14 +315,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       // Drain: every asynchronous tcgen05.commit arrival must land before this CTA retires, or it
       // would hit the barriers of the next CTA scheduled onto this SM's shared memory.
       for (int t = max(0, nchunks - NS); t < nchunks; ++t) {
-        for (int x = STATE_ONLY ? 1 : 0; x < 3; ++x) mbar_wait(&bars.empty[x][t % NS], (t / NS) & 1);
-        if (STATE_ONLY && t == nchunks - 1) mbar_wait(&bars.ds_last, 0);
-        if (!STATE_ONLY) mbar_wait(&bars.y_done[t & 1], (t >> 1) & 1);
+        for (int x = 0; x < 3; ++x) mbar_wait(&bars.empty[x][t % NS], (t / NS) & 1);
+        mbar_wait(&bars.y_done[t & 1], (t >> 1) & 1);
       }
     }
   } else if (warp < WARP_O) {
     // ------------------------------------------------------------ A~ / P conversion (warps 2..9)
-    if (!STATE_ONLY) {
+    {
       const int quad = warp & 3;
       const int half = (warp - WARP_P) >> 2;  // A~ columns [64 half, +64); key blocks {half, half + 2}
       const int i = quad * 32 + lane;         // chunk row == TMEM lane
@@ -473,48 +446,34 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const int s = t % NS;
       const int r0 = chunk_row0(t);
       const int b = chunk_len(t);
-      if (STATE_ONLY)
-        mbar_wait(&bars.full[1][s], (t / NS) & 1);
-      else
-        mbar_wait(&bars.s_full[t & 1], (t >> 1) & 1);
+      mbar_wait(&bars.s_full[t & 1], (t >> 1) & 1);
       if (warp == WARP_O && lane == 0) LA_TR(t, 11);
       // B~ = in_scale * B, in place once S has consumed B (row i, this warp's 64 columns):
       // fwd lam^(b-1-i), rev lam^(i+1).  Row scaling is order-free, so visit the row's 16-byte chunks in
       // swizzled order: lane i touches physical chunk m ^ (i & 7), spreading a warp over all 32 banks.
       {
         float isc = (i < b) ? (rev ? pw[i + 1] : pw[b - 1 - i]) : 0.f;
-        if (STATE_ONLY) {
-          // state-only: weight rows by their full distance to the segment's far edge, lam^(p1-1-s) (fwd)
-          // or lam^(s-p0+1) (rev), so chunks accumulate without decaying the running state
-          isc *= (float)pow(s_lam, (double)(rev ? (r0 - p0) : (p1 - r0 - b)));
-        }
 #ifdef LA_MUTATE_DKV
         if (rev) isc = -isc;  // fault injection: the reference's `_dkv_step` sign flip (test_kernels.py:249-268)
 #endif
         const uint32_t isc2 = pack_bf16x2(isc, isc);
         const uint32_t base = tile_b(s) + hh * HALF + i * 128;
-#ifndef LA_KO_B
         uint4 x[8];
 #pragma unroll
         for (int m = 0; m < 8; ++m) x[m] = lds128(base + ((m ^ (i & 7)) << 4));
 #pragma unroll
         for (int m = 0; m < 8; ++m) sts128(base + ((m ^ (i & 7)) << 4), mul_bf16x2(x[m], isc2));
-#else
-        (void)isc2; (void)base;
-#endif
       }
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars.b_scaled[s]);
       if (warp == WARP_O && lane == 0) LA_TR(t, 12);
-      if (STATE_ONLY) continue;
       // out = bf16(O): TMEM -> registers (then O's columns are released) -> C's SMEM slot -> TMA store
       (void)r0;
       mbar_wait(&bars.o_full, t & 1);
       if (warp == WARP_O && lane == 0) LA_TR(t, 8);
       tc_fence_after();
       uint32_t pk[32];
-#ifndef LA_KO_O
 #pragma unroll
       for (int cb = 0; cb < 2; ++cb) {
         float y[32];
@@ -523,22 +482,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
         for (int e = 0; e < 16; ++e) pk[cb * 16 + e] = pack_bf16x2(y[2 * e], y[2 * e + 1]);
       }
-#else
-      (void)o_cols;
-#pragma unroll
-      for (int e = 0; e < 32; ++e) pk[e] = 0u;
-#endif
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars.o_free);  // O's TMEM is free; the stores proceed from registers
-#ifndef LA_KO_O
       {
         const uint32_t base = tile_c(s) + hh * HALF;
 #pragma unroll
         for (int m = 0; m < 8; ++m)
           sts128(base + sw128(i, m), make_uint4(pk[4 * m], pk[4 * m + 1], pk[4 * m + 2], pk[4 * m + 3]));
       }
-#endif
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars.o_staged[s]);
@@ -550,9 +502,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const int hh = (warp - WARP_KV) >> 2;  // which 64 state columns
     const int i = quad * 32 + lane;        // state row (d_k index) == TMEM lane
     const uint32_t st_cols = tmem + ((uint32_t)(quad * 32) << 16) + TM_ST + hh * 64;
-    // publish bf16(state) to SMEM (unless state-only) and pre-scale the TMEM state by `next_decay`
+    // publish bf16(state) to SMEM and pre-scale the TMEM state by `next_decay`
     auto publish = [&](const float (&x)[16], int q4, float next_decay) {
-      if (!STATE_ONLY) {
+      {
         const uint32_t base = st_bf16 + hh * HALF;
         sts128(base + sw128(i, 2 * q4),
                make_uint4(pack_bf16x2(x[0], x[1]), pack_bf16x2(x[2], x[3]), pack_bf16x2(x[4], x[5]),
@@ -569,7 +521,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     auto signal_ready = [&]() {
       tmem_st_wait();
       tc_fence_before();
-      if (!STATE_ONLY) fence_proxy_async_smem();
+      fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars.st_ready);
     };
@@ -578,7 +530,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll 1
       for (int q4 = 0; q4 < 4; ++q4) {
         float x[16];
-        if (!STATE_ONLY && args.state_in != nullptr) {
+        if (args.state_in != nullptr) {
           const float* src = args.state_in + (int64_t)bh * args.in_bh_stride + (int64_t)seg * args.in_seg_stride;
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
@@ -593,16 +545,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
       signal_ready();
     }
-    for (int t = 0; t < (STATE_ONLY ? 0 : nchunks); ++t) {
+    for (int t = 0; t < nchunks; ++t) {
       // the tensor core accumulated this chunk: read the state, publish it for chunk t+1 once X(t)
       // has finished reading the previous bf16 copy
       mbar_wait(&bars.ds_full, t & 1);
-      if (!STATE_ONLY) mbar_wait(&bars.x_done, t & 1);
+      mbar_wait(&bars.x_done, t & 1);
       if (warp == WARP_KV && lane == 0) LA_TR(t, 13);
       tc_fence_after();
       if (t + 1 < nchunks) {
         const float next_decay = pw[chunk_len(t + 1)];
-#ifndef LA_KO_ST
 #pragma unroll 1
         for (int q4 = 0; q4 < 4; ++q4) {
           float x[16];
@@ -610,27 +561,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           tmem_ld_wait();
           publish(x, q4, next_decay);
         }
-#else
-        (void)next_decay;
-#endif
         signal_ready();
       }
       if (warp == WARP_KV && lane == 0) LA_TR(t, 14);
     }
-    if (STATE_ONLY && nchunks > 0) {
-      mbar_wait(&bars.ds_last, 0);
-      tc_fence_after();
-    }
-    if (nchunks > 0) {
-      float* dst = nullptr;
-      int T = 0;
-      if (STATE_ONLY) {
-        dst = args.delta_out + ((int64_t)bh * args.nseg * args.sub_per_seg + seg) * D * D;
-      } else if (args.state_out != nullptr && (rev ? seg == 0 : seg == args.nseg - 1)) {
-        dst = args.state_out + (int64_t)bh * D * D;
-        T = args.out_T;
-      }
-      if (dst != nullptr) {
+    if (nchunks > 0 && args.state_out != nullptr && (rev ? seg == 0 : seg == args.nseg - 1)) {
+      // the pass's final state F(n) / R(0): kv_out / dkv_out
+      float* dst = args.state_out + (int64_t)bh * D * D;
+      const int T = args.out_T;
+      {
 #pragma unroll 1
         for (int q4 = 0; q4 < 4; ++q4) {
           float x[16];
@@ -696,13 +635,12 @@ bool tc_make_map(CUtensorMap* map, const void* base, const PassDesc& p, int box_
 
 namespace {
 
-template <bool STATE_ONLY>
 cudaError_t launch_tc(const PassDesc& p, cudaStream_t st) {
   CUtensorMap ma, mb, mc, mo;
   std::memset(&ma, 0, sizeof(ma));
   std::memset(&mo, 0, sizeof(mo));
   if (!tc_make_map(&mb, p.b, p) || !tc_make_map(&mc, p.c, p)) return cudaErrorInvalidValue;
-  if (!STATE_ONLY && (!tc_make_map(&ma, p.a, p) || !tc_make_map(&mo, p.out, p))) return cudaErrorInvalidValue;
+  if (!tc_make_map(&ma, p.a, p) || !tc_make_map(&mo, p.out, p)) return cudaErrorInvalidValue;
   TcArgs a;
   a.out = reinterpret_cast<uint16_t*>(p.out);
   a.sb = p.sb;
@@ -720,15 +658,11 @@ cudaError_t launch_tc(const PassDesc& p, cudaStream_t st) {
   a.in_T = p.state_in_T;
   a.state_out = reinterpret_cast<float*>(p.state_out);
   a.out_T = p.state_out_T;
-  a.delta_out = reinterpret_cast<float*>(p.delta_out);
-  a.sub_len = p.sub_len;
-  a.sub_per_seg = p.sub_per_seg;
-  a.g_lo = p.g_lo;
-  auto kern = tc_pass_kernel<STATE_ONLY>;
-  const size_t smem_bytes = STATE_ONLY ? SMEM_BYTES_S : SMEM_BYTES;
+  auto kern = tc_pass_kernel;
+  const size_t smem_bytes = SMEM_BYTES;
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes);
   if (err != cudaSuccess) return err;
-  dim3 grid(STATE_ONLY ? (p.g_hi - p.g_lo + 1) * p.sub_per_seg : p.nseg, p.batch * p.heads);
+  dim3 grid(p.nseg, p.batch * p.heads);
   kern<<<grid, NUM_THREADS, smem_bytes, st>>>(ma, mb, mc, mo, a);
   return cudaGetLastError();
 }
@@ -790,7 +724,7 @@ Plan tc_plan(int64_t bh, int64_t n, int d, int64_t want_segments) {
 
 cudaError_t tc_launch(const PassDesc& p, bool state_only, cudaStream_t st) {
   // summaries: the lean two-CTAs-per-SM kernel of la_summary.cu
-  return state_only ? tc_summary_launch(p, st) : launch_tc<false>(p, st);
+  return state_only ? tc_summary_launch(p, st) : launch_tc(p, st);
 }
 
 }  // namespace la
