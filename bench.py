@@ -254,14 +254,25 @@ def measure_rows(ops, device, stream, pk) -> dict:
     g = torch.Generator(device=device).manual_seed(7)
     rnd = lambda *shape: (torch.randn(*shape, device=device, generator=g) * 0.5).to(torch.bfloat16)  # noqa: E731
     lam = [decay_rate(h, 1, H, L_LAYERS) for h in range(1, H + 1)]
-    # decode: 64 sequences x 16 heads, one token each per step; fp32 states read + written once
-    bsz = 64
+    # decode: 256 sequences x 16 heads, one token each per step; fp32 states (256 MB, > L2) read + written
+    # once per step
+    bsz = 256
     q, k, v = rnd(bsz, H, D), rnd(bsz, H, D), rnd(bsz, H, D)
     kv = torch.zeros(bsz, H, D, D, device=device, dtype=torch.float32)
     lam_dev = ops.decay_tensor(lam, H, device)
-    ms = _time_ms(lambda: ops.la_decode(q, k, v, None, kv, lam_dev=lam_dev), stream, reps=50)
+    # a decode step is a few microseconds of GPU work, below the host's per-call overhead: time it as a
+    # CUDA graph of 32 steps (what a serving loop replays), per-step time = graph time / 32
+    steps_per_graph = 32
+    for _ in range(3):
+        ops.la_decode(q, k, v, None, kv, lam_dev=lam_dev)
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        for _ in range(steps_per_graph):
+            ops.la_decode(q, k, v, None, kv, lam_dev=lam_dev)
+    ms = _time_ms(graph.replay, stream, reps=10) / steps_per_graph
     state_bytes = bsz * H * D * D * 4 * 2
-    out["decode"] = {"batch": bsz, "heads": H, "head_dim": D, "ms_per_step": round(ms, 4),
+    out["decode"] = {"batch": bsz, "heads": H, "head_dim": D, "ms_per_step": round(ms, 5), "timing": "CUDA graph of 32 steps",
                      "tokens_per_s": round(bsz / (ms / 1e3)), "state_gbs": round(state_bytes / (ms / 1e3) / 1e9, 1),
                      "frac_hbm": round(state_bytes / (ms / 1e3) / 1e9 / pk["hbm_gbs"], 3)}
     # GLA stages on [8, 8192, 2048] (64K tokens), LRPE on

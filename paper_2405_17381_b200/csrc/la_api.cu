@@ -167,15 +167,18 @@ void* ws_seg_in(void* ws, const la_desc* desc, const la::Plan& plan) {
                                       desc->d * desc->d;
 }
 
-// This library carries its own (static) CUDA runtime.  A caller's thread may
-// have its device selected only through another runtime instance (e.g.
-// torch's autograd worker threads), so every entry binds the context that owns
-// the caller's stream before touching the runtime or the driver.
+// This library carries its own (static) CUDA runtime.  A caller's thread may have selected its device
+// only through another runtime instance (e.g. torch's autograd worker threads), so every entry binds
+// the context that owns the caller's stream before touching the runtime.  The driver entry points
+// are requested at the CUDA 12.0 ABI: the default cuStreamGetCtx is the three-argument _v2, and
+// calling it with two arguments (an earlier version did) corrupted memory -- it crashed under CUDA
+// graph capture.  (cudaStreamGetDevice would be simpler but invalidates a capture in progress.)
 template <typename F>
 F driver_fn(const char* name) {
   void* p = nullptr;
   cudaDriverEntryPointQueryResult q;
-  if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess)
+  if (cudaGetDriverEntryPointByVersion(name, &p, 12000, cudaEnableDefault, &q) != cudaSuccess ||
+      q != cudaDriverEntryPointSuccess)
     return nullptr;
   return reinterpret_cast<F>(p);
 }

@@ -1,0 +1,44 @@
+"""The C ABI is stream-ordered and capture-safe (include/lightning_attn.h): forward, backward (with
+sequence segments and the side-stream summaries), decode and the GLA stages replay from a CUDA graph
+with the same results as eager calls."""
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def test_forward_backward_decode_replay_from_a_cuda_graph():
+    from paper_2405_17381_b200 import ops
+    dev = torch.device("cuda", 0)
+    torch.manual_seed(0)
+    b, h, n, d = 1, 4, 4096, 128  # bh = 4: the plan splits each sequence into segments
+    q, k, v, do = (torch.randn(b, h, n, d, device=dev, dtype=torch.bfloat16) * d ** -0.5 for _ in range(4))
+    lam = ops.decay_tensor([0.99, 0.9, 0.5, 1.0], h, dev)
+    assert ops.segment_count(ops._desc(ops._geometry(q, "bhnd"), q.dtype, None, "auto", 0)) > 1
+    qd, kd, vd = (torch.randn(8, h, d, device=dev, dtype=torch.bfloat16) for _ in range(3))
+    kv0 = torch.randn(8, h, d, d, device=dev) * 0.01
+
+    def step(kv):
+        o, seg = ops.la_forward(q, k, v, None, lam_dev=lam, want_seg_states=True)
+        dq, dk, dv = ops.la_backward(q, k, v, do, None, lam_dev=lam, fwd_seg_states=seg)
+        od = ops.la_decode(qd, kd, vd, None, kv, lam_dev=lam)
+        return o, dq, dk, dv, od
+
+    kv_eager = kv0.clone()
+    want = [t.clone() for t in step(kv_eager)]
+    kv_graph = kv0.clone()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        step(kv_graph.clone())  # warm-up on the capture stream
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        got = step(kv_graph)
+    g.replay()
+    torch.cuda.synchronize()
+    for a, w in zip(got, want):
+        assert torch.equal(a, w)
+    assert torch.equal(kv_graph, kv_eager)
