@@ -51,8 +51,9 @@ __device__ __forceinline__ void rot_cs(double theta, int64_t pos, Tacc* c, Tacc*
     *c = (Tacc)cc;
     *s = (Tacc)ss;
   } else {
+    // |ang| <= pi after the fp64 reduction: the hardware approximation is accurate to ~2^-21 there
     float cc, ss;
-    sincosf((float)ang, &ss, &cc);
+    __sincosf((float)ang, &ss, &cc);
     *c = (Tacc)cc;
     *s = (Tacc)ss;
   }
