@@ -1,4 +1,6 @@
-# small fwd+bwd on both backends, for compute-sanitizer (memcheck / racecheck / synccheck)
+# small runs of every kernel for compute-sanitizer (memcheck / racecheck / synccheck): the tcgen05 pass,
+# dK/dV sweep, summary and scan kernels (segmented), the SIMT path, decode (bulk and generic), the GLA
+# stages (with LRPE) and the TP stages
 import sys, torch
 sys.path.insert(0, '.')
 from paper_2405_17381_b200 import ops
@@ -7,5 +9,19 @@ for dtype, backend, n, segs in ((torch.bfloat16, "tcgen05", 300, 0), (torch.bflo
     q, k, v, do = (torch.rand(1, 2, n, 128, device="cuda", dtype=dtype) for _ in range(4))
     o, seg = ops.la_forward(q, k, v, [0.9, 0.99], backend=backend, segments=segs, want_seg_states=True)
     ops.la_backward(q, k, v, do, [0.9, 0.99], backend=backend, segments=segs, fwd_seg_states=seg)
+for dtype, d in ((torch.bfloat16, 128), (torch.float32, 128), (torch.float64, 64), (torch.float32, 40)):
+    q, k, v = (torch.rand(3, 2, d, device="cuda", dtype=dtype) for _ in range(3))
+    kv = torch.rand(3, 2, d, d, device="cuda", dtype=ops.state_dtype(dtype))
+    ops.la_decode(q, k, v, [0.9, 0.5], kv)
+for dtype in (torch.bfloat16, torch.float32):
+    qp, kp, a, u, g = (torch.rand(2, 37, 256, device="cuda", dtype=dtype) for _ in range(5))
+    theta = torch.rand(32, dtype=torch.float64)
+    ops.gla_prologue(qp, kp, 4, theta=theta, offset=5)
+    ops.gla_prologue_backward(qp, kp, a, u, 4, theta=theta, offset=5)
+    gated, raw = ops.gla_epilogue(a, u, 4)
+    ops.gla_epilogue_backward(g, a, u, raw, 4)
+    red = torch.zeros(74, 257, device="cuda", dtype=ops.state_dtype(dtype))
+    ops.gla_gate_rowsq(a, u, 4, red[:, 256], rowsq_stride=257)
+    ops.gla_rowscale(red, 256)
 torch.cuda.synchronize()
 print("ok")
