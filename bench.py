@@ -292,6 +292,23 @@ def measure_rows(ops, device, stream, pk) -> dict:
     stages["prologue_bwd"] = (ms, 6 * row_bytes)
     out["gla_stages"] = {k: {"ms": round(t, 4), "gbs": round(by / (t / 1e3) / 1e9, 1),
                              "frac_hbm": round(by / (t / 1e3) / 1e9 / pk["hbm_gbs"], 3)} for k, (t, by) in stages.items()}
+    # BASELINE configs[1]: the TNL-385M attention shape (H = 8, d = 128), n = 2K..16K at 64K tokens/batch
+    cfg385 = {}
+    lam8 = ops.decay_tensor([decay_rate(h, 1, 8, 24) for h in range(1, 9)], 8, device)
+    for n385 in (2048, 4096, 8192, 16384):
+        bt = TOKENS // n385
+        qq, kk, vv, dd = (rnd(bt, 8, n385, D) for _ in range(4))
+
+        def fb():
+            _, seg = ops.la_forward(qq, kk, vv, None, lam_dev=lam8, want_seg_states=True)
+            ops.la_backward(qq, kk, vv, dd, None, lam_dev=lam8, fwd_seg_states=seg)
+
+        t = _time_ms(fb, stream, reps=5)
+        cfg385[str(n385)] = {"batch": bt, "ms_fwd_bwd": round(t, 4), "tokens_per_s": round(TOKENS / (t / 1e3)),
+                          "pct_bf16_peak": round(100 * TOKENS / (t / 1e3) * 8 * FLOPS_PER_HEAD_TOKEN
+                                                 / (pk["bf16_tflops"] * 1e12), 2)}
+        del qq, kk, vv, dd
+    out["tnl385m_attention"] = cfg385
     # the whole GLA layer, fwd + bwd through autograd
     x = rnd(b, n, w).requires_grad_(True)
     ws = gla.GlaWeights(*(rnd(w, w).mul_(w ** -0.5 * 2).requires_grad_(True) for _ in range(5)))
