@@ -23,20 +23,39 @@ namespace la {
 
 namespace {
 
+// fp32 accumulation uses the SFU forms (ex2 + rcp approximations, ~2^-21 relative): the stages are
+// bound by instruction issue otherwise; fp64 keeps the library functions
 template <typename Tacc>
-__device__ __forceinline__ Tacc act_fwd(Tacc x, int act) {
-  if (act == LA_ACT_SWISH) return x * (Tacc)0.5 * ((Tacc)1 + tanh((Tacc)0.5 * x));  // tanh form, model.py:57-66
-  if (act == LA_ACT_ONE_PLUS_ELU) return x > (Tacc)0 ? x + (Tacc)1 : exp(x);
-  return x;
+__device__ __forceinline__ Tacc sigmoid(Tacc x) {
+  if constexpr (sizeof(Tacc) == 8) return (Tacc)0.5 * ((Tacc)1 + tanh((Tacc)0.5 * x));  // tanh form, model.py:57-66
+  else return __fdividef(1.f, 1.f + __expf(-x));
 }
 template <typename Tacc>
-__device__ __forceinline__ Tacc act_grad(Tacc x, int act) {
+__device__ __forceinline__ Tacc expo(Tacc x) {
+  if constexpr (sizeof(Tacc) == 8) return exp(x);
+  else return __expf(x);
+}
+template <typename Tacc>
+__device__ __forceinline__ Tacc act_fwd(Tacc x, int act) {
+  if (act == LA_ACT_SWISH) return x * sigmoid(x);
+  if (act == LA_ACT_ONE_PLUS_ELU) return x > (Tacc)0 ? x + (Tacc)1 : expo(x);
+  return x;
+}
+// act(x) and act'(x) sharing one sigmoid / exp
+template <typename Tacc>
+__device__ __forceinline__ void act_both(Tacc x, int act, Tacc& a, Tacc& g) {
   if (act == LA_ACT_SWISH) {
-    const Tacc s = (Tacc)0.5 * ((Tacc)1 + tanh((Tacc)0.5 * x));
-    return s * ((Tacc)1 + x * ((Tacc)1 - s));
+    const Tacc s = sigmoid(x);
+    a = x * s;
+    g = s * ((Tacc)1 + x * ((Tacc)1 - s));
+  } else if (act == LA_ACT_ONE_PLUS_ELU) {
+    const Tacc e = expo(x < (Tacc)0 ? x : (Tacc)0);
+    a = x > (Tacc)0 ? x + (Tacc)1 : e;
+    g = x > (Tacc)0 ? (Tacc)1 : e;
+  } else {
+    a = x;
+    g = (Tacc)1;
   }
-  if (act == LA_ACT_ONE_PLUS_ELU) return x > (Tacc)0 ? (Tacc)1 : exp(x);
-  return (Tacc)1;
 }
 
 // cos / sin of theta (t + offset): the angle is formed and reduced mod 2 pi in fp64, so long
@@ -59,6 +78,36 @@ __device__ __forceinline__ void rot_cs(double theta, int64_t pos, Tacc* c, Tacc*
   }
 }
 
+// LRPE angles along consecutive rows of one column vector: exact (fp64-reduced) at the first row, at
+// every sequence start and every kAnchor rows; in between the angle-addition step
+// (c, s) <- (c, s) * (cos th, sin th) (4 FMAs, ~1e-7 relative drift per step).  fp64 is exact per row.
+constexpr int kAnchor = 16;
+template <typename Tacc, int NP>
+struct RotWalk {
+  double th[NP];
+  Tacc c[NP], s[NP], c1[NP], s1[NP];
+  __device__ __forceinline__ void init(const double* theta, int j0, int hd) {
+#pragma unroll
+    for (int pr = 0; pr < NP; ++pr) {
+      th[pr] = theta[(j0 + pr) % hd];
+      rot_cs<Tacc>(th[pr], 1, &c1[pr], &s1[pr]);
+    }
+  }
+  // angles of position `pos`; `fresh`: no valid previous position (pos - 1) in registers
+  __device__ __forceinline__ void at(int64_t pos, bool fresh) {
+#pragma unroll
+    for (int pr = 0; pr < NP; ++pr) {
+      if (sizeof(Tacc) == 8 || fresh) {
+        rot_cs<Tacc>(th[pr], pos, &c[pr], &s[pr]);
+      } else {
+        const Tacc cn = c[pr] * c1[pr] - s[pr] * s1[pr];
+        s[pr] = s[pr] * c1[pr] + c[pr] * s1[pr];
+        c[pr] = cn;
+      }
+    }
+  }
+};
+
 // 16-byte vectors of the operand type (8 bf16, 4 fp32, 2 fp64 = 4, 2, 1 feature pairs)
 template <typename T> struct Vec {
   static constexpr int N = 16 / sizeof(T);
@@ -75,39 +124,48 @@ __device__ __forceinline__ void stv(T* p, const Vec<T>& r) {
   *reinterpret_cast<uint4*>(p) = *reinterpret_cast<const uint4*>(r.v);
 }
 
-// one thread per 16-byte vector of one row (its feature pairs share the row's position)
+// grid (ceil(rows / kRowsFwd), ceil(width/V / blockDim)): a thread owns one 16-byte column vector and walks
+// kRowsFwd consecutive rows (its feature pairs' angles advance by one position per row)
+constexpr int kRowsFwd = 16;
 template <typename T, typename Tacc>
-__global__ void prologue_kernel(const T* __restrict__ qp, const T* __restrict__ kp, const double* __restrict__ theta,
-                                T* __restrict__ q, T* __restrict__ k, int64_t rows, int n, int width, int d,
-                                int64_t offset, int act) {
+__global__ void __launch_bounds__(256) prologue_kernel(const T* __restrict__ qp, const T* __restrict__ kp,
+                                                       const double* __restrict__ theta, T* __restrict__ q,
+                                                       T* __restrict__ k, int64_t rows, int n, int width, int d,
+                                                       int64_t offset, int act) {
   constexpr int V = Vec<T>::N;
-  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int vw = width / V;
-  if (idx >= rows * vw) return;
-  const int64_t row = idx / vw;
-  const int c0 = (int)(idx % vw) * V;
-  const int64_t e = row * width + c0;
-  const Vec<T> xq = ldv(qp + e), xk = ldv(kp + e);
-  Vec<T> oq, ok;
-  const int64_t pos = row % n + offset;
+  const int vc = blockIdx.y * blockDim.x + threadIdx.x;
+  if (vc >= vw) return;
+  const int c0 = vc * V;
+  RotWalk<Tacc, V / 2> rw;
+  if (theta != nullptr) rw.init(theta, c0 >> 1, d >> 1);
+  const int64_t r0 = (int64_t)blockIdx.x * kRowsFwd;
+  const int64_t r1 = r0 + kRowsFwd < rows ? r0 + kRowsFwd : rows;
+#pragma unroll 2
+  for (int64_t row = r0; row < r1; ++row) {
+    const int64_t e = row * width + c0;
+    const Vec<T> xq = ldv(qp + e), xk = ldv(kp + e);
+    Vec<T> oq, ok;
+    const int64_t tp = row % n;
+    if (theta != nullptr) rw.at(tp + offset, row == r0 || tp == 0 || ((row - r0) % kAnchor) == 0);
 #pragma unroll
-  for (int pr = 0; pr < V / 2; ++pr) {
-    Tacc q1 = act_fwd<Tacc>((Tacc)Cvt<T>::to_f(xq.v[2 * pr]), act), q2 = act_fwd<Tacc>((Tacc)Cvt<T>::to_f(xq.v[2 * pr + 1]), act);
-    Tacc k1 = act_fwd<Tacc>((Tacc)Cvt<T>::to_f(xk.v[2 * pr]), act), k2 = act_fwd<Tacc>((Tacc)Cvt<T>::to_f(xk.v[2 * pr + 1]), act);
-    if (theta != nullptr) {
-      Tacc c, s;
-      rot_cs<Tacc>(theta[((c0 >> 1) + pr) % (d >> 1)], pos, &c, &s);
-      const Tacc a1 = q1 * c - q2 * s, a2 = q1 * s + q2 * c;
-      const Tacc b1 = k1 * c - k2 * s, b2 = k1 * s + k2 * c;
-      q1 = a1, q2 = a2, k1 = b1, k2 = b2;
+    for (int pr = 0; pr < V / 2; ++pr) {
+      Tacc q1 = act_fwd<Tacc>((Tacc)Cvt<T>::to_f(xq.v[2 * pr]), act), q2 = act_fwd<Tacc>((Tacc)Cvt<T>::to_f(xq.v[2 * pr + 1]), act);
+      Tacc k1 = act_fwd<Tacc>((Tacc)Cvt<T>::to_f(xk.v[2 * pr]), act), k2 = act_fwd<Tacc>((Tacc)Cvt<T>::to_f(xk.v[2 * pr + 1]), act);
+      if (theta != nullptr) {
+        const Tacc c = rw.c[pr], s = rw.s[pr];
+        const Tacc a1 = q1 * c - q2 * s, a2 = q1 * s + q2 * c;
+        const Tacc b1 = k1 * c - k2 * s, b2 = k1 * s + k2 * c;
+        q1 = a1, q2 = a2, k1 = b1, k2 = b2;
+      }
+      oq.v[2 * pr] = Cvt<T>::from_f(q1);
+      oq.v[2 * pr + 1] = Cvt<T>::from_f(q2);
+      ok.v[2 * pr] = Cvt<T>::from_f(k1);
+      ok.v[2 * pr + 1] = Cvt<T>::from_f(k2);
     }
-    oq.v[2 * pr] = Cvt<T>::from_f(q1);
-    oq.v[2 * pr + 1] = Cvt<T>::from_f(q2);
-    ok.v[2 * pr] = Cvt<T>::from_f(k1);
-    ok.v[2 * pr + 1] = Cvt<T>::from_f(k2);
+    stv(q + e, oq);
+    stv(k + e, ok);
   }
-  stv(q + e, oq);
-  stv(k + e, ok);
 }
 
 constexpr int kRowsPerBlock = 64;
@@ -135,28 +193,32 @@ __global__ void __launch_bounds__(256) prologue_bwd_kernel(const T* __restrict__
   for (int pr = 0; pr < V / 2; ++pr) acc[pr] = 0;
   const int c0 = vc * V;
   if (vc < vw) {
-    double th[V / 2];
-#pragma unroll
-    for (int pr = 0; pr < V / 2; ++pr) th[pr] = theta != nullptr ? theta[((c0 >> 1) + pr) % hd] : 0.0;
+    RotWalk<Tacc, V / 2> rw;
+    if (theta != nullptr) rw.init(theta, c0 >> 1, hd);
     const int64_t r0 = (int64_t)blockIdx.y * kRowsPerBlock;
     const int64_t r1 = r0 + kRowsPerBlock < rows ? r0 + kRowsPerBlock : rows;
+#pragma unroll 2
     for (int64_t row = r0; row < r1; ++row) {
       const int64_t e = row * width + c0;
       const Vec<T> xq = ldv(qp + e), xk = ldv(kp + e), gq = ldv(dq + e), gk = ldv(dk + e);
       Vec<T> oq, ok;
-      const int64_t pos = row % n + offset;
+      const int64_t tp = row % n;
+      const int64_t pos = tp + offset;
+      if (theta != nullptr) rw.at(pos, row == r0 || tp == 0 || ((row - r0) % kAnchor) == 0);
 #pragma unroll
       for (int pr = 0; pr < V / 2; ++pr) {
         const Tacc xq1 = (Tacc)Cvt<T>::to_f(xq.v[2 * pr]), xq2 = (Tacc)Cvt<T>::to_f(xq.v[2 * pr + 1]);
         const Tacc xk1 = (Tacc)Cvt<T>::to_f(xk.v[2 * pr]), xk2 = (Tacc)Cvt<T>::to_f(xk.v[2 * pr + 1]);
         Tacc gq1 = (Tacc)Cvt<T>::to_f(gq.v[2 * pr]), gq2 = (Tacc)Cvt<T>::to_f(gq.v[2 * pr + 1]);
         Tacc gk1 = (Tacc)Cvt<T>::to_f(gk.v[2 * pr]), gk2 = (Tacc)Cvt<T>::to_f(gk.v[2 * pr + 1]);
+        Tacc aq1, aq2, ak1, ak2, hq1, hq2, hk1, hk2;  // act and act' (one sigmoid each)
+        act_both<Tacc>(xq1, act, aq1, hq1);
+        act_both<Tacc>(xq2, act, aq2, hq2);
+        act_both<Tacc>(xk1, act, ak1, hk1);
+        act_both<Tacc>(xk2, act, ak2, hk2);
         if (theta != nullptr) {
-          Tacc c, s;
-          rot_cs<Tacc>(th[pr], pos, &c, &s);
+          const Tacc c = rw.c[pr], s = rw.s[pr];
           // rotated activations y (recomputed) for the angle gradient
-          const Tacc aq1 = act_fwd<Tacc>(xq1, act), aq2 = act_fwd<Tacc>(xq2, act);
-          const Tacc ak1 = act_fwd<Tacc>(xk1, act), ak2 = act_fwd<Tacc>(xk2, act);
           const Tacc yq1 = aq1 * c - aq2 * s, yq2 = aq1 * s + aq2 * c;
           const Tacc yk1 = ak1 * c - ak2 * s, yk2 = ak1 * s + ak2 * c;
           acc[pr] += (Tacc)pos * ((gq2 * yq1 - gq1 * yq2) + (gk2 * yk1 - gk1 * yk2));
@@ -165,10 +227,10 @@ __global__ void __launch_bounds__(256) prologue_bwd_kernel(const T* __restrict__
           const Tacc rk1 = gk1 * c + gk2 * s, rk2 = -gk1 * s + gk2 * c;
           gq1 = rq1, gq2 = rq2, gk1 = rk1, gk2 = rk2;
         }
-        oq.v[2 * pr] = Cvt<T>::from_f(gq1 * act_grad<Tacc>(xq1, act));
-        oq.v[2 * pr + 1] = Cvt<T>::from_f(gq2 * act_grad<Tacc>(xq2, act));
-        ok.v[2 * pr] = Cvt<T>::from_f(gk1 * act_grad<Tacc>(xk1, act));
-        ok.v[2 * pr + 1] = Cvt<T>::from_f(gk2 * act_grad<Tacc>(xk2, act));
+        oq.v[2 * pr] = Cvt<T>::from_f(gq1 * hq1);
+        oq.v[2 * pr + 1] = Cvt<T>::from_f(gq2 * hq2);
+        ok.v[2 * pr] = Cvt<T>::from_f(gk1 * hk1);
+        ok.v[2 * pr + 1] = Cvt<T>::from_f(gk2 * hk2);
       }
       stv(dqp + e, oq);
       stv(dkp + e, ok);
@@ -301,6 +363,63 @@ __global__ void __launch_bounds__(32 * kEpiWarps) epilogue_bwd_kernel(const T* _
   }
 }
 
+// the same with the row held in registers (width = NV x 32 lanes x V): one read of a, u, dgated
+template <typename T, typename Tacc, int NV>
+__global__ void __launch_bounds__(32 * kEpiWarps) epilogue_bwd_reg_kernel(const T* __restrict__ dgated,
+                                                                          const T* __restrict__ a,
+                                                                          const T* __restrict__ u,
+                                                                          const Tacc* __restrict__ rawnorm,
+                                                                          T* __restrict__ da, T* __restrict__ du,
+                                                                          int64_t rows, int width, double eps) {
+  constexpr int V = Vec<T>::N;
+  const int64_t row = (int64_t)blockIdx.x * kEpiWarps + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const int64_t off = row * width;
+  Vec<T> xs[NV], gs[NV], us[NV];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int c = (i * 32 + lane) * V;
+    xs[i] = ldv(a + off + c);
+    gs[i] = ldv(dgated + off + c);
+    if (u != nullptr) us[i] = ldv(u + off + c);
+  }
+  const Tacc raw = rawnorm[row];
+  const Tacc r = raw > (Tacc)eps ? raw : (Tacc)eps;
+  const Tacc scale = sqrt((Tacc)width) / r;
+  Tacc dot = 0;  // sum_c a_c * dan_c
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int c = (i * 32 + lane) * V;
+    if (u != nullptr) {
+      Vec<T> o;
+#pragma unroll
+      for (int e = 0; e < V; ++e) {
+        const Tacc xf = (Tacc)Cvt<T>::to_f(xs[i].v[e]), gf = (Tacc)Cvt<T>::to_f(gs[i].v[e]);
+        dot += xf * gf * (Tacc)Cvt<T>::to_f(us[i].v[e]);
+        o.v[e] = Cvt<T>::from_f(gf * xf * scale);  // du = dgated * an
+      }
+      stv(du + off + c, o);
+    } else {
+#pragma unroll
+      for (int e = 0; e < V; ++e) dot += (Tacc)Cvt<T>::to_f(xs[i].v[e]) * (Tacc)Cvt<T>::to_f(gs[i].v[e]);
+    }
+  }
+  dot = warp_sum(dot);
+  const Tacc proj = raw >= (Tacc)eps ? dot / (r * r) : (Tacc)0;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int c = (i * 32 + lane) * V;
+    Vec<T> o;
+#pragma unroll
+    for (int e = 0; e < V; ++e) {
+      const Tacc dan = (Tacc)Cvt<T>::to_f(gs[i].v[e]) * (u != nullptr ? (Tacc)Cvt<T>::to_f(us[i].v[e]) : (Tacc)1);
+      o.v[e] = Cvt<T>::from_f((dan - (Tacc)Cvt<T>::to_f(xs[i].v[e]) * proj) * scale);
+    }
+    stv(da + off + c, o);
+  }
+}
+
 // tensor-parallel GLA (parallel.py:138-178): gated = a * u (no norm) and the row's sum of squares
 // of this shard's attention output, written as the last column of an augmented [rows, out_w + 1]
 // buffer row (the all-reduce payload); the output projection fills columns [0, out_w)
@@ -354,10 +473,10 @@ __global__ void __launch_bounds__(256) rowscale_kernel(const Tacc* __restrict__ 
 template <typename T, typename Tacc>
 cudaError_t prologue_t(const GlaRows& g, const void* qp, const void* kp, const double* theta, void* q, void* k,
                        cudaStream_t st) {
-  const int64_t vecs = g.rows * (g.width / Vec<T>::N);
-  const int threads = 256;
-  const int64_t blocks = (vecs + threads - 1) / threads;
-  prologue_kernel<T, Tacc><<<(unsigned)blocks, threads, 0, st>>>(
+  const int vw = g.width / Vec<T>::N;
+  const int threads = vw >= 256 ? 256 : (vw + 31) / 32 * 32;
+  const dim3 grid((unsigned)((g.rows + kRowsFwd - 1) / kRowsFwd), (unsigned)((vw + threads - 1) / threads));
+  prologue_kernel<T, Tacc><<<grid, threads, 0, st>>>(
       static_cast<const T*>(qp), static_cast<const T*>(kp), theta, static_cast<T*>(q), static_cast<T*>(k), g.rows,
       g.n, g.width, g.d, g.offset, g.act);
   return cudaGetLastError();
@@ -391,9 +510,20 @@ cudaError_t epilogue_t(const GlaRows& g, const void* a, const void* u, void* gat
 template <typename T, typename Tacc>
 cudaError_t epilogue_bwd_t(const GlaRows& g, const void* dgated, const void* a, const void* u, const void* rawnorm,
                            void* da, void* du, double eps, cudaStream_t st) {
-  epilogue_bwd_kernel<T, Tacc><<<(unsigned)((g.rows + kEpiWarps - 1) / kEpiWarps), 32 * kEpiWarps, 0, st>>>(
-      static_cast<const T*>(dgated), static_cast<const T*>(a), static_cast<const T*>(u),
-      static_cast<const Tacc*>(rawnorm), static_cast<T*>(da), static_cast<T*>(du), g.rows, g.width, eps);
+  const unsigned blocks = (unsigned)((g.rows + kEpiWarps - 1) / kEpiWarps);
+  const int per = 32 * Vec<T>::N;
+  const int nv = g.width % per == 0 ? g.width / per : 0;
+#define LA_EPI_BWD_ARGS                                                                                      \
+  static_cast<const T*>(dgated), static_cast<const T*>(a), static_cast<const T*>(u),                        \
+      static_cast<const Tacc*>(rawnorm), static_cast<T*>(da), static_cast<T*>(du), g.rows, g.width, eps
+  switch (nv) {
+    case 1: epilogue_bwd_reg_kernel<T, Tacc, 1><<<blocks, 32 * kEpiWarps, 0, st>>>(LA_EPI_BWD_ARGS); break;
+    case 2: epilogue_bwd_reg_kernel<T, Tacc, 2><<<blocks, 32 * kEpiWarps, 0, st>>>(LA_EPI_BWD_ARGS); break;
+    case 4: epilogue_bwd_reg_kernel<T, Tacc, 4><<<blocks, 32 * kEpiWarps, 0, st>>>(LA_EPI_BWD_ARGS); break;
+    case 8: epilogue_bwd_reg_kernel<T, Tacc, 8><<<blocks, 32 * kEpiWarps, 0, st>>>(LA_EPI_BWD_ARGS); break;
+    default: epilogue_bwd_kernel<T, Tacc><<<blocks, 32 * kEpiWarps, 0, st>>>(LA_EPI_BWD_ARGS);
+  }
+#undef LA_EPI_BWD_ARGS
   return cudaGetLastError();
 }
 

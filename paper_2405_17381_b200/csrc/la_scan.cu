@@ -11,58 +11,75 @@ namespace {
 //   rev: in[last] = user (or 0); walking g, j downwards: same
 // seg_in[g] = s on entering segment g.  `final_out` (nullable; needs every segment summarised) receives
 // the inclusive total (F(n) / R(0)).
-constexpr int kScanThreads = 256;
-constexpr int kScanElems = 8;  // state elements per thread (consecutive)
+constexpr int kScanThreads = 128;
+constexpr int kBatch = 8;  // sub-segment loads in flight per thread
 
-template <typename Tacc>
+template <typename Tacc, int V> struct alignas(16) VecA {
+  Tacc x[V];
+};
+
+// One thread owns V consecutive state elements (one 16-byte vector): many small blocks, every load of a
+// batch of sub-segments issued before the first is folded in (the scan is latency-bound, ~nsub loads deep).
+template <typename Tacc, int V>
 __global__ void __launch_bounds__(kScanThreads) segment_scan_kernel(
     const Tacc* __restrict__ delta, Tacc* __restrict__ seg_in, const void* user_in, int user_T,
     Tacc* final_out, int final_T, const double* lam, int heads, int d, int n, int seg_len, int nseg,
     int sub_len, int sub_per_seg, int g_lo, int g_hi, int rev) {
-  extern __shared__ unsigned char scan_smem[];
-  Tacc* s_dec = reinterpret_cast<Tacc*>(scan_smem);  // lam^len of every sub-segment, once per block
+  using Vec = VecA<Tacc, V>;
+  // lam^len of a sub-segment: len is sub_len, a segment's short last sub-segment, or the sequence's
+  // short last one -- three pow()s per block instead of one per sub-segment
+  __shared__ Tacc s_pow[3];
+  __shared__ int s_len[3];
   const int bh = blockIdx.y;
   const int nsub = nseg * sub_per_seg;
-  {
-    const double l = lam[bh % heads];
-    for (int kk = threadIdx.x; kk < nsub; kk += blockDim.x) {
-      const int g = kk / sub_per_seg, j = kk % sub_per_seg;
-      const int p0 = g * seg_len + j * sub_len;
-      const int p1 = min(min(n, (g + 1) * seg_len), p0 + sub_len);
-      s_dec[kk] = p1 > p0 ? (Tacc)pow(l, (double)(p1 - p0)) : (Tacc)1;
+  auto sub_range = [&](int kk, int& p0, int& p1) {
+    const int g = kk / sub_per_seg, j = kk % sub_per_seg;
+    p0 = g * seg_len + j * sub_len;
+    p1 = min(min(n, (g + 1) * seg_len), p0 + sub_len);
+  };
+  if (threadIdx.x < 3) {
+    const int last_in_seg = (seg_len - 1) / sub_len;  // index of a full segment's last sub-segment
+    int len = sub_len;
+    if (threadIdx.x == 1) len = seg_len - last_in_seg * sub_len;
+    if (threadIdx.x == 2) {
+      int p0, p1;
+      const int gl = (n - 1) / seg_len;
+      sub_range(gl * sub_per_seg + ((n - 1 - gl * seg_len) / sub_len), p0, p1);
+      len = p1 - p0;
     }
-    __syncthreads();
+    s_len[threadIdx.x] = len;
+    s_pow[threadIdx.x] = (Tacc)pow(lam[bh % heads], (double)len);
   }
-  // a thread owns kScanElems consecutive state elements: few, fat blocks (the scan is latency-bound)
-  const int e0 = (blockIdx.x * kScanThreads + threadIdx.x) * kScanElems;
+  __syncthreads();
   const int dd = d * d;
+  const int e0 = (blockIdx.x * kScanThreads + threadIdx.x) * V;
   if (e0 >= dd) return;
-  const int ne = min(kScanElems, dd - e0);
-  Tacc s[kScanElems];
+  Tacc s[V];
 #pragma unroll
-  for (int q = 0; q < kScanElems; ++q) {
+  for (int q = 0; q < V; ++q) {
     s[q] = 0;
-    const int e = e0 + q;
-    if (user_in != nullptr && q < ne) {
+    if (user_in != nullptr) {
       const Tacc* u = reinterpret_cast<const Tacc*>(user_in) + (int64_t)bh * dd;
+      const int e = e0 + q;
       s[q] = user_T ? u[(e % d) * d + e / d] : u[e];
     }
   }
   const Tacc* dcol = delta + (int64_t)bh * nsub * dd + e0;
   Tacc* scol = seg_in != nullptr ? seg_in + (int64_t)bh * nseg * dd + e0 : nullptr;
-  // Walk the sub-segments in scan order (k -> segment g, sub-segment j); their loads are independent:
-  // issue a batch, then fold it in order.
-  constexpr int kBatch = 4;
   for (int k0 = 0; k0 < nsub; k0 += kBatch) {
-    Tacc x[kBatch][kScanElems];
+    Vec x[kBatch];
 #pragma unroll
     for (int u = 0; u < kBatch; ++u) {
       const int k = k0 + u;
       const int kk = rev ? nsub - 1 - k : k;
-      const int g = kk / sub_per_seg, j = kk % sub_per_seg;
-      const bool live = k < nsub && g >= g_lo && g <= g_hi && g * seg_len + j * sub_len < min(n, (g + 1) * seg_len);
+      const int g = kk / sub_per_seg;
+      int p0, p1;
+      sub_range(kk, p0, p1);
+      if (k < nsub && g >= g_lo && g <= g_hi && p1 > p0)
+        x[u] = *reinterpret_cast<const Vec*>(dcol + (int64_t)kk * dd);
+      else
 #pragma unroll
-      for (int q = 0; q < kScanElems; ++q) x[u][q] = (live && q < ne) ? dcol[(int64_t)kk * dd + q] : (Tacc)0;
+        for (int q = 0; q < V; ++q) x[u].x[q] = 0;
     }
 #pragma unroll
     for (int u = 0; u < kBatch; ++u) {
@@ -72,23 +89,25 @@ __global__ void __launch_bounds__(kScanThreads) segment_scan_kernel(
       const int g = kk / sub_per_seg, j = kk % sub_per_seg;
       // entering segment g: its first sub-segment in scan order
       if (scol != nullptr && j == (rev ? sub_per_seg - 1 : 0)) {
+        Vec o;
 #pragma unroll
-        for (int q = 0; q < kScanElems; ++q)
-          if (q < ne) scol[(int64_t)g * dd + q] = s[q];
+        for (int q = 0; q < V; ++q) o.x[q] = s[q];
+        *reinterpret_cast<Vec*>(scol + (int64_t)g * dd) = o;
       }
-      if (g < g_lo || g > g_hi) continue;
-      const int p0 = g * seg_len + j * sub_len;
-      if (p0 >= min(min(n, (g + 1) * seg_len), p0 + sub_len)) continue;  // past the end: never written
-      const Tacc dec = s_dec[kk];
+      int p0, p1;
+      sub_range(kk, p0, p1);
+      if (g < g_lo || g > g_hi || p1 <= p0) continue;  // not summarised / past the end
+      const int len = p1 - p0;
+      const Tacc dec = len == s_len[0] ? s_pow[0] : len == s_len[1] ? s_pow[1] : s_pow[2];
 #pragma unroll
-      for (int q = 0; q < kScanElems; ++q) s[q] = dec * s[q] + x[u][q];
+      for (int q = 0; q < V; ++q) s[q] = dec * s[q] + x[u].x[q];
     }
   }
   if (final_out != nullptr) {
 #pragma unroll
-    for (int q = 0; q < kScanElems; ++q) {
+    for (int q = 0; q < V; ++q) {
       const int e = e0 + q;
-      if (q < ne) final_out[(int64_t)bh * dd + (final_T ? (e % d) * d + e / d : e)] = s[q];
+      final_out[(int64_t)bh * dd + (final_T ? (e % d) * d + e / d : e)] = s[q];
     }
   }
 }
@@ -98,18 +117,23 @@ __global__ void __launch_bounds__(kScanThreads) segment_scan_kernel(
 cudaError_t launch_segment_scan(bool acc_double, const void* delta, void* seg_in, const void* user_in, int user_T,
                                 void* final_out, int final_T, const double* lam, int bh, int heads, int d,
                                 const PassDesc& p, cudaStream_t st) {
-  dim3 grid((unsigned)((d * d + kScanThreads * kScanElems - 1) / (kScanThreads * kScanElems)), bh);
-  const size_t smem = (size_t)p.nseg * p.sub_per_seg * (acc_double ? sizeof(double) : sizeof(float));
-  if (acc_double)
-    segment_scan_kernel<double><<<grid, kScanThreads, smem, st>>>(
-        reinterpret_cast<const double*>(delta), reinterpret_cast<double*>(seg_in), user_in, user_T,
-        reinterpret_cast<double*>(final_out), final_T, lam, heads, d, p.n, p.seg_len, p.nseg, p.sub_len,
-        p.sub_per_seg, p.g_lo, p.g_hi, p.rev);
-  else
-    segment_scan_kernel<float><<<grid, kScanThreads, smem, st>>>(
-        reinterpret_cast<const float*>(delta), reinterpret_cast<float*>(seg_in), user_in, user_T,
-        reinterpret_cast<float*>(final_out), final_T, lam, heads, d, p.n, p.seg_len, p.nseg, p.sub_len,
-        p.sub_per_seg, p.g_lo, p.g_hi, p.rev);
+  const int dd = d * d;
+  auto grid = [&](int v) { return dim3((unsigned)((dd / v + kScanThreads - 1) / kScanThreads), bh); };
+#define LA_SCAN_ARGS(T)                                                                                          \
+  reinterpret_cast<const T*>(delta), reinterpret_cast<T*>(seg_in), user_in, user_T, reinterpret_cast<T*>(final_out), \
+      final_T, lam, heads, d, p.n, p.seg_len, p.nseg, p.sub_len, p.sub_per_seg, p.g_lo, p.g_hi, p.rev
+  if (acc_double) {
+    if (dd % 2 == 0)
+      segment_scan_kernel<double, 2><<<grid(2), kScanThreads, 0, st>>>(LA_SCAN_ARGS(double));
+    else
+      segment_scan_kernel<double, 1><<<grid(1), kScanThreads, 0, st>>>(LA_SCAN_ARGS(double));
+  } else {
+    if (dd % 4 == 0)
+      segment_scan_kernel<float, 4><<<grid(4), kScanThreads, 0, st>>>(LA_SCAN_ARGS(float));
+    else
+      segment_scan_kernel<float, 1><<<grid(1), kScanThreads, 0, st>>>(LA_SCAN_ARGS(float));
+  }
+#undef LA_SCAN_ARGS
   return cudaGetLastError();
 }
 

@@ -33,8 +33,8 @@ namespace {
 
 using namespace ptx;
 
-#ifndef LA_PF
-#define LA_PF 0  // L2 prefetch distance in chunks (0: off)
+#ifndef LA_PFKV
+#define LA_PFKV 0  // 1: L2 prefetch of the next K and V tiles
 #endif
 
 #ifdef LA_TRACE
@@ -200,6 +200,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           uint8_t* g = slot_gen(r == 0 ? SLOT_Q + s : r == 1 ? SLOT_D + s : r == 2 ? SLOT_K : SLOT_V);
           tma_load_4d(maps[r], full, g, 0, r0, hi, bi);
           tma_load_4d(maps[r], full, g + HALF, 64, r0, hi, bi);
+#if LA_PFKV
+          // K and V are single-slotted: their next tile can only be loaded once this chunk has consumed
+          // the slot, so warm L2 with it now and the later load sees L2 latency, not DRAM latency
+          if (r >= 2 && t + 1 < nchunks) {
+            tma_prefetch_l2_4d(maps[r], 0, chunk_row0(t + 1), hi, bi);
+            tma_prefetch_l2_4d(maps[r], 64, chunk_row0(t + 1), hi, bi);
+          }
+#endif
           next[r] = t + 1;
         }
         if ((spins & 0xFFFFF) == 0) {  // watchdog, as mbar_wait
@@ -236,8 +244,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const uint32_t k_addr = slot(SLOT_K), v_addr = slot(SLOT_V);
         // Sv = K Q^T (SV's previous P/K~ consumed by dV(t-1))
         mbar_wait(&bars.full_q[s], (t >> 1) & 1);
+        LB_TR(t, 24);
         mbar_wait(&bars.full_k, t & 1);
+        LB_TR(t, 22);
         if (t >= 1) mbar_wait(&bars.ov_full, (t - 1) & 1);
+        LB_TR(t, 23);
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {

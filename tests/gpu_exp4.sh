@@ -1,0 +1,5 @@
+# same-box A/B of build/var variants against the in-tree library (tools/exp_time.py), then a trace
+for rep in 1 2; do
+for lib in paper_2405_17381_b200/libla_b200.so $(ls build/var/lib*.so | grep -v tr); do echo "$lib $(LA_B200_LIB=$lib timeout 120 python tools/exp_time.py 2>&1 | tail -1)"; done
+done
+LA_B200_LIB=build/var/libtrpf.so timeout 200 python tests/tc_trace_bwd.py 8x8192 > gpurun_out/trace_bwd_pf.log 2>&1

@@ -6,7 +6,7 @@ from paper_2405_17381_b200 import ops, _lib
 lib = _lib.load()
 dev = torch.device('cuda', 0)
 names = ["tmaQ", "tmaD", "tmaK", "tmaV", "Sv", "Sk", "st_iss", "dV_iss", "dV_com", "dK_iss", "dK_com", "PvS", "PvE",
-         "PkS", "PkE", "W_rdy", "epiV", "epiK", "ST_ds", "ST_pub", "stV", "stRd"]
+         "PkS", "PkE", "W_rdy", "epiV", "epiK", "ST_ds", "ST_pub", "stV", "stRd", "Kfull", "ovf", "Qfull"]
 shapes = [tuple(map(int, a.split('x'))) for a in sys.argv[1:]] or [(8, 8192)]
 for (b, n) in shapes:
     q, k, v, do = (torch.randn(b, 16, n, 128, device=dev, dtype=torch.bfloat16) * 128 ** -0.5 for _ in range(4))
