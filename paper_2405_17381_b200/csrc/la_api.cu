@@ -215,7 +215,10 @@ cudaError_t side_stream(SideStream** out) {
   if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
   SideStream& r = res[dev];
   if (r.stream == nullptr) {
-    if ((err = cudaStreamCreateWithFlags(&r.stream, cudaStreamNonBlocking)) != cudaSuccess) return err;
+    // high priority: the side stream carries the backward's critical chain (summaries, scan, dK/dV sweep)
+    int least = 0, greatest = 0;
+    if ((err = cudaDeviceGetStreamPriorityRange(&least, &greatest)) != cudaSuccess) return err;
+    if ((err = cudaStreamCreateWithPriority(&r.stream, cudaStreamNonBlocking, greatest)) != cudaSuccess) return err;
     if ((err = cudaEventCreateWithFlags(&r.fork, cudaEventDisableTiming)) != cudaSuccess) return err;
     if ((err = cudaEventCreateWithFlags(&r.join, cudaEventDisableTiming)) != cudaSuccess) return err;
   }
@@ -238,6 +241,36 @@ int prepare(const la_desc* desc, size_t ws_bytes, const void* ws, Prepared* out)
   out->need = ws_bytes_for(desc, out->backend, out->plan);
   if (out->need > 0 && (ws == nullptr || ws_bytes < out->need))
     return fail(LA_ERR_SHAPE, "workspace too small: need %zu bytes, got %zu", out->need, ws_bytes);
+  return LA_OK;
+}
+
+// The fused dK/dV sweep (la_tc_bwd.cu): q, k, v, do read once, one state update.  seg_in: the
+// adjoint state entering every segment (split sequences), else the caller's dkv_in.
+int dkdv(const la_desc* desc, const la::PassDesc& base, const void* q, const void* k, const void* v,
+         const void* dout, void* dq, void* dk, void* dv, const void* dkv_in, void* dkv_out, const void* seg_in,
+         cudaStream_t st) {
+  (void)desc;
+  la::PassDesc p = base;
+  p.rev = 1;
+  p.b = q;
+  p.c = dout;
+  p.a = k;
+  p.out = dv;
+  p.state_out = dkv_out;
+  const int64_t dd = (int64_t)p.d * p.d;
+  if (seg_in != nullptr) {
+    p.state_in = seg_in;
+    p.state_in_bh_stride = (int64_t)p.nseg * dd;
+    p.state_in_seg_stride = dd;
+  } else {
+    p.state_in = dkv_in;
+    p.state_in_bh_stride = dd;
+    p.state_in_seg_stride = 0;
+  }
+  if (!la::tc_pointers_ok(p) || (reinterpret_cast<uintptr_t>(v) & 15) || (reinterpret_cast<uintptr_t>(dk) & 15))
+    return cuda_fail(cudaErrorMisalignedAddress, "la_bwd dkdv");
+  cudaError_t err = la::tc_dkdv_launch(p, q, k, v, dout, dq, dk, dv, st);
+  if (err != cudaSuccess) return cuda_fail(err, "la_bwd dkdv");
   return LA_OK;
 }
 
@@ -318,6 +351,30 @@ int la_bwd(const la_desc* desc, const void* q, const void* k, const void* v, con
   pd.c = dout;
   pd.rev = 1;
   pd.state_in = dkv_in;
+#ifndef LA_BWD_CONCURRENT
+#define LA_BWD_CONCURRENT 1
+#endif
+  if (LA_BWD_CONCURRENT && pr.backend == LA_BACKEND_TCGEN05 && (!split || fwd_seg_states != nullptr)) {
+    // The dq pass and the fused dK/dV sweep are independent: the sweep's chain (adjoint summaries and
+    // scan when the sequence is split, then the sweep) runs on the high-priority side stream, the dq
+    // pass beside it on the caller's stream.  Together they keep all 148 SMs streaming (each alone
+    // fills 128 of them at n = 8K) and overlap each other's ramp and tail.
+    SideStream* side = nullptr;
+    if ((err = side_stream(&side)) != cudaSuccess) return cuda_fail(err, "la_bwd side stream");
+    if ((err = cudaEventRecord(side->fork, st)) != cudaSuccess ||
+        (err = cudaStreamWaitEvent(side->stream, side->fork, 0)) != cudaSuccess)
+      return cuda_fail(err, "la_bwd fork");
+    if (split && (err = segment_states(pr.backend, desc->dtype, pd, delta, seg_in, side->stream)) != cudaSuccess)
+      return cuda_fail(err, "la_bwd dkv states");
+    if ((rc = dkdv(desc, base, q, k, v, dout, dq, dk, dv, dkv_in, dkv_out, split ? seg_in : nullptr, side->stream)) !=
+        LA_OK)
+      return rc;
+    if ((err = cudaEventRecord(side->join, side->stream)) != cudaSuccess) return cuda_fail(err, "la_bwd join");
+    if ((err = main_pass(pr.backend, desc->dtype, p, fwd_seg_states, 1, st)) != cudaSuccess)
+      return cuda_fail(err, "la_bwd dq");
+    if ((err = cudaStreamWaitEvent(st, side->join, 0)) != cudaSuccess) return cuda_fail(err, "la_bwd join");
+    return LA_OK;
+  }
   if (split && fwd_seg_states != nullptr) {
     // the dq pass needs only the forward's segment states, so the adjoint summaries (the workspace's
     // only user) run on a side stream beside it: each alone leaves SMs idle
@@ -339,31 +396,8 @@ int la_bwd(const la_desc* desc, const void* q, const void* k, const void* v, con
     if (split && (err = segment_states(pr.backend, desc->dtype, pd, delta, seg_in, st)) != cudaSuccess)
       return cuda_fail(err, "la_bwd dkv states");
   }
-  if (pr.backend == LA_BACKEND_TCGEN05) {
-    // one fused sweep for dk and dv (la_tc_bwd.cu): q, k, v, do read once, one state update
-    p = base;
-    p.rev = 1;
-    p.b = q;
-    p.c = dout;
-    p.a = k;
-    p.out = dv;
-    p.state_out = dkv_out;
-    const int64_t dd = (int64_t)p.d * p.d;
-    if (split) {
-      p.state_in = seg_in;
-      p.state_in_bh_stride = (int64_t)p.nseg * dd;
-      p.state_in_seg_stride = dd;
-    } else {
-      p.state_in = dkv_in;
-      p.state_in_bh_stride = dd;
-      p.state_in_seg_stride = 0;
-    }
-    if (!la::tc_pointers_ok(p) || (reinterpret_cast<uintptr_t>(v) & 15) || (reinterpret_cast<uintptr_t>(dk) & 15))
-      return cuda_fail(cudaErrorMisalignedAddress, "la_bwd dkdv");
-    if ((err = la::tc_dkdv_launch(p, q, k, v, dout, dq, dk, dv, st)) != cudaSuccess)
-      return cuda_fail(err, "la_bwd dkdv");
-    return LA_OK;
-  }
+  if (pr.backend == LA_BACKEND_TCGEN05) return dkdv(desc, base, q, k, v, dout, dq, dk, dv, dkv_in, dkv_out,
+                                                     split ? seg_in : nullptr, st);
   p = base;
   p.a = v;
   p.b = dout;
