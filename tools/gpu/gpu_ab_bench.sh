@@ -1,4 +1,4 @@
-# same-box A/B of the bench sweep: bash tests/gpu_ab_bench.sh <reps> <lib> [<lib> ...]
+# same-box A/B of the bench sweep: bash tools/gpu/gpu_ab_bench.sh <reps> <lib> [<lib> ...]
 reps=$1; shift
 for rep in $(seq $reps); do
 for lib in "$@"; do

@@ -1,4 +1,4 @@
-"""Relative view of tests/tc_trace.py output: per chunk, event times minus that chunk's S issue."""
+"""Relative view of tools/gpu/tc_trace.py output: per chunk, event times minus that chunk's S issue."""
 import sys
 txt = open(sys.argv[1] if len(sys.argv) > 1 else 'gpurun_out/trace.log').read()
 names = ["tmaA", "S_iss", "pfull", "Ocom", "bsc", "dScom", "Psf", "Pdone", "Oof", "Ofree", "-", "KVsf", "KVsc", "KVds",
