@@ -40,6 +40,9 @@ using namespace ptx;
 //   2: W lives in V's slot; K by the P warps once K~ is in TMEM, V by the commit after W's product
 #define LA_BWD_REL 0
 #endif
+#ifndef LA_POLL_SLEEP_NS
+#define LA_POLL_SLEEP_NS 0  // producer back-off when no ring had a free slot (experiment)
+#endif
 #ifndef LA_PFKV
 #define LA_PFKV 1  // L2 prefetch of the next K and V tiles (+1.2% on the bench sweep, same-box A/B)
 #endif
@@ -191,6 +194,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       long long t0 = 0;
       for (uint32_t spins = 1; next[0] < nchunks || next[1] < nchunks || next[2] < nchunks || next[3] < nchunks;
            ++spins) {
+#if LA_POLL_SLEEP_NS > 0
+        const int issued0 = next[0] + next[1] + next[2] + next[3];
+#endif
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
           const int t = next[r];
@@ -217,6 +223,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #endif
           next[r] = t + 1;
         }
+#if LA_POLL_SLEEP_NS > 0
+        if (next[0] + next[1] + next[2] + next[3] == issued0) __nanosleep(LA_POLL_SLEEP_NS);  // nothing free yet
+#endif
         if ((spins & 0xFFFFF) == 0) {  // watchdog, as mbar_wait
           if (t0 == 0) t0 = clock64();
           else if (clock64() - t0 > 40000000000LL) __trap();

@@ -189,6 +189,29 @@ def test_state_chaining_matches_whole_sequence(dtype):
     assert orc.max_rel_error(host(dd2), host(g2[3])) <= tol
 
 
+@pytest.mark.parametrize("segments", [0, 1, 3])
+def test_backward_with_edge_states_and_saved_segment_states(segments):
+    """The backward's concurrent schedule (dq pass beside the dK/dV chain) with kv_in, dkv_in, dkv_out and
+    the forward's segment states: the same gradients and dkv_out as the sequential recomputation."""
+    b, h, n, d = 2, 3, 1500, 128
+    lams = [1.0, 0.97, 0.6]
+    q, k, v, do = (dev(a, torch.bfloat16) for a in _batched(b, h, n, d, seed=9))
+    kv_in = torch.randn(b, h, d, d, device="cuda") * 0.05
+    dkv_in = torch.randn(b, h, d, d, device="cuda") * 0.05
+    o, seg = ops.la_forward(q, k, v, lams, kv_in=kv_in, segments=segments, want_seg_states=True)
+    want = ops.la_backward(q, k, v, do, lams, kv_in=kv_in, dkv_in=dkv_in, segments=segments, want_state=True)
+    got = ops.la_backward(q, k, v, do, lams, kv_in=kv_in, dkv_in=dkv_in, segments=segments, want_state=True,
+                          fwd_seg_states=seg)
+    for a, w in zip(got[:3], want[:3]):
+        assert orc.max_rel_error(host(a), host(w)) <= 1e-2
+    assert orc.max_rel_error(host(got[3]), host(want[3])) <= 1e-5
+    # and against the oracle run on the same bf16 inputs with the same edge states
+    qq, kk, vv, dd = (host(t) for t in (q, k, v, do))
+    (rdq, rdk, rdv), rdkv = orc.batched_backward(qq, kk, vv, dd, lams, kv_in=host(kv_in), dkv_in=host(dkv_in))
+    for a, r in zip(got[:3], (rdq, rdk, rdv)):
+        assert orc.max_rel_error(host(a), r) <= TOL[torch.bfloat16]
+
+
 def test_autograd_function_matches_ops():
     b, h, n, d = 2, 2, 333, 128
     lams = [0.9, 0.99]
