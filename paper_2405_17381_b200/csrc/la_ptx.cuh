@@ -61,6 +61,16 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
 #endif
   return ok != 0;
 }
+// x^k for k >= 0 by binary exponentiation (<= 2 log2 k + 1 roundings)
+__device__ __forceinline__ double pow_int(double x, int k) {
+  double r = 1.0;
+  while (k > 0) {
+    if (k & 1) r *= x;
+    x *= x;
+    k >>= 1;
+  }
+  return r;
+}
 // Non-blocking probe: has the phase with this parity completed?
 __device__ __forceinline__ bool mbar_test(uint32_t addr, uint32_t parity) {
   uint32_t ok;

@@ -170,13 +170,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     mbar_init(&bars.x_done, 1);
     mbar_init(&bars.st_ready, NUM_KV);
     fence_mbar_init();
-    double x = 1.0;
-    const double lam = args.lam[hi];
-    for (int k = 0; k <= C; ++k) {
-      pw[k] = (float)x;
-      x *= lam;
-    }
   }
+  // lam^0 .. lam^C, one power per thread (binary exponentiation in fp64): a serial ladder here held
+  // every warp (and the first TMA loads) back by ~130 dependent multiplies
+  if (threadIdx.x <= C) pw[threadIdx.x] = (float)pow_int(args.lam[hi], (int)threadIdx.x);
   if (warp == WARP_TMA && lane == 0) {
     tma_prefetch(&map_a);
     tma_prefetch(&map_b);
