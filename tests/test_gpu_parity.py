@@ -212,6 +212,25 @@ def test_backward_with_edge_states_and_saved_segment_states(segments):
         assert orc.max_rel_error(host(a), r) <= TOL[torch.bfloat16]
 
 
+def test_persistent_units_with_edge_states():
+    """More (batch, head) units than one wave and an unsplit sequence: each CTA walks several units
+    of one head (la_tc.cu), exporting every unit's kv_out and loading every unit's kv_in; ragged n."""
+    b, h, n, d = 37, 5, 300, 128  # bh = 185 > 148: 95 CTAs, 1-2 units each
+    lams = [1.0, 0.99, 0.9, 0.7, 0.5]
+    q, k, v, do = (dev(a, torch.bfloat16) for a in _batched(b, h, n, d, seed=21))
+    kv_in = torch.randn(b, h, d, d, device="cuda") * 0.05
+    dkv_in = torch.randn(b, h, d, d, device="cuda") * 0.05
+    assert ops.segment_count(ops._desc(ops._geometry(q, "bhnd"), q.dtype, None, "auto", 0)) == 1
+    o, kv_out = ops.la_forward(q, k, v, lams, kv_in=kv_in, want_state=True)
+    dq, dk, dv, dkv_out = ops.la_backward(q, k, v, do, lams, kv_in=kv_in, dkv_in=dkv_in, want_state=True)
+    qq, kk, vv, dd = (host(t) for t in (q, k, v, do))
+    ro, rkv = orc.batched_forward(qq, kk, vv, lams, kv_in=host(kv_in))
+    (rdq, rdk, rdv), rdkv = orc.batched_backward(qq, kk, vv, dd, lams, kv_in=host(kv_in), dkv_in=host(dkv_in))
+    tol = TOL[torch.bfloat16]
+    for got, ref in ((o, ro), (kv_out, rkv), (dq, rdq), (dk, rdk), (dv, rdv), (dkv_out, rdkv)):
+        assert orc.max_rel_error(host(got), ref) <= tol
+
+
 def test_autograd_function_matches_ops():
     b, h, n, d = 2, 2, 333, 128
     lams = [0.9, 0.99]

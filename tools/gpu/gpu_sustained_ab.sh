@@ -1,5 +1,7 @@
-# sustained-load A/B (power cap regime): 40 steps each, alternating
-for rep in 1 2; do for v in base sleep; do
-lib=paper_2405_17381_b200/libla_b200.so; [ $v = sleep ] && lib=build/var/libsleep.so
-LA_B200_LIB=$lib timeout 300 python tools/step_probe.py 40 > gpurun_out/sp_${v}_$rep.log 2>&1
+# sustained-load A/B (power-cap regime): tools/step_probe.py 40 steps per arm, alternating, 2 reps.
+# Arms are "name:env" pairs, e.g.  bash tools/gpu/gpu_sustained_ab.sh base:LA_PERSISTENT=1 nopers:LA_PERSISTENT=0
+# (LA_B200_LIB=<lib> as the env selects a library variant).  Logs: gpurun_out/sp_<name>_<rep>.log
+for rep in 1 2; do for arm in "$@"; do
+  name=${arm%%:*}; envs=${arm#*:}
+  env $envs timeout 300 python tools/step_probe.py 40 > gpurun_out/sp_${name}_$rep.log 2>&1
 done; done
