@@ -184,6 +184,9 @@ def run_ours(args) -> None:
                                                                  / (pk["bf16_tflops"] * 1e12), 2),
             "pct_hbm_roofline": round(100 * tok_s * H * BYTES_PER_HEAD_TOKEN / (pk["hbm_gbs"] * 1e9), 2),
         }
+    # per-step device time (first n's fwd start -> last n's bwd end): shows the clock drift inside the
+    # timed region once the board reaches its power cap (sw_power_cap)
+    step_ms = [round(ev[seq_lens[0]][s][0].elapsed_time(ev[seq_lens[-1]][s][2]), 3) for s in range(args.steps)]
     step_tokens = sum(tokens.values()) * world
     value = step_tokens * args.steps / (total_ms / 1e3)
 
@@ -214,6 +217,7 @@ def run_ours(args) -> None:
                    "l2": "inputs larger than L2 (268 MB per tensor per n)"},
         "pct_bf16_peak": round(100 * value / world * H * FLOPS_PER_HEAD_TOKEN / (pk["bf16_tflops"] * 1e12), 2),
         "flatness_128k_over_1k": round(flat, 3),
+        "step_ms": step_ms,
         "sweep": sweep,
         "roofline": roof,
         "gpu_launches": launches,
