@@ -32,6 +32,10 @@ _LAZY = {
     "lightning_backward": ("kernels", "lightning_backward"),
     "lightning_forward_decay": ("kernels", "lightning_forward_decay"),
     "lightning_backward_decay": ("kernels", "lightning_backward_decay"),
+    "BenchGrid": ("records", "BenchGrid"),
+    "run_bench": ("records", "run_bench"),
+    "write_csv": ("records", "write_csv"),
+    "read_csv": ("records", "read_csv"),
 }
 
 
