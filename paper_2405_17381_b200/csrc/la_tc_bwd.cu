@@ -33,16 +33,6 @@ namespace {
 
 using namespace ptx;
 
-#ifndef LA_BWD_REL
-// who hands K's and V's single slots back to the TMA producer (experiment):
-//   0: the MMA issuer's commits after W's state product (K) and after dK's inter product (V)
-//   1: as 0 for K; V by the P warps once V~ is in TMEM (Sk has completed by then)
-//   2: W lives in V's slot; K by the P warps once K~ is in TMEM, V by the commit after W's product
-#define LA_BWD_REL 0
-#endif
-#ifndef LA_POLL_SLEEP_NS
-#define LA_POLL_SLEEP_NS 0  // producer back-off when no ring had a free slot (experiment)
-#endif
 #ifndef LA_PFKV
 #define LA_PFKV 1  // L2 prefetch of the next K and V tiles (+1.2% on the bench sweep, same-box A/B)
 #endif
@@ -136,9 +126,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       mbar_init(&bars.empty_d[s], 1);
     }
     mbar_init(&bars.full_k, 1);
-    mbar_init(&bars.empty_k, LA_BWD_REL == 2 ? NUM_P : 1);
+    mbar_init(&bars.empty_k, 1);
     mbar_init(&bars.full_v, 1);
-    mbar_init(&bars.empty_v, LA_BWD_REL == 1 ? NUM_P : 1);
+    mbar_init(&bars.empty_v, 1);
     mbar_init(&bars.sv_full, 1);
     mbar_init(&bars.sk_full, 1);
     mbar_init(&bars.av_full, NUM_P);
@@ -191,9 +181,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       long long t0 = 0;
       for (uint32_t spins = 1; next[0] < nchunks || next[1] < nchunks || next[2] < nchunks || next[3] < nchunks;
            ++spins) {
-#if LA_POLL_SLEEP_NS > 0
-        const int issued0 = next[0] + next[1] + next[2] + next[3];
-#endif
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
           const int t = next[r];
@@ -220,9 +207,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #endif
           next[r] = t + 1;
         }
-#if LA_POLL_SLEEP_NS > 0
-        if (next[0] + next[1] + next[2] + next[3] == issued0) __nanosleep(LA_POLL_SLEEP_NS);  // nothing free yet
-#endif
         if ((spins & 0xFFFFF) == 0) {  // watchdog, as mbar_wait
           if (t0 == 0) t0 = clock64();
           else if (clock64() - t0 > 40000000000LL) __trap();
@@ -292,9 +276,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
         for (int kk = 0; kk < C / 16; ++kk)
           mma_bf16_ss(tmem + TM_ST, smem_desc_sw128(q_addr + kk * 2048, HALF, 1024),
-                      smem_desc_sw128((LA_BWD_REL == 2 ? v_addr : k_addr) + kk * 2048, HALF, 1024), IDESC_MNMN, 1);
+                      smem_desc_sw128(k_addr + kk * 2048, HALF, 1024), IDESC_MNMN, 1);
         mma_commit(&bars.ds_full);
-        mma_commit(LA_BWD_REL == 2 ? &bars.empty_v : &bars.empty_k);  // W's slot: W (and Sv / K~ or Sk / V~) consumed
+        mma_commit(&bars.empty_k);  // K's slot: Sv, K~ and W all consumed
         // dV = K~ state + Pv dO
         mbar_wait(&bars.st_pub, t & 1);
         if (t >= 1) mbar_wait(&bars.o_free, (2 * t - 1) & 1);
@@ -328,7 +312,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                       kk > 0);
         }
         mma_commit(&bars.x_done);
-        if (LA_BWD_REL == 0) mma_commit(&bars.empty_v);  // V's slot: Sk and V~ consumed
+        mma_commit(&bars.empty_v);  // V's slot: Sk and V~ consumed
         mbar_wait(&bars.pk_full, t & 1);
         tc_fence_after();
 #pragma unroll
@@ -392,8 +376,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     };
     // one score buffer: S block (half + 2) first (its columns then take this warp's X~ half), then the
     // two P blocks into S block `half`'s columns -- a warp only overwrites columns it has read
-    auto convert = [&](uint32_t tm_s, uint32_t x_addr, float osc, uint64_t* a_bar, uint64_t* p_bar,
-                       uint64_t* rel_bar) {
+    auto convert = [&](uint32_t tm_s, uint32_t x_addr, float osc, uint64_t* a_bar, uint64_t* p_bar) {
       const uint32_t sbuf = tmem + lane_off + tm_s;
       uint32_t p_hi[16];
       convert_block(sbuf, half + 2, p_hi);
@@ -417,7 +400,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(a_bar);
-        if (lane == 0 && rel_bar != nullptr) mbar_arrive(rel_bar);  // this warp is done with X's slot
       }
       uint32_t p_lo[16];
       convert_block(sbuf, half, p_lo);
@@ -433,12 +415,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       mbar_wait(&bars.sv_full, t & 1);
       if (warp == WARP_P && lane == 0) LB_TR(t, 11);
       tc_fence_after();
-      convert(TM_SV, slot(SLOT_K), osc, &bars.av_full, &bars.pv_full, LA_BWD_REL == 2 ? &bars.empty_k : nullptr);
+      convert(TM_SV, slot(SLOT_K), osc, &bars.av_full, &bars.pv_full);
       if (warp == WARP_P && lane == 0) LB_TR(t, 12);
       mbar_wait(&bars.sk_full, t & 1);
       if (warp == WARP_P && lane == 0) LB_TR(t, 13);
       tc_fence_after();
-      convert(TM_SK, slot(SLOT_V), osc, &bars.ak_full, &bars.pk_full, LA_BWD_REL == 1 ? &bars.empty_v : nullptr);
+      convert(TM_SK, slot(SLOT_V), osc, &bars.ak_full, &bars.pk_full);
       if (warp == WARP_P && lane == 0) LB_TR(t, 14);
     }
   } else if (warp < WARP_KV) {
@@ -476,7 +458,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const int b = chunk_len(t);
       // W = in_scale dO into K's slot (row i: lam^(i+1), rows past the tail 0), once Sv and K~ are done with K
       mbar_wait(&bars.full_d[s], (t >> 1) & 1);
-      mbar_wait(LA_BWD_REL == 2 ? &bars.ak_full : &bars.av_full, t & 1);
+      mbar_wait(&bars.av_full, t & 1);
       {
 #ifndef LA_MUTATE_DKV
         const float isc = i < b ? pw[i + 1] : 0.f;
@@ -485,7 +467,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #endif
         const uint32_t isc2 = pack_bf16x2(isc, isc);
         const uint32_t src = slot(SLOT_D + s) + hh * HALF + i * 128;
-        const uint32_t dst = slot(LA_BWD_REL == 2 ? SLOT_V : SLOT_K) + hh * HALF + i * 128;
+        const uint32_t dst = slot(SLOT_K) + hh * HALF + i * 128;
         uint4 x[8];
 #pragma unroll
         for (int m = 0; m < 8; ++m) x[m] = lds128(src + ((m ^ (i & 7)) << 4));
