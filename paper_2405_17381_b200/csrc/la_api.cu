@@ -69,7 +69,7 @@ int pick_backend(const la_desc* desc, int* backend) {
   if (desc->backend == LA_BACKEND_TCGEN05) {
     if (!tc_ok)
       return fail(LA_ERR_UNSUPPORTED,
-                  "tcgen05 backend needs bf16, d in {64, 128}, 16-byte aligned strides (dtype=%d d=%lld)",
+                  "tcgen05 backend needs bf16, d = 128, 16-byte aligned strides (dtype=%d d=%lld)",
                   desc->dtype, (long long)desc->d);
     *backend = LA_BACKEND_TCGEN05;
   } else if (desc->backend == LA_BACKEND_SIMT) {
