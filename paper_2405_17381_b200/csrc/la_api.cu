@@ -80,10 +80,14 @@ int pick_backend(const la_desc* desc, int* backend) {
   return LA_OK;
 }
 
+#ifndef LA_SIMT_MIN_CHUNKS
+#define LA_SIMT_MIN_CHUNKS 1  // chunks per segment on the SIMT path (latency-bound: more CTAs win)
+#endif
+
 la::Plan plan_for(const la_desc* desc, int backend) {
   const int64_t bh = desc->batch * desc->heads;
   if (backend == LA_BACKEND_TCGEN05) return la::tc_plan(bh, desc->n, (int)desc->d, desc->segments);
-  return la::make_plan(bh, desc->n, la::simt_chunk(desc->dtype), desc->segments, 2 * la::kNumSMs, 4);
+  return la::make_plan(bh, desc->n, la::simt_chunk(desc->dtype), desc->segments, 2 * la::kNumSMs, LA_SIMT_MIN_CHUNKS);
 }
 
 size_t acc_bytes(int dtype) { return dtype == LA_F64 ? sizeof(double) : sizeof(float); }

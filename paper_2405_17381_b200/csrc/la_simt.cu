@@ -30,6 +30,9 @@ __device__ __forceinline__ Tacc load_state(const void* base, int64_t off, int d,
 
 template <typename Tin, typename Tacc, int C, bool STATE_ONLY>
 __global__ void __launch_bounds__(kThreads) simt_pass_kernel(PassDesc p) {
+  constexpr int RP = C / 16;                      // chunk rows (and keys) per thread
+  constexpr int CP = 8;                           // feature columns per thread: 16 x 8 = 128 >= d
+  constexpr int SU = sizeof(Tacc) == 8 ? 2 : 4;   // state rows per thread per pass
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int d = p.d;
   const int ld = d + 1;  // padded row stride of the chunk tiles
@@ -87,48 +90,125 @@ __global__ void __launch_bounds__(kThreads) simt_pass_kernel(PassDesc p) {
     }
     __syncthreads();
 
+    // Register tiles (a 16 x 16 thread grid): each thread owns RP rows x up to CP columns of every
+    // product and reuses each shared-memory operand it loads across the whole tile.
+    const int tr = tid >> 4, tc = tid & 15;
     if (!STATE_ONLY) {
-      // S = (A B^T) * M
-      for (int idx = tid; idx < b * b; idx += kThreads) {
-        const int i = idx / b, j = idx % b;
-        const bool keep = p.rev ? (j >= i) : (j <= i);
-        Tacc s = 0;
-        if (keep) {
-          const Tacc* ar = sA + i * ld;
-          const Tacc* br = sB + j * ld;
-          for (int k = 0; k < d; ++k) s += ar[k] * br[k];
-          s *= pw[p.rev ? (j - i) : (i - j)];
+      // S = (A B^T) * M: rows tr*RP .. +RP, keys tc*RP .. +RP
+      {
+        Tacc acc[RP][RP];
+#pragma unroll
+        for (int x = 0; x < RP; ++x)
+#pragma unroll
+          for (int y = 0; y < RP; ++y) acc[x][y] = 0;
+        for (int k = 0; k < d; ++k) {
+          Tacc av[RP], bv[RP];
+#pragma unroll
+          for (int x = 0; x < RP; ++x) av[x] = sA[(tr * RP + x) * ld + k];
+#pragma unroll
+          for (int y = 0; y < RP; ++y) bv[y] = sB[(tc * RP + y) * ld + k];
+#pragma unroll
+          for (int x = 0; x < RP; ++x)
+#pragma unroll
+            for (int y = 0; y < RP; ++y) acc[x][y] += av[x] * bv[y];
         }
-        sS[i * (C + 1) + j] = s;
+#pragma unroll
+        for (int x = 0; x < RP; ++x)
+#pragma unroll
+          for (int y = 0; y < RP; ++y) {
+            const int i = tr * RP + x, j = tc * RP + y;
+            const bool keep = i < b && j < b && (p.rev ? (j >= i) : (j <= i));
+            sS[i * (C + 1) + j] = keep ? acc[x][y] * pw[p.rev ? (j - i) : (i - j)] : (Tacc)0;
+          }
       }
       __syncthreads();
-      // out = S C + out_scale * (A state)
-      for (int idx = tid; idx < b * d; idx += kThreads) {
-        const int i = idx / d, col = idx % d;
-        const int jlo = p.rev ? i : 0, jhi = p.rev ? b : i + 1;
-        Tacc intra = 0;
-        for (int j = jlo; j < jhi; ++j) intra += sS[i * (C + 1) + j] * sC[j * ld + col];
-        Tacc inter = 0;
-        const Tacc* ar = sA + i * ld;
-        for (int k = 0; k < d; ++k) inter += ar[k] * sKV[k * d + col];
-        const Tacc osc = pw[p.rev ? (b - 1 - i) : (i + 1)];
-        O[(int64_t)(r0 + i) * p.sn + col] = Cvt<Tin>::from_f(intra + osc * inter);
+      // out = S C + out_scale * (A state): rows tr*RP .. +RP, columns tc + 16 q
+      {
+        Tacc intra[RP][CP], inter[RP][CP];
+#pragma unroll
+        for (int x = 0; x < RP; ++x)
+#pragma unroll
+          for (int q = 0; q < CP; ++q) intra[x][q] = inter[x][q] = 0;
+        // S is zero outside the causal band, so the key range only needs to cover this tile's rows
+        const int jlo = p.rev ? min(tr * RP, b) : 0;
+        const int jhi = p.rev ? b : min(tr * RP + RP, b);
+        for (int j = jlo; j < jhi; ++j) {
+          Tacc sv[RP], cv[CP];
+#pragma unroll
+          for (int x = 0; x < RP; ++x) sv[x] = sS[(tr * RP + x) * (C + 1) + j];
+#pragma unroll
+          for (int q = 0; q < CP; ++q) cv[q] = (tc + 16 * q < d) ? sC[j * ld + tc + 16 * q] : (Tacc)0;
+#pragma unroll
+          for (int x = 0; x < RP; ++x)
+#pragma unroll
+            for (int q = 0; q < CP; ++q) intra[x][q] += sv[x] * cv[q];
+        }
+        for (int k = 0; k < d; ++k) {
+          Tacc av[RP], kv[CP];
+#pragma unroll
+          for (int x = 0; x < RP; ++x) av[x] = sA[(tr * RP + x) * ld + k];
+#pragma unroll
+          for (int q = 0; q < CP; ++q) kv[q] = (tc + 16 * q < d) ? sKV[k * d + tc + 16 * q] : (Tacc)0;
+#pragma unroll
+          for (int x = 0; x < RP; ++x)
+#pragma unroll
+            for (int q = 0; q < CP; ++q) inter[x][q] += av[x] * kv[q];
+        }
+#pragma unroll
+        for (int x = 0; x < RP; ++x) {
+          const int i = tr * RP + x;
+          if (i >= b) continue;
+          const Tacc osc = pw[p.rev ? (b - 1 - i) : (i + 1)];
+#pragma unroll
+          for (int q = 0; q < CP; ++q) {
+            const int col = tc + 16 * q;
+            if (col < d) O[(int64_t)(r0 + i) * p.sn + col] = Cvt<Tin>::from_f(intra[x][q] + osc * inter[x][q]);
+          }
+        }
       }
       __syncthreads();
     }
-    // state <- lam^b state + sum_j in_scale[j] B[j]^T C[j]
-    const Tacc decay = pw[b];
-    for (int e = tid; e < d * d; e += kThreads) {
-      const int k = e / d, col = e % d;
-      Tacc acc = 0;
-      for (int j = 0; j < b; ++j) {
-        const Tacc isc = pw[p.rev ? (j + 1) : (b - 1 - j)];
-        acc += isc * sB[j * ld + k] * sC[j * ld + col];
-      }
+    // state <- lam^b state + sum_j in_scale[j] B[j]^T C[j]: state rows tr + 16 u, columns tc + 16 q,
+    // in row passes of SU rows per thread (bounded registers for fp64 at d = 128)
+    {
+      const Tacc decay = pw[b];
+      for (int u0 = 0; u0 * 16 < d; u0 += SU) {
+        Tacc acc[SU][CP];
+#pragma unroll
+        for (int u = 0; u < SU; ++u)
+#pragma unroll
+          for (int q = 0; q < CP; ++q) acc[u][q] = 0;
+        for (int j = 0; j < b; ++j) {
+          const Tacc isc = pw[p.rev ? (j + 1) : (b - 1 - j)];
+          Tacc bv[SU], cv[CP];
+#pragma unroll
+          for (int u = 0; u < SU; ++u) {
+            const int k = tr + 16 * (u0 + u);
+            bv[u] = k < d ? isc * sB[j * ld + k] : (Tacc)0;
+          }
+#pragma unroll
+          for (int q = 0; q < CP; ++q) cv[q] = (tc + 16 * q < d) ? sC[j * ld + tc + 16 * q] : (Tacc)0;
+#pragma unroll
+          for (int u = 0; u < SU; ++u)
+#pragma unroll
+            for (int q = 0; q < CP; ++q) acc[u][q] += bv[u] * cv[q];
+        }
+#pragma unroll
+        for (int u = 0; u < SU; ++u) {
+          const int k = tr + 16 * (u0 + u);
+          if (k >= d) continue;
+#pragma unroll
+          for (int q = 0; q < CP; ++q) {
+            const int col = tc + 16 * q;
+            if (col >= d) continue;
+            Tacc a = acc[u][q];
 #ifdef LA_MUTATE_DKV
-      if (p.rev) acc = -acc;  // fault injection: the reference's `_dkv_step` sign flip (test_kernels.py:249-268)
+            if (p.rev) a = -a;  // fault injection: the reference's `_dkv_step` sign flip (test_kernels.py:249-268)
 #endif
-      sKV[e] = decay * sKV[e] + acc;
+            sKV[k * d + col] = decay * sKV[k * d + col] + a;
+          }
+        }
+      }
     }
     __syncthreads();
   }

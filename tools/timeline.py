@@ -2,6 +2,7 @@
 each kernel's start offset, duration and the idle gap before it.  A design probe, not a bench.
 
 usage: python tools/timeline.py [b:n ...]   (default 8:8192 4:16384 2:32768 1:65536 1:131072)
+       TL_H / TL_D / TL_DTYPE (bf16 | f32 | f64) set heads, head dim and dtype (default 16, 128, bf16)
 """
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -11,12 +12,13 @@ from paper_2405_17381_b200 import ops
 from paper_2405_17381_b200.positional import decay_rate
 
 dev = torch.device("cuda", 0)
-H, D = 16, 128
+H, D = int(os.environ.get("TL_H", 16)), int(os.environ.get("TL_D", 128))
+DT = {"bf16": torch.bfloat16, "f32": torch.float32, "f64": torch.float64}[os.environ.get("TL_DTYPE", "bf16")]
 lam = ops.decay_tensor([decay_rate(h, 1, H, 16) for h in range(1, H + 1)], H, dev)
 shapes = [tuple(int(x) for x in a.split(":")) for a in sys.argv[1:]] or [(8, 8192), (4, 16384), (2, 32768),
                                                                           (1, 65536), (1, 131072)]
 for b, n in shapes:
-    q, k, v, do = (torch.randn(b, H, n, D, device=dev, dtype=torch.bfloat16) * D ** -0.5 for _ in range(4))
+    q, k, v, do = (torch.randn(b, H, n, D, device=dev, dtype=DT) * D ** -0.5 for _ in range(4))
 
     def fb():
         _, seg = ops.la_forward(q, k, v, None, lam_dev=lam, want_seg_states=True)
