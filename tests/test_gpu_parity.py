@@ -231,6 +231,23 @@ def test_persistent_units_with_edge_states():
         assert orc.max_rel_error(host(got), ref) <= tol
 
 
+@pytest.mark.parametrize("n", [1, 2, 127, 129, 255])
+def test_tcgen05_tiny_and_ragged_lengths(n):
+    """The tensor-core path at lengths shorter than / just around one 128-row chunk (TMA boxes past the
+    end read zeros and store nothing), with kv_in and every edge state exported."""
+    b, h, d = 2, 3, 128
+    lams = [1.0, 0.9, 0.5]
+    q, k, v, do = (dev(a, torch.bfloat16) for a in _batched(b, h, n, d, seed=100 + n))
+    kv_in = torch.rand(b, h, d, d, device="cuda") * 0.05
+    o, kv_out = ops.la_forward(q, k, v, lams, kv_in=kv_in, want_state=True, backend="tcgen05")
+    dq, dk, dv, dkv_out = ops.la_backward(q, k, v, do, lams, kv_in=kv_in, want_state=True, backend="tcgen05")
+    qq, kk, vv, dd = (host(t) for t in (q, k, v, do))
+    ro, rkv = orc.batched_forward(qq, kk, vv, lams, kv_in=host(kv_in))
+    (rdq, rdk, rdv), rdkv = orc.batched_backward(qq, kk, vv, dd, lams, kv_in=host(kv_in))
+    for got, ref in ((o, ro), (kv_out, rkv), (dq, rdq), (dk, rdk), (dv, rdv), (dkv_out, rdkv)):
+        assert orc.max_rel_error(host(got), ref) <= TOL[torch.bfloat16]
+
+
 def test_autograd_function_matches_ops():
     b, h, n, d = 2, 2, 333, 128
     lams = [0.9, 0.99]
