@@ -313,6 +313,24 @@ def measure_rows(ops, device, stream, pk) -> dict:
                                                  / (pk["bf16_tflops"] * 1e12), 2)}
         del qq, kk, vv, dd
     out["tnl385m_attention"] = cfg385
+    # BASELINE configs[3] on one GPU (TNL-7B attention shape: 32 heads, d 128, L = 30), fixed 64K tokens;
+    # at N GPUs the heads shard 32 / N per rank with no collective, so this is the per-GPU-equivalent line
+    cfg7 = {}
+    lam32 = ops.decay_tensor([decay_rate(h, 1, 32, 30) for h in range(1, 33)], 32, device)
+    for n7 in (2048, 8192, 32768):
+        bt = TOKENS // n7
+        qq, kk, vv, dd = (rnd(bt, 32, n7, D) for _ in range(4))
+
+        def fb7():
+            _, seg = ops.la_forward(qq, kk, vv, None, lam_dev=lam32, want_seg_states=True)
+            ops.la_backward(qq, kk, vv, dd, None, lam_dev=lam32, fwd_seg_states=seg)
+
+        t = _time_ms(fb7, stream, reps=5)
+        cfg7[str(n7)] = {"batch": bt, "ms_fwd_bwd": round(t, 4), "tokens_per_s": round(TOKENS / (t / 1e3)),
+                         "pct_bf16_peak": round(100 * TOKENS / (t / 1e3) * 32 * FLOPS_PER_HEAD_TOKEN
+                                                / (pk["bf16_tflops"] * 1e12), 2)}
+        del qq, kk, vv, dd
+    out["tnl7b_attention_1gpu"] = cfg7
     # BASELINE configs[0] (the reference's CPU-runnable parity case): batch 1, H 4, n 1024, d 64, fp32 on
     # the precision (SIMT) path, lam (1, 0.99, 0.9, 0.5); latency-bound (4 sequences), so no roofline
     c1 = [torch.randn(1, 4, 1024, 64, device=device, generator=g) * 0.5 for _ in range(4)]
