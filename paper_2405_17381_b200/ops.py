@@ -178,9 +178,14 @@ def la_backward(q, k, v, do, lam, *, block=None, kv_in=None, dkv_in=None, want_s
     dkv_out = torch.empty((g.batch, g.heads, g.d, g.d), dtype=state_dtype(q.dtype), device=q.device) \
         if want_state else None
     ws, nbytes = _workspace(lib, desc, q.device)
-    if fwd_seg_states is not None and fwd_seg_states.shape[2] != segment_count(desc):
-        raise ShapeError(f"fwd_seg_states holds {fwd_seg_states.shape[2]} segments, the plan has "
-                         f"{segment_count(desc)}")
+    if fwd_seg_states is not None:
+        want = (g.batch, g.heads, segment_count(desc), g.d, g.d)
+        if tuple(fwd_seg_states.shape) != want:
+            raise ShapeError(f"fwd_seg_states has shape {tuple(fwd_seg_states.shape)}, this problem's plan "
+                             f"needs {want}")
+        if fwd_seg_states.dtype != state_dtype(q.dtype) or fwd_seg_states.device != q.device \
+                or not fwd_seg_states.is_contiguous():
+            raise ShapeError(f"fwd_seg_states must be a contiguous {state_dtype(q.dtype)} tensor on {q.device}")
     _lib.check(lib.la_bwd(ctypes.byref(desc), _ptr(q), _ptr(k), _ptr(v), _ptr(do), _lam_ptr(lam_dev),
                           _ptr(kv_in), _ptr(dkv_in), _ptr(fwd_seg_states), _ptr(dq), _ptr(dk), _ptr(dv),
                           _ptr(dkv_out), _ptr(ws), nbytes, _stream(q.device)))

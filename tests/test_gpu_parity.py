@@ -305,3 +305,18 @@ def test_full_size_properties(n):
     _, kv1 = ops.la_forward(sl(qb, 0, cut), sl(kb, 0, cut), sl(vb, 0, cut), lams, want_state=True)
     o2 = ops.la_forward(sl(qb, cut, n), sl(kb, cut, n), sl(vb, cut, n), lams, kv_in=kv1).float()
     assert ((o2 - o_auto[:, :, cut:]).abs().max() / scale).item() <= 2e-2
+
+
+def test_saved_segment_states_are_validated():
+    """fwd_seg_states from another problem (other plan, dtype or layout) is refused, not misread."""
+    from paper_2405_17381_b200.errors import ShapeError
+    b, h, n, d = 1, 2, 4096, 128
+    q, k, v, do = (torch.rand(b, h, n, d, device="cuda", dtype=torch.bfloat16) for _ in range(4))
+    _, seg = ops.la_forward(q, k, v, [0.9, 0.99], want_seg_states=True)
+    assert seg is not None
+    with pytest.raises(ShapeError):
+        ops.la_backward(q, k, v, do, [0.9, 0.99], fwd_seg_states=seg[:, :, :-1])
+    with pytest.raises(ShapeError):
+        ops.la_backward(q, k, v, do, [0.9, 0.99], fwd_seg_states=seg.double())
+    with pytest.raises(ShapeError):
+        ops.la_backward(q, k, v, do, [0.9, 0.99], fwd_seg_states=seg.transpose(3, 4))
