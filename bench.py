@@ -522,23 +522,28 @@ def run_reference(args) -> None:
         return
     cores = len(os.sched_getaffinity(0))
     pool = CpuPool(cores)
+    # one step = the sweep's n = 8192 batch (8 sequences x 16 heads = 128 units), handed out one unit at a
+    # time so the strongly decaying heads (subnormal-heavy on the CPU) do not leave cores idle
+    units = (TOKENS // CPU_N) * H
     try:
         for _ in range(args.warmup):
-            pool.run(H, CPU_N)
-        walls = [pool.run(H, CPU_N) for _ in range(args.steps)]
+            pool.run(units, CPU_N)
+        walls = [pool.run(units, CPU_N) for _ in range(args.steps)]
     finally:
         pool.close()
     total = sum(walls)
-    value = H * CPU_N * len(walls) / total / H
+    value = units * CPU_N * len(walls) / total / H
     line = {
         "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(1e3 * total / len(walls), 2), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic", "impl": "reference",
-        "config": {"workload": "TNL-1B attention core (BASELINE configs[2]) on host cores: H=16, d=128; step = all 16 "
-                               f"heads of one sequence of n={CPU_N}, fwd+bwd, spread over {cores} processes",
-                   "heads": H, "head_dim": D, "seq_len": CPU_N, "parallelism": f"{cores} processes x 1 BLAS thread"},
+        "config": {"workload": "TNL-1B attention core (BASELINE configs[2]) on host cores: H=16, d=128; step = the "
+                               f"sweep's n={CPU_N} batch ({TOKENS // CPU_N} sequences x {H} heads), fwd+bwd, over "
+                               f"{cores} processes",
+                   "heads": H, "head_dim": D, "seq_len": CPU_N, "batch": TOKENS // CPU_N,
+                   "parallelism": f"{cores} processes x 1 BLAS thread"},
         "cpu_baseline": {"value": round(value, 1), "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"{H} (head) units of n={CPU_N} per step; reference tiled algorithm "
+                         "sample": f"{units} (batch, head) units of n={CPU_N} per step; reference tiled algorithm "
                                    "(oracle restatement of kernels.py:253-334), numpy/OpenBLAS fp32"},
         "e2e": {"value": round(value, 1), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
