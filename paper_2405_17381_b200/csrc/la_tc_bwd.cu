@@ -169,6 +169,31 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   // reverse sweep: chunk t covers rows [row0(t), row0(t) + len(t))
   auto chunk_row0 = [&](int t) { return p0 + (nchunks - 1 - t) * C; };
   auto chunk_len = [&](int t) { return min(C, p1 - chunk_row0(t)); };
+  // W = in_scale dO into K's slot (row i: lam^(i+1), rows past the tail 0), once Sv and K~ are done with K;
+  // the B/O warps run it (thread -> row i, 64-column half hh).  (Moving it to the state warps, idle at
+  // that point, measured no faster: the pass is bound by shared-memory traffic, not by who issues it.)
+  auto build_w = [&](int t, int i, int hh) {
+    const int s = t & 1;
+    const int b = chunk_len(t);
+    mbar_wait(&bars.full_d[s], (t >> 1) & 1);
+    mbar_wait(&bars.av_full, t & 1);
+#ifndef LA_MUTATE_DKV
+    const float isc = i < b ? pw[i + 1] : 0.f;
+#else
+    const float isc = i < b ? -pw[i + 1] : 0.f;  // fault injection: `_dkv_step` sign flip (test_kernels.py:249-268)
+#endif
+    const uint32_t isc2 = pack_bf16x2(isc, isc);
+    const uint32_t src = slot(SLOT_D + s) + hh * HALF + i * 128;
+    const uint32_t dst = slot(SLOT_K) + hh * HALF + i * 128;
+    uint4 x[8];
+#pragma unroll
+    for (int m = 0; m < 8; ++m) x[m] = lds128(src + ((m ^ (i & 7)) << 4));
+#pragma unroll
+    for (int m = 0; m < 8; ++m) sts128(dst + ((m ^ (i & 7)) << 4), mul_bf16x2(x[m], isc2));
+    fence_proxy_async_smem();
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) mbar_arrive(&bars.w_ready);
+  };
 
   if (warp == WARP_TMA) {
     // ------------------------------------------------------------ producers (lanes 0-3) + store lane (4)
@@ -455,28 +480,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     };
     for (int t = 0; t < nchunks; ++t) {
       const int s = t & 1;
-      const int b = chunk_len(t);
-      // W = in_scale dO into K's slot (row i: lam^(i+1), rows past the tail 0), once Sv and K~ are done with K
-      mbar_wait(&bars.full_d[s], (t >> 1) & 1);
-      mbar_wait(&bars.av_full, t & 1);
-      {
-#ifndef LA_MUTATE_DKV
-        const float isc = i < b ? pw[i + 1] : 0.f;
-#else
-        const float isc = i < b ? -pw[i + 1] : 0.f;  // fault injection: `_dkv_step` sign flip (test_kernels.py:249-268)
-#endif
-        const uint32_t isc2 = pack_bf16x2(isc, isc);
-        const uint32_t src = slot(SLOT_D + s) + hh * HALF + i * 128;
-        const uint32_t dst = slot(SLOT_K) + hh * HALF + i * 128;
-        uint4 x[8];
-#pragma unroll
-        for (int m = 0; m < 8; ++m) x[m] = lds128(src + ((m ^ (i & 7)) << 4));
-#pragma unroll
-        for (int m = 0; m < 8; ++m) sts128(dst + ((m ^ (i & 7)) << 4), mul_bf16x2(x[m], isc2));
-      }
-      fence_proxy_async_smem();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&bars.w_ready);
+      build_w(t, i, hh);
       if (warp == WARP_O && lane == 0) LB_TR(t, 15);
       epilogue(&bars.ov_full, 2 * t, slot(SLOT_D + s), &bars.dv_staged[s], t);
       if (warp == WARP_O && lane == 0) LB_TR(t, 16);
