@@ -17,7 +17,8 @@
 //   dK = V~ state^T + Pk Q            TS-MMAs -> TMEM O -> SMEM (Q's slot)  -> TMA store
 //
 // SMEM: Q and dO double-slotted, K and V single-slotted (they are consumed first in a
-// chunk, so their refill overlaps the rest of it), bf16 state: 7 x 32 KB = 224 KB.
+// chunk, so their refill overlaps the rest of it; the tile after each refill is prefetched
+// into L2 so the next refill sees L2 latency), bf16 state: 7 x 32 KB = 224 KB.
 // TMEM: SV | SK | O | state = 512 columns.  Warp roles as in la_tc.cu (26 warps).
 #include <cudaTypedefs.h>
 
