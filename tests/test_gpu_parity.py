@@ -320,3 +320,20 @@ def test_saved_segment_states_are_validated():
         ops.la_backward(q, k, v, do, [0.9, 0.99], fwd_seg_states=seg.double())
     with pytest.raises(ShapeError):
         ops.la_backward(q, k, v, do, [0.9, 0.99], fwd_seg_states=seg.transpose(3, 4))
+
+
+@pytest.mark.parametrize("n", [5000, 12345, 33333])
+def test_long_ragged_segmented_sequences(n):
+    """Long sequences whose length is no multiple of the chunk, segment or sub-segment length (the
+    planner splits them; every boundary is ragged), forward + backward with saved segment states."""
+    b, h, d = 1, 2, 128
+    lams = [0.999, 0.9]
+    q, k, v, do = (dev(a, torch.bfloat16) for a in _batched(b, h, n, d, seed=n))
+    assert ops.segment_count(ops._desc(ops._geometry(q, "bhnd"), q.dtype, None, "auto", 0)) > 1
+    (o, kv_out), seg = ops.la_forward(q, k, v, lams, want_state=True, want_seg_states=True)
+    dq, dk, dv, dkv_out = ops.la_backward(q, k, v, do, lams, want_state=True, fwd_seg_states=seg)
+    qq, kk, vv, dd = (host(t) for t in (q, k, v, do))
+    ro, rkv = orc.batched_forward(qq, kk, vv, lams)
+    (rdq, rdk, rdv), rdkv = orc.batched_backward(qq, kk, vv, dd, lams)
+    for got, ref in ((o, ro), (kv_out, rkv), (dq, rdq), (dk, rdk), (dv, rdv), (dkv_out, rdkv)):
+        assert orc.max_rel_error(host(got), ref) <= TOL[torch.bfloat16]
