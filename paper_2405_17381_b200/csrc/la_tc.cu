@@ -606,6 +606,10 @@ thread_local char g_detail[256];
 
 }  // namespace
 
+#ifndef LA_L2_PROMO
+#define LA_L2_PROMO CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+#endif
+
 bool tc_make_map(CUtensorMap* map, const void* base, const PassDesc& p, int box_rows) {
   auto enc = encode_fn();
   if (enc == nullptr) {
@@ -620,7 +624,7 @@ bool tc_make_map(CUtensorMap* map, const void* base, const PassDesc& p, int box_
   if (p.heads == 1) strides[1] = strides[0] * (cuuint64_t)p.n;
   if (p.batch == 1) strides[2] = strides[1] * (cuuint64_t)p.heads;
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, (CUtensorMapL2promotion)LA_L2_PROMO,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     snprintf(g_detail, sizeof(g_detail), "cuTensorMapEncodeTiled failed (CUresult %d) base=%p dims=%llu,%llu,%llu,%llu "
