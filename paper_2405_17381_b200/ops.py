@@ -28,8 +28,18 @@ def state_dtype(dtype: torch.dtype) -> torch.dtype:
     return torch.float64 if dtype == torch.float64 else torch.float32
 
 
+_DECAY_CACHE: dict = {}
+_DECAY_CACHE_MAX = 64
+
+
 def decay_tensor(lam, heads: int, device) -> torch.Tensor:
-    """Validate per-head decays (host side) and return a device fp64 [heads] tensor."""
+    """Validate per-head decays (host side) and return a device fp64 [heads] tensor.
+
+    Results are cached per (values, device): a call with host values (float / list / CPU tensor)
+    after the first costs no host-to-device copy, so the autograd ops and the GLA layer keep the
+    host ahead of the GPU (a pageable copy per call would serialise them) and stay capturable in a
+    CUDA graph.  The returned tensor is shared: treat it as read-only.  A CUDA tensor argument is
+    read back to validate it (a synchronisation) -- build it once with this function instead."""
     if isinstance(lam, torch.Tensor):
         vals = lam.detach().to("cpu", torch.float64).reshape(-1).tolist()
     elif isinstance(lam, (int, float)):
@@ -40,9 +50,20 @@ def decay_tensor(lam, heads: int, device) -> torch.Tensor:
         vals = vals * heads
     if len(vals) != heads:
         raise ShapeError(f"need one decay per head: got {len(vals)} for {heads} heads")
+    dev = torch.device(device)
+    if dev.type == "cuda" and dev.index is None:
+        dev = torch.device("cuda", torch.cuda.current_device())
+    key = (tuple(vals), dev.type, dev.index)
+    hit = _DECAY_CACHE.get(key)
+    if hit is not None:
+        return hit
     for x in vals:
         check_decay(x)
-    return torch.tensor(vals, dtype=torch.float64, device=device)
+    t = torch.tensor(vals, dtype=torch.float64, device=dev)
+    if len(_DECAY_CACHE) >= _DECAY_CACHE_MAX:
+        _DECAY_CACHE.pop(next(iter(_DECAY_CACHE)))
+    _DECAY_CACHE[key] = t
+    return t
 
 
 @dataclass(frozen=True)

@@ -94,3 +94,20 @@ def test_segment_count_and_launches_follow_the_plan():
     assert lib.la_segment_count(ctypes.byref(long_)) > 1
     assert [lib.la_launch_count(ctypes.byref(long_), w) for w in (0, 1, 2)] == [3, 6, 4]
     assert lib.la_segment_count(ctypes.byref(_desc(n=0))) == -1
+
+
+def test_decay_tensor_is_validated_once_and_cached():
+    """Host decays are validated and copied once per (values, device); later calls reuse the tensor
+    (no per-call host-to-device copy in the autograd ops), invalid values still raise every time."""
+    import torch
+    from paper_2405_17381_b200 import ops
+    from paper_2405_17381_b200.errors import DomainError, ShapeError
+    a = ops.decay_tensor([0.9, 0.5], 2, "cpu")
+    assert a is ops.decay_tensor([0.9, 0.5], 2, torch.device("cpu"))
+    assert a is not ops.decay_tensor([0.9, 0.6], 2, "cpu")
+    assert ops.decay_tensor(0.7, 3, "cpu").tolist() == [0.7, 0.7, 0.7]
+    for bad in ([1.5, 0.5], [0.0, 0.5]):
+        with pytest.raises(DomainError):
+            ops.decay_tensor(bad, 2, "cpu")
+    with pytest.raises(ShapeError):
+        ops.decay_tensor([0.9, 0.5, 0.4], 2, "cpu")
