@@ -110,9 +110,13 @@ class SequenceParallelLightning(torch.autograd.Function):
     """o_p = slice p of LA(q, k, v) for the full sequence; inputs are this rank's slice."""
 
     @staticmethod
-    def forward(ctx, q, k, v, lam, group, kernels, n_axis):
+    def forward(ctx, q, k, v, lam, group, kernels, n_axis, lengths=None):
         rank = dist.get_rank(group)
-        lengths = _lengths(q.shape[n_axis], group)
+        if lengths is None:
+            lengths = _lengths(q.shape[n_axis], group)
+        elif len(lengths) != dist.get_world_size(group) or lengths[rank] != q.shape[n_axis]:
+            raise ShapeError(f"lengths {list(lengths)} do not match this group / this rank's slice "
+                             f"({q.shape[n_axis]} positions on rank {rank})")
         delta = kernels.forward_state(k, v, lam)
         kv_in = prefix_states(_gather(delta, group), lengths, lam, rank)
         o = kernels.forward(q, k, v, lam, kv_in)
@@ -129,15 +133,18 @@ class SequenceParallelLightning(torch.autograd.Function):
         r = kernels.backward_state(q, do, lam)
         dkv_in = suffix_states(_gather(r, group), ctx.lengths, lam, rank)
         dq, dk, dv = kernels.backward(q, k, v, do, lam, kv_in, dkv_in)
-        return dq, dk, dv, None, None, None, None
+        return dq, dk, dv, None, None, None, None, None
 
 
-def sp_lightning_attention(q, k, v, lam, group=None, *, layout: str = "bhnd", kernels: LocalKernels | None = None):
+def sp_lightning_attention(q, k, v, lam, group=None, *, layout: str = "bhnd", kernels: LocalKernels | None = None,
+                           lengths: Sequence[int] | None = None):
     """Sequence-parallel lightning attention over ``group`` (default: WORLD).
 
     ``q, k, v``: this rank's contiguous slice of positions, [b, h, n_p, d] ("bhnd") or [b, n_p, h, d]
     ("bnhd"); ranks hold slices in rank order.  ``lam``: one decay per head (float64 tensor on the
-    inputs' device, or anything ``ops.decay_tensor`` accepts).
+    inputs' device, or anything ``ops.decay_tensor`` accepts).  ``lengths``: every rank's slice length in
+    rank order, when the caller knows them (fixed slicing); otherwise they are exchanged with one small
+    all_gather per call, whose read-back synchronises the host with the stream.
     """
     if layout not in ("bhnd", "bnhd"):
         raise ShapeError(f"layout must be 'bhnd' or 'bnhd', got {layout!r}")
@@ -148,4 +155,5 @@ def sp_lightning_attention(q, k, v, lam, group=None, *, layout: str = "bhnd", ke
         lam = decay_tensor(lam, heads, q.device)
     if kernels is None:
         kernels = CudaKernels(layout=layout)
-    return SequenceParallelLightning.apply(q, k, v, lam, group, kernels, 2 if layout == "bhnd" else 1)
+    return SequenceParallelLightning.apply(q, k, v, lam, group, kernels, 2 if layout == "bhnd" else 1,
+                                           None if lengths is None else [int(x) for x in lengths])
