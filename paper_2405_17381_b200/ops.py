@@ -106,7 +106,8 @@ def _prep(tensors: Sequence[torch.Tensor], names: str, layout: str):
         if t.dtype != first.dtype or t.device != first.device:
             raise ShapeError(f"{name}: dtype/device {t.dtype}/{t.device} != {first.dtype}/{first.device}")
     # contiguous, 16-byte aligned operands (TMA descriptors need aligned bases)
-    out = [t if (t.is_contiguous() and t.data_ptr() % 16 == 0) else t.contiguous().clone() for t in tensors]
+    out = [t if (t.is_contiguous() and t.data_ptr() % 16 == 0)
+           else (t.clone() if t.is_contiguous() else t.contiguous()) for t in tensors]  # one copy at most
     return out, _geometry(out[0], layout)
 
 
