@@ -149,7 +149,15 @@ def _workspace(lib, desc, device):
     return ws, nbytes
 
 
+_RAW_STREAM = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+
+
 def _stream(device) -> ctypes.c_void_p:
+    # the raw handle of the caller's current stream; torch.cuda.current_stream() builds a Stream
+    # object per call (~7 us of a ~25 us host path for a decode step)
+    if _RAW_STREAM is not None:
+        idx = device.index if device.index is not None else torch.cuda.current_device()
+        return ctypes.c_void_p(_RAW_STREAM(idx))
     return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
 
 
