@@ -74,6 +74,20 @@ struct PassDesc {
 };
 
 // Segment plan shared by host code of every backend.
+// Raise a kernel's dynamic shared-memory limit once per (kernel, device) instead of on every launch
+// (cudaFuncSetAttribute costs microseconds of host time).  `done` is the caller's per-kernel flag
+// array, indexed by device ordinal.
+template <typename K>
+inline cudaError_t set_smem_once(K kernel, int bytes, bool (&done)[64]) {
+  int dev = 0;
+  cudaError_t err = cudaGetDevice(&dev);
+  if (err != cudaSuccess) return err;
+  if (dev >= 0 && dev < 64 && done[dev]) return cudaSuccess;
+  err = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (err == cudaSuccess && dev >= 0 && dev < 64) done[dev] = true;
+  return err;
+}
+
 struct Plan {
   int chunk;        // rows per chunk in the kernel
   int nseg;         // segments per (b, h)

@@ -167,12 +167,10 @@ __global__ void __launch_bounds__(256) decode_bulk_kernel(const T* __restrict__ 
 cudaError_t decode_launch(int dtype, int batch, int heads, int d, int64_t sb, int64_t sh, const void* q,
                           const void* k, const void* v, const double* lam, void* kv, void* o, cudaStream_t st) {
   const dim3 grid((unsigned)(batch * heads));
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(decode_bulk_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 128 * 4);
-    cudaFuncSetAttribute(decode_bulk_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 128 * 4);
-    attr_set = true;
-  }
+  static bool set_f32[64] = {}, set_bf16[64] = {};  // per device: a process may drive several GPUs
+  cudaError_t aerr = set_smem_once(decode_bulk_kernel<float>, 128 * 128 * 4, set_f32);
+  if (aerr == cudaSuccess) aerr = set_smem_once(decode_bulk_kernel<__nv_bfloat16>, 128 * 128 * 4, set_bf16);
+  if (aerr != cudaSuccess) return aerr;
   // 16-byte state accesses when a warp's 32 vectors span exactly one row (d = 128 fp32, d = 64 fp64)
   switch (dtype) {
     case LA_F64:

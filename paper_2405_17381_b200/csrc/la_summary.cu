@@ -190,8 +190,8 @@ cudaError_t tc_summary_launch(const PassDesc& p, cudaStream_t st) {
   a.g_lo = p.g_lo;
   a.lam = p.lam;
   a.delta_out = reinterpret_cast<float*>(p.delta_out);
-  cudaError_t err =
-      cudaFuncSetAttribute(tc_summary_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S_SMEM_BYTES);
+  static bool smem_set[64] = {};
+  cudaError_t err = set_smem_once(tc_summary_kernel, (int)S_SMEM_BYTES, smem_set);
   if (err != cudaSuccess) return err;
   dim3 grid((p.g_hi - p.g_lo + 1) * p.sub_per_seg, p.batch * p.heads);
   tc_summary_kernel<<<grid, S_THREADS, S_SMEM_BYTES, st>>>(mb, mc, a);
