@@ -19,6 +19,7 @@
 //   rev: mask M[i][j] = lam^(j-i) (j >= i); out-scale lam^(b-1-i); in-scale lam^(j+1)
 //   state <- lam^b * state + sum_j in_scale[j] b[j] c[j]^T
 #pragma once
+#include <atomic>
 
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
@@ -78,13 +79,13 @@ struct PassDesc {
 // (cudaFuncSetAttribute costs microseconds of host time).  `done` is the caller's per-kernel flag
 // array, indexed by device ordinal.
 template <typename K>
-inline cudaError_t set_smem_once(K kernel, int bytes, bool (&done)[64]) {
+inline cudaError_t set_smem_once(K kernel, int bytes, std::atomic<bool> (&done)[64]) {
   int dev = 0;
   cudaError_t err = cudaGetDevice(&dev);
   if (err != cudaSuccess) return err;
-  if (dev >= 0 && dev < 64 && done[dev]) return cudaSuccess;
-  err = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  if (err == cudaSuccess && dev >= 0 && dev < 64) done[dev] = true;
+  if (dev >= 0 && dev < 64 && done[dev].load(std::memory_order_acquire)) return cudaSuccess;
+  err = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);  // idempotent
+  if (err == cudaSuccess && dev >= 0 && dev < 64) done[dev].store(true, std::memory_order_release);
   return err;
 }
 

@@ -167,7 +167,7 @@ __global__ void __launch_bounds__(256) decode_bulk_kernel(const T* __restrict__ 
 cudaError_t decode_launch(int dtype, int batch, int heads, int d, int64_t sb, int64_t sh, const void* q,
                           const void* k, const void* v, const double* lam, void* kv, void* o, cudaStream_t st) {
   const dim3 grid((unsigned)(batch * heads));
-  static bool set_f32[64] = {}, set_bf16[64] = {};  // per device: a process may drive several GPUs
+  static std::atomic<bool> set_f32[64] = {}, set_bf16[64] = {};  // per device: a process may drive several GPUs
   cudaError_t aerr = set_smem_once(decode_bulk_kernel<float>, 128 * 128 * 4, set_f32);
   if (aerr == cudaSuccess) aerr = set_smem_once(decode_bulk_kernel<__nv_bfloat16>, 128 * 128 * 4, set_bf16);
   if (aerr != cudaSuccess) return aerr;

@@ -237,7 +237,7 @@ template <typename Tin, typename Tacc, int C, bool STATE_ONLY>
 cudaError_t launch_simt(const PassDesc& p, cudaStream_t st) {
   auto kern = simt_pass_kernel<Tin, Tacc, C, STATE_ONLY>;
   const size_t smem = simt_smem_bytes<Tacc, C>(p.d);
-  static bool smem_set[64] = {};  // raised once to the d = 128 footprint, which covers every d <= 128
+  static std::atomic<bool> smem_set[64] = {};  // raised once to the d = 128 footprint, which covers every d <= 128
   cudaError_t err = set_smem_once(kern, (int)simt_smem_bytes<Tacc, C>(128), smem_set);
   if (err != cudaSuccess) return err;
   dim3 grid(p.nseg, p.batch * p.heads);

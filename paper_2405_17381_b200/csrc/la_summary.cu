@@ -190,7 +190,7 @@ cudaError_t tc_summary_launch(const PassDesc& p, cudaStream_t st) {
   a.g_lo = p.g_lo;
   a.lam = p.lam;
   a.delta_out = reinterpret_cast<float*>(p.delta_out);
-  static bool smem_set[64] = {};
+  static std::atomic<bool> smem_set[64] = {};
   cudaError_t err = set_smem_once(tc_summary_kernel, (int)S_SMEM_BYTES, smem_set);
   if (err != cudaSuccess) return err;
   dim3 grid((p.g_hi - p.g_lo + 1) * p.sub_per_seg, p.batch * p.heads);

@@ -661,7 +661,7 @@ cudaError_t launch_tc(const PassDesc& p, cudaStream_t st) {
   a.out_T = p.state_out_T;
   auto kern = tc_pass_kernel;
   const size_t smem_bytes = SMEM_BYTES;
-  static bool smem_set[64] = {};
+  static std::atomic<bool> smem_set[64] = {};
   cudaError_t err = set_smem_once(kern, (int)smem_bytes, smem_set);
   if (err != cudaSuccess) return err;
   dim3 grid(p.nseg, p.batch * p.heads);

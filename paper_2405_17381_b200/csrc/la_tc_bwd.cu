@@ -591,7 +591,7 @@ cudaError_t tc_dkdv_launch(const PassDesc& p, const void* q, const void* k, cons
   a.in_bh_stride = p.state_in_bh_stride;
   a.in_seg_stride = p.state_in_seg_stride;
   a.state_out = reinterpret_cast<float*>(p.state_out);
-  static bool smem_set[64] = {};
+  static std::atomic<bool> smem_set[64] = {};
   cudaError_t err = set_smem_once(tc_dkdv_kernel, (int)SMEM_BYTES, smem_set);
   if (err != cudaSuccess) return err;
   dim3 grid(p.nseg, p.batch * p.heads);
