@@ -42,3 +42,47 @@ def test_forward_backward_decode_replay_from_a_cuda_graph():
     for a, w in zip(got, want):
         assert torch.equal(a, w)
     assert torch.equal(kv_graph, kv_eager)
+
+
+def test_entry_points_from_two_host_threads():
+    """Two host threads, each on its own stream, call forward + backward (segmented, with the
+    backward's side stream) concurrently: results equal the single-threaded ones."""
+    import threading
+
+    from paper_2405_17381_b200 import ops
+    dev = torch.device("cuda", 0)
+    torch.manual_seed(1)
+    shapes = [(1, 4, 4096, 128), (2, 2, 3000, 128)]
+    data = [[torch.randn(*s, device=dev, dtype=torch.bfloat16) * 128 ** -0.5 for _ in range(4)] for s in shapes]
+    lams = [[0.99, 0.9, 0.5, 1.0], [0.95, 0.7]]
+
+    def run(i):
+        q, k, v, do = data[i]
+        o, seg = ops.la_forward(q, k, v, lams[i], want_seg_states=True)
+        return (o,) + tuple(ops.la_backward(q, k, v, do, lams[i], fwd_seg_states=seg))
+
+    want = [run(0), run(1)]
+    torch.cuda.synchronize()
+    got, errors = [None, None], []
+
+    def worker(i):
+        try:
+            torch.cuda.set_device(0)
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                for _ in range(5):
+                    out = run(i)
+                s.synchronize()
+            got[i] = out
+        except Exception as e:  # noqa: BLE001 -- surfaced below
+            errors.append(e)
+
+    threads = [threading.Thread(target=worker, args=(i,)) for i in range(2)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join(timeout=120)
+    assert not errors, errors
+    for i in range(2):
+        for a, w in zip(got[i], want[i]):
+            assert torch.equal(a, w)
