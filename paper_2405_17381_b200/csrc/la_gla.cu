@@ -181,13 +181,9 @@ __global__ void __launch_bounds__(256) prologue_bwd_kernel(const T* __restrict__
                                                            int64_t rows, int n, int width, int d, int64_t offset,
                                                            int act) {
   constexpr int V = Vec<T>::N;
-  extern __shared__ double sdt[];  // [d/2]
+  extern __shared__ double sdt[];  // [blockDim.x][V / 2]: this block's per-pair partials
   const int vw = width / V, hd = d >> 1;
   const int vc = blockIdx.x * blockDim.x + threadIdx.x;
-  if (theta != nullptr) {
-    for (int j = threadIdx.x; j < hd; j += blockDim.x) sdt[j] = 0.0;
-    __syncthreads();
-  }
   Tacc acc[V / 2];
 #pragma unroll
   for (int pr = 0; pr < V / 2; ++pr) acc[pr] = 0;
@@ -237,13 +233,19 @@ __global__ void __launch_bounds__(256) prologue_bwd_kernel(const T* __restrict__
     }
   }
   if (theta == nullptr) return;
-  if (vc < vw) {
 #pragma unroll
-    for (int pr = 0; pr < V / 2; ++pr) atomicAdd(&sdt[((c0 >> 1) + pr) % hd], (double)acc[pr]);  // over heads
-  }
+  for (int pr = 0; pr < V / 2; ++pr) sdt[threadIdx.x * (V / 2) + pr] = vc < vw ? (double)acc[pr] : 0.0;
   __syncthreads();
+  // fold the heads: pair p of the row belongs to angle p % hd; each angle sums its block-local pairs in
+  // increasing order (no atomics, so dtheta is bitwise reproducible)
+  const int npairs = blockDim.x * (V / 2);
+  const int base = blockIdx.x * npairs;  // row pair index of this block's first pair
   double* dst = partial + ((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * hd;
-  for (int j = threadIdx.x; j < hd; j += blockDim.x) dst[j] = sdt[j];
+  for (int j = threadIdx.x; j < hd; j += blockDim.x) {
+    double sum = 0.0;
+    for (int lp = ((j - base) % hd + hd) % hd; lp < npairs; lp += hd) sum += sdt[lp];
+    dst[j] = sum;
+  }
 }
 
 __global__ void reduce_theta_kernel(const double* __restrict__ partial, int64_t nparts, int hd,
@@ -487,7 +489,7 @@ cudaError_t prologue_bwd_t(const GlaRows& g, const void* qp, const void* kp, con
                            const void* dk, void* dqp, void* dkp, double* partial, double* dtheta, cudaStream_t st) {
   const int vw = g.width / Vec<T>::N, hd = g.d / 2;
   const dim3 grid((unsigned)((vw + 255) / 256), (unsigned)((g.rows + kRowsPerBlock - 1) / kRowsPerBlock));
-  const size_t smem = theta != nullptr ? (size_t)hd * sizeof(double) : 0;
+  const size_t smem = theta != nullptr ? (size_t)256 * (Vec<T>::N / 2) * sizeof(double) : 0;
   prologue_bwd_kernel<T, Tacc><<<grid, 256, smem, st>>>(
       static_cast<const T*>(qp), static_cast<const T*>(kp), theta, static_cast<const T*>(dq),
       static_cast<const T*>(dk), static_cast<T*>(dqp), static_cast<T*>(dkp), partial, g.rows, g.n, g.width, g.d,

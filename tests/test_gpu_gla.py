@@ -146,3 +146,20 @@ def test_gla_epilogue_zero_rows_and_errors():
         ops.gla_prologue(a, a, 2, act="gelu")
     with pytest.raises(ShapeError):
         ops.gla_prologue(a, a, 2, theta=torch.ones(3))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32, torch.float64])
+def test_prologue_backward_is_bitwise_reproducible(dtype):
+    """dtheta sums over heads, rows and blocks in a fixed order (no atomics): repeated calls agree
+    bit for bit."""
+    from paper_2405_17381_b200 import ops
+    dev = torch.device("cuda", 0)
+    torch.manual_seed(5)
+    b, n, heads, d = 2, 777, 8, 64
+    qp, kp, dq, dk = (torch.randn(b, n, heads * d, device=dev, dtype=dtype) for _ in range(4))
+    theta = torch.rand(d // 2, dtype=torch.float64, device=dev)
+    runs = [ops.gla_prologue_backward(qp, kp, dq, dk, heads, theta=theta, offset=3) for _ in range(3)]
+    for r in runs[1:]:
+        for a, w in zip(r, runs[0]):
+            assert torch.equal(a, w)
