@@ -31,7 +31,7 @@ def _case(i):
     n = int(rng.choice([1, 3, 64, 127, 128, 129, 300, 513, 1000, 2048]))
     segments = int(rng.choice([0, 0, 1, 2, 3, 5]))
     layout = "bnhd" if rng.random() < 0.3 else "bhnd"
-    lams = [float(rng.choice([1.0, 0.999, 0.99, 0.9, 0.5])) for _ in range(h)]
+    lams = [float(rng.choice([1.0, 0.999, 0.99, 0.9, 0.5, 0.05, 5.5e-4])) for _ in range(h)]
     with_kv, with_dkv, saved = rng.random() < 0.5, rng.random() < 0.5, rng.random() < 0.5
     return dict(dtype=dtype, b=b, h=h, n=n, d=d, segments=segments, layout=layout, lams=lams, with_kv=with_kv,
                 with_dkv=with_dkv, saved=saved, seed=int(rng.integers(1 << 30)))
