@@ -147,6 +147,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const int p1 = min(args.n, p0 + args.seg_len);
   const int nchunks = p1 > p0 ? (p1 - p0 + C - 1) / C : 0;
   const int rev = args.rev;
+  auto chunk_row0 = [&](int t) { return p0 + (rev ? (nchunks - 1 - t) : t) * C; };
+  auto chunk_len = [&](int t) { return min(C, p1 - chunk_row0(t)); };
+  const int early = nchunks < NSTAGE ? nchunks : NSTAGE;  // chunks whose tiles thread 0 loads before the sync
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < NS; ++s) {
@@ -179,6 +182,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     tma_prefetch(&map_b);
     tma_prefetch(&map_c);
     tma_prefetch(&map_o);
+    // the first ring stages need no empty-slot wait: start their loads now, before the CTA-wide sync
+    // and the TMEM allocation, so the first tiles are in flight during the setup
+    for (int t = 0; t < early; ++t)
+      for (int x = 0; x < 3; ++x) {
+        const CUtensorMap* map = x == 0 ? &map_a : (x == 1 ? &map_b : &map_c);
+        mbar_arrive_expect_tx(&bars.full[x][t], TILE);
+        uint8_t* g = smem_gen + (t * 3 + x) * TILE;
+        tma_load_4d(map, &bars.full[x][t], g, 0, chunk_row0(t), hi, bi);
+        tma_load_4d(map, &bars.full[x][t], g + HALF, 64, chunk_row0(t), hi, bi);
+      }
   }
   if (warp == WARP_MMA) tmem_alloc(&bars.tmem_base, TM_COLS);
   tc_fence_before();
@@ -186,8 +199,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   tc_fence_after();
   const uint32_t tmem = bars.tmem_base;
 
-  auto chunk_row0 = [&](int t) { return p0 + (rev ? (nchunks - 1 - t) : t) * C; };
-  auto chunk_len = [&](int t) { return min(C, p1 - chunk_row0(t)); };
 
   if (warp == WARP_TMA) {
     // ------------------------------------------------------------ TMA producer
@@ -196,7 +207,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const int x = lane;
     if (x < 3) {
       const CUtensorMap* map = x == 0 ? &map_a : (x == 1 ? &map_b : &map_c);
-      for (int t = 0; t < nchunks; ++t) {
+      for (int t = early; t < nchunks; ++t) {
         const int s = t % NS;
         if (t >= NS) mbar_wait(&bars.empty[x][s], ((t / NS) - 1) & 1);
         const int r0 = chunk_row0(t);
