@@ -81,9 +81,19 @@ __global__ void __launch_bounds__(S_THREADS, 2)
     mbar_init(&bars.done, 1);
     fence_mbar_init();
   }
+  const int early = nchunks < SNST ? nchunks : SNST;  // ring stages loaded before the CTA-wide sync
   if (warp == 0 && lane == 0) {
     tma_prefetch(&map_b);
     tma_prefetch(&map_c);
+    for (int t = 0; t < early; ++t) {  // no empty-slot wait for the first stages
+      const int r0 = p0 + t * SC;
+      mbar_arrive_expect_tx(&bars.full[t], 2 * STILE);
+      uint8_t* gb = smem_gen + (size_t)t * 2 * STILE;
+      tma_load_4d(&map_b, &bars.full[t], gb, 0, r0, hi, bi);
+      tma_load_4d(&map_b, &bars.full[t], gb + SHALF, 64, r0, hi, bi);
+      tma_load_4d(&map_c, &bars.full[t], gb + STILE, 0, r0, hi, bi);
+      tma_load_4d(&map_c, &bars.full[t], gb + STILE + SHALF, 64, r0, hi, bi);
+    }
   }
   if (warp == 1) tmem_alloc(&bars.tmem_base, S_TM_COLS);
   tc_fence_before();
@@ -93,7 +103,7 @@ __global__ void __launch_bounds__(S_THREADS, 2)
 
   if (warp == 0) {
     if (lane == 0) {
-      for (int t = 0; t < nchunks; ++t) {
+      for (int t = early; t < nchunks; ++t) {
         const int s = t % SNST;
         if (t >= SNST) mbar_wait(&bars.empty[s], ((t / SNST) - 1) & 1);
         const int r0 = p0 + t * SC;
