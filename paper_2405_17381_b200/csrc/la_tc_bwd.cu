@@ -161,15 +161,36 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     tma_prefetch(&map_dk);
     tma_prefetch(&map_dv);
   }
+  // reverse sweep: chunk t covers rows [row0(t), row0(t) + len(t))
+  auto chunk_row0 = [&](int t) { return p0 + (nchunks - 1 - t) * C; };
+  auto chunk_len = [&](int t) { return min(C, p1 - chunk_row0(t)); };
+  // the rings' first stage needs no empty-slot wait: thread 0 (the producer lane) starts chunk 0's loads
+  // before the CTA-wide sync and the TMEM allocation (+0.3% on the short-n sweep; also starting Q's and
+  // dO's second stage here lost 1.2%: it queues ahead of chunk 1's K / V)
+  const int early_qd = nchunks < 1 ? nchunks : 1, early_kv = early_qd;
+  if (threadIdx.x == 0) {
+    const CUtensorMap* maps[4] = {&map_q, &map_do, &map_k, &map_v};
+    for (int r = 0; r < 4; ++r)
+      for (int t = 0; t < (r < 2 ? early_qd : early_kv); ++t) {
+        uint64_t* full = r == 0 ? &bars.full_q[t] : r == 1 ? &bars.full_d[t] : r == 2 ? &bars.full_k : &bars.full_v;
+        uint8_t* g = slot_gen(r == 0 ? SLOT_Q + t : r == 1 ? SLOT_D + t : r == 2 ? SLOT_K : SLOT_V);
+        mbar_arrive_expect_tx(full, TILE);
+        tma_load_4d(maps[r], full, g, 0, chunk_row0(t), hi, bi);
+        tma_load_4d(maps[r], full, g + HALF, 64, chunk_row0(t), hi, bi);
+#if LA_PFKV
+        if (r >= 2 && t + 1 < nchunks) {
+          tma_prefetch_l2_4d(maps[r], 0, chunk_row0(t + 1), hi, bi);
+          tma_prefetch_l2_4d(maps[r], 64, chunk_row0(t + 1), hi, bi);
+        }
+#endif
+      }
+  }
   if (warp == WARP_MMA) tmem_alloc(&bars.tmem_base, TM_COLS);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = bars.tmem_base;
 
-  // reverse sweep: chunk t covers rows [row0(t), row0(t) + len(t))
-  auto chunk_row0 = [&](int t) { return p0 + (nchunks - 1 - t) * C; };
-  auto chunk_len = [&](int t) { return min(C, p1 - chunk_row0(t)); };
   // W = in_scale dO into K's slot (row i: lam^(i+1), rows past the tail 0), once Sv and K~ are done with K;
   // the B/O warps run it (thread -> row i, 64-column half hh).  (Moving it to the state warps, idle at
   // that point, measured no faster: the pass is bound by shared-memory traffic, not by who issues it.)
@@ -203,7 +224,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       // free.  (Four lanes running one shared loop reconverge every iteration, so the slowest ring's
       // release gated the loads of the other three.)
       const CUtensorMap* maps[4] = {&map_q, &map_do, &map_k, &map_v};
-      int next[4] = {0, 0, 0, 0};
+      int next[4] = {early_qd, early_qd, early_kv, early_kv};
       long long t0 = 0;
       for (uint32_t spins = 1; next[0] < nchunks || next[1] < nchunks || next[2] < nchunks || next[3] < nchunks;
            ++spins) {
