@@ -71,6 +71,9 @@ constexpr int D = 128;           // head dim (only d == 128 on this backend)
 constexpr int TILE = C * D * 2;  // 32 KB bf16 tile
 constexpr int HALF = TILE / 2;   // [128 rows][64 cols] = 16 KB, one 128B-swizzle column block
 constexpr int NSTAGE = 2;
+#ifndef LA_EARLY_STAGES
+#define LA_EARLY_STAGES NSTAGE  // ring stages thread 0 loads before the CTA-wide sync
+#endif
 constexpr int WARP_TMA = 0, WARP_MMA = 1, WARP_P = 2, NUM_P = 8, WARP_O = 10, NUM_O = 8, WARP_KV = 18, NUM_KV = 8;
 constexpr int NUM_WARPS = WARP_KV + NUM_KV;
 constexpr int NUM_THREADS = NUM_WARPS * 32;
@@ -149,7 +152,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const int rev = args.rev;
   auto chunk_row0 = [&](int t) { return p0 + (rev ? (nchunks - 1 - t) : t) * C; };
   auto chunk_len = [&](int t) { return min(C, p1 - chunk_row0(t)); };
-  const int early = nchunks < NSTAGE ? nchunks : NSTAGE;  // chunks whose tiles thread 0 loads before the sync
+  const int early = nchunks < LA_EARLY_STAGES ? nchunks : LA_EARLY_STAGES;  // chunks thread 0 loads before the sync
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < NS; ++s) {
