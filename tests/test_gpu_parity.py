@@ -337,3 +337,25 @@ def test_long_ragged_segmented_sequences(n):
     (rdq, rdk, rdv), rdkv = orc.batched_backward(qq, kk, vv, dd, lams)
     for got, ref in ((o, ro), (kv_out, rkv), (dq, rdq), (dk, rdk), (dv, rdv), (dkv_out, rdkv)):
         assert orc.max_rel_error(host(got), ref) <= TOL[torch.bfloat16]
+
+
+def test_grid_limit_batch_heads():
+    """batch * heads at the grid limit (65535 (batch, head) rows of CTAs): sampled sequences match the
+    oracle; one more is refused with the unsupported status, not launched."""
+    b, h, n, d = 16383, 4, 3, 128
+    rng = np.random.default_rng(77)
+    q, k, v, do = (torch.as_tensor(rng.uniform(0.05, 1.0, (b, h, n, d)), dtype=torch.bfloat16, device="cuda")
+                   for _ in range(4))
+    lams = [0.9, 0.5, 1.0, 0.99]
+    o = ops.la_forward(q, k, v, lams)
+    dq, dk, dv = ops.la_backward(q, k, v, do, lams)
+    for bi in (0, 4097, b - 1):
+        sl = lambda t: host(t[bi:bi + 1])  # noqa: E731
+        ro, _ = orc.batched_forward(sl(q), sl(k), sl(v), lams)
+        (rdq, rdk, rdv), _ = orc.batched_backward(sl(q), sl(k), sl(v), sl(do), lams)
+        for got, ref in ((o, ro), (dq, rdq), (dk, rdk), (dv, rdv)):
+            assert orc.max_rel_error(sl(got), ref) <= TOL[torch.bfloat16]
+    from paper_2405_17381_b200._lib import UnsupportedError
+    q2 = torch.zeros(16384, 4, n, d, device="cuda", dtype=torch.bfloat16)
+    with pytest.raises(UnsupportedError):
+        ops.la_forward(q2, q2, q2, lams)
