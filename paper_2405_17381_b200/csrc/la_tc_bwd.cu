@@ -34,6 +34,9 @@ namespace {
 
 using namespace ptx;
 
+#ifndef LA_PFKV_DIST
+#define LA_PFKV_DIST 1  // chunks ahead
+#endif
 #ifndef LA_PFKV
 #define LA_PFKV 1  // L2 prefetch of the next K and V tiles (+1.2% on the bench sweep, same-box A/B)
 #endif
@@ -178,9 +181,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         tma_load_4d(maps[r], full, g, 0, chunk_row0(t), hi, bi);
         tma_load_4d(maps[r], full, g + HALF, 64, chunk_row0(t), hi, bi);
 #if LA_PFKV
-        if (r >= 2 && t + 1 < nchunks) {
-          tma_prefetch_l2_4d(maps[r], 0, chunk_row0(t + 1), hi, bi);
-          tma_prefetch_l2_4d(maps[r], 64, chunk_row0(t + 1), hi, bi);
+        for (int u = t + 1; r >= 2 && u <= t + LA_PFKV_DIST && u < nchunks; ++u) {
+          tma_prefetch_l2_4d(maps[r], 0, chunk_row0(u), hi, bi);
+          tma_prefetch_l2_4d(maps[r], 64, chunk_row0(u), hi, bi);
         }
 #endif
       }
@@ -247,9 +250,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #if LA_PFKV
           // K and V are single-slotted: their next tile can only be loaded once this chunk has consumed
           // the slot, so warm L2 with it now and the later load sees L2 latency, not DRAM latency
-          if (r >= 2 && t + 1 < nchunks) {
-            tma_prefetch_l2_4d(maps[r], 0, chunk_row0(t + 1), hi, bi);
-            tma_prefetch_l2_4d(maps[r], 64, chunk_row0(t + 1), hi, bi);
+          if (r >= 2 && t + LA_PFKV_DIST < nchunks) {
+            tma_prefetch_l2_4d(maps[r], 0, chunk_row0(t + LA_PFKV_DIST), hi, bi);
+            tma_prefetch_l2_4d(maps[r], 64, chunk_row0(t + LA_PFKV_DIST), hi, bi);
           }
 #endif
           next[r] = t + 1;
