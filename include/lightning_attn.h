@@ -31,7 +31,9 @@
  * Memory: every pointer is device memory; q,k,v,o,do,dq,dk,dv share the desc's
  * strides (element strides of batch, head, position; the feature stride is 1).
  * States are [batch, heads, d, d] row-major in the accumulation type (float for
- * LA_F32 / LA_BF16, double for LA_F64).  `lam` is a device array of `heads`
+ * LA_F32 / LA_BF16, double for LA_F64), 16-byte aligned (LA_ERR_SHAPE otherwise);
+ * the tensor-core path also needs 16-byte aligned operand bases and strides.
+ * `lam` is a device array of `heads`
  * doubles in (0, 1].  The caller allocates outputs and the workspace
  * (la_workspace_bytes); the library keeps no global state besides the
  * thread-local error string.  Calls are asynchronous on `stream` and reentrant.

@@ -11,6 +11,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <initializer_list>
 #include <string>
 
 #include <cuda.h>
@@ -230,6 +231,13 @@ cudaError_t side_stream(SideStream** out) {
   return cudaSuccess;
 }
 
+// The state buffers (d x d rows in the accumulation type) are read and written as 16-byte vectors.
+bool states_aligned(std::initializer_list<const void*> ptrs) {
+  for (const void* p : ptrs)
+    if (p != nullptr && (reinterpret_cast<uintptr_t>(p) & 15) != 0) return false;
+  return true;
+}
+
 struct Prepared {
   int backend;
   la::Plan plan;
@@ -302,6 +310,8 @@ int la_fwd(const la_desc* desc, const void* q, const void* k, const void* v, con
   int rc = prepare(desc, workspace_bytes, workspace, &pr);
   if (rc != LA_OK) return rc;
   if (!q || !k || !v || !o || !lam) return fail(LA_ERR_SHAPE, "la_fwd: null q/k/v/o/lam");
+  if (!states_aligned({kv_in, kv_out, seg_states_out}))
+    return fail(LA_ERR_SHAPE, "la_fwd: state buffers must be 16-byte aligned");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   bind_stream_context(st);
   la::PassDesc p = base_pass(desc, pr.plan, lam);
@@ -331,6 +341,8 @@ int la_bwd(const la_desc* desc, const void* q, const void* k, const void* v, con
   if (rc != LA_OK) return rc;
   if (!q || !k || !v || !dout || !dq || !dk || !dv || !lam)
     return fail(LA_ERR_SHAPE, "la_bwd: null q/k/v/do/dq/dk/dv/lam");
+  if (!states_aligned({kv_in, dkv_in, fwd_seg_states, dkv_out}))
+    return fail(LA_ERR_SHAPE, "la_bwd: state buffers must be 16-byte aligned");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   bind_stream_context(st);
   const la::PassDesc base = base_pass(desc, pr.plan, lam);
@@ -467,6 +479,7 @@ int la_decode(const la_desc* desc, const void* q, const void* k, const void* v, 
   if (desc->n != 1) return fail(LA_ERR_SHAPE, "la_decode advances one token per sequence: need n == 1, got n=%lld",
                                 (long long)desc->n);
   if (!q || !k || !v || !kv || !o || !lam) return fail(LA_ERR_SHAPE, "la_decode: null q/k/v/kv/o/lam");
+  if (!states_aligned({kv})) return fail(LA_ERR_SHAPE, "la_decode: kv must be 16-byte aligned");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   bind_stream_context(st);
   cudaError_t err = la::decode_launch(desc->dtype, (int)desc->batch, (int)desc->heads, (int)desc->d, desc->stride[0],

@@ -543,10 +543,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         float x[16];
         if (args.state_in != nullptr) {
           const float* src = args.state_in + (int64_t)bh * args.in_bh_stride + (int64_t)seg * args.in_seg_stride;
+          if (args.in_T) {
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const int col = hh * 64 + q4 * 16 + j;
-            x[j] = args.in_T ? src[col * D + i] : src[i * D + col];
+            for (int j = 0; j < 16; ++j) x[j] = src[(hh * 64 + q4 * 16 + j) * D + i];  // lanes: consecutive i
+          } else {
+            // row i, 16 consecutive columns: four 16-byte loads (the state buffers are 16-byte aligned)
+            const float4* s4 = reinterpret_cast<const float4*>(src + i * D + hh * 64 + q4 * 16);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const float4 w = s4[j];
+              x[4 * j] = w.x, x[4 * j + 1] = w.y, x[4 * j + 2] = w.z, x[4 * j + 3] = w.w;
+            }
           }
         } else {
 #pragma unroll

@@ -527,8 +527,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           if (args.state_in != nullptr) {
             const float* src = args.state_in + (int64_t)bh * args.in_bh_stride + (int64_t)seg * args.in_seg_stride +
                                (int64_t)i * D + hh * 64 + q4 * 16;
+            const float4* s4 = reinterpret_cast<const float4*>(src);  // 16-byte aligned state rows
 #pragma unroll
-            for (int j = 0; j < 16; ++j) x[j] = src[j];
+            for (int j = 0; j < 4; ++j) {
+              const float4 w = s4[j];
+              x[4 * j] = w.x, x[4 * j + 1] = w.y, x[4 * j + 2] = w.z, x[4 * j + 3] = w.w;
+            }
           } else {
 #pragma unroll
             for (int j = 0; j < 16; ++j) x[j] = 0.f;

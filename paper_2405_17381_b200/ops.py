@@ -140,7 +140,8 @@ def _state(t, g: Geometry, dtype, name):
         return None
     if t.shape != (g.batch, g.heads, g.d, g.d):
         raise ShapeError(f"{name}: expected shape {(g.batch, g.heads, g.d, g.d)}, got {tuple(t.shape)}")
-    return t.to(dtype=state_dtype(dtype)).contiguous()
+    t = t.to(dtype=state_dtype(dtype)).contiguous()
+    return t if t.data_ptr() % 16 == 0 else t.clone()  # the kernels read state rows as 16-byte vectors
 
 
 def _workspace(lib, desc, device):

@@ -359,3 +359,30 @@ def test_grid_limit_batch_heads():
     q2 = torch.zeros(16384, 4, n, d, device="cuda", dtype=torch.bfloat16)
     with pytest.raises(UnsupportedError):
         ops.la_forward(q2, q2, q2, lams)
+
+
+def test_misaligned_states_rejected_by_the_abi_and_realigned_by_ops():
+    """The C ABI refuses state buffers that are not 16-byte aligned (the kernels read them as 16-byte
+    vectors); the Python layer copies such a state instead of passing it through."""
+    import ctypes
+    from paper_2405_17381_b200 import _lib
+    b, h, n, d = 1, 2, 256, 128
+    q, k, v = (torch.rand(b, h, n, d, device="cuda", dtype=torch.bfloat16) for _ in range(3))
+    buf = torch.zeros(b * h * d * d + 1, device="cuda")
+    kv_off = buf[1:].view(b, h, d, d)  # 4 bytes past an aligned base
+    assert kv_off.data_ptr() % 16 == 4
+    lib = _lib.load()
+    desc = ops._desc(ops._geometry(q, "bhnd"), q.dtype, None, "auto", 0)
+    lam = ops.decay_tensor([0.9, 0.5], h, q.device)
+    o = torch.empty_like(q)
+    ws, nbytes = ops._workspace(lib, desc, q.device)
+    rc = lib.la_fwd(ctypes.byref(desc), ctypes.c_void_p(q.data_ptr()), ctypes.c_void_p(k.data_ptr()),
+                    ctypes.c_void_p(v.data_ptr()), ctypes.cast(ctypes.c_void_p(lam.data_ptr()),
+                                                                ctypes.POINTER(ctypes.c_double)),
+                    ctypes.c_void_p(kv_off.data_ptr()), ctypes.c_void_p(o.data_ptr()), None, None,
+                    ctypes.c_void_p(ws.data_ptr()), nbytes, ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+    assert rc == _lib.LA_ERR_SHAPE and b"aligned" in lib.la_last_error()
+    kv_ok = kv_off.clone()
+    kv_off.copy_(torch.rand_like(kv_off) * 0.05)
+    kv_ok.copy_(kv_off)
+    assert torch.equal(ops.la_forward(q, k, v, [0.9, 0.5], kv_in=kv_off), ops.la_forward(q, k, v, [0.9, 0.5], kv_in=kv_ok))
