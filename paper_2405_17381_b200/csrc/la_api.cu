@@ -231,7 +231,7 @@ cudaError_t side_stream(SideStream** out) {
   return cudaSuccess;
 }
 
-// The state buffers (d x d rows in the accumulation type) are read and written as 16-byte vectors.
+// State buffers (d x d rows in the accumulation type) and GLA rows are read and written as 16-byte vectors.
 bool states_aligned(std::initializer_list<const void*> ptrs) {
   for (const void* p : ptrs)
     if (p != nullptr && (reinterpret_cast<uintptr_t>(p) & 15) != 0) return false;
@@ -526,6 +526,7 @@ int la_gla_prologue(const la_gla_desc* desc, const void* qp, const void* kp, con
   int rc = gla_prepare(desc, theta != nullptr, &g);
   if (rc != LA_OK) return rc;
   if (!qp || !kp || !q || !k) return fail(LA_ERR_SHAPE, "la_gla_prologue: null qp/kp/q/k");
+  if (!states_aligned({qp, kp, q, k})) return fail(LA_ERR_SHAPE, "la_gla_prologue: rows must be 16-byte aligned");
   if (g.width % 2) return fail(LA_ERR_SHAPE, "la_gla_prologue: heads * d must be even");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   bind_stream_context(st);
@@ -540,6 +541,8 @@ int la_gla_prologue_bwd(const la_gla_desc* desc, const void* qp, const void* kp,
   int rc = gla_prepare(desc, theta != nullptr, &g);
   if (rc != LA_OK) return rc;
   if (!qp || !kp || !dq || !dk || !dqp || !dkp) return fail(LA_ERR_SHAPE, "la_gla_prologue_bwd: null operand");
+  if (!states_aligned({qp, kp, dq, dk, dqp, dkp}))
+    return fail(LA_ERR_SHAPE, "la_gla_prologue_bwd: rows must be 16-byte aligned");
   if (g.width % 2) return fail(LA_ERR_SHAPE, "la_gla_prologue_bwd: heads * d must be even");
   if (theta != nullptr) {
     if (dtheta == nullptr) return fail(LA_ERR_SHAPE, "la_gla_prologue_bwd: theta given without dtheta");
@@ -558,6 +561,7 @@ int la_gla_epilogue(const la_gla_desc* desc, const void* a, const void* u, void*
   int rc = gla_prepare(desc, false, &g);
   if (rc != LA_OK) return rc;
   if (!a || !gated || !rawnorm) return fail(LA_ERR_SHAPE, "la_gla_epilogue: null a/gated/rawnorm");
+  if (!states_aligned({a, u, gated})) return fail(LA_ERR_SHAPE, "la_gla_epilogue: rows must be 16-byte aligned");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   bind_stream_context(st);
   cudaError_t err = la::gla_epilogue(g, a, u, gated, rawnorm, desc->eps, st);
@@ -571,6 +575,8 @@ int la_gla_epilogue_bwd(const la_gla_desc* desc, const void* dgated, const void*
   if (rc != LA_OK) return rc;
   if (!dgated || !a || !rawnorm || !da || (u != nullptr && du == nullptr))
     return fail(LA_ERR_SHAPE, "la_gla_epilogue_bwd: null operand");
+  if (!states_aligned({dgated, a, u, da, du}))
+    return fail(LA_ERR_SHAPE, "la_gla_epilogue_bwd: rows must be 16-byte aligned");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   bind_stream_context(st);
   cudaError_t err = la::gla_epilogue_bwd(g, dgated, a, u, rawnorm, da, du, desc->eps, st);
@@ -583,6 +589,7 @@ int la_gla_gate_rowsq(const la_gla_desc* desc, const void* a, const void* u, voi
   int rc = gla_prepare(desc, false, &g);
   if (rc != LA_OK) return rc;
   if (!a || !gated || !rowsq || rowsq_stride < 1) return fail(LA_ERR_SHAPE, "la_gla_gate_rowsq: null operand / bad stride");
+  if (!states_aligned({a, u, gated})) return fail(LA_ERR_SHAPE, "la_gla_gate_rowsq: rows must be 16-byte aligned");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   bind_stream_context(st);
   cudaError_t err = la::gla_gate_rowsq(g, a, u, gated, rowsq, rowsq_stride, st);

@@ -333,7 +333,8 @@ def _rows(tensors, names):
         if t.shape != first.shape or t.dtype != first.dtype or t.device != first.device:
             raise ShapeError(f"{name}: shape/dtype/device {tuple(t.shape)}/{t.dtype}/{t.device} do not match "
                              f"{tuple(first.shape)}/{first.dtype}/{first.device}")
-        out.append(t.contiguous())
+        t = t.contiguous()
+        out.append(t if t.data_ptr() % 16 == 0 else t.clone())  # the stages move 16-byte vectors
     return out
 
 
