@@ -2,6 +2,10 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
+``--gpus N`` (N > 1) without a torchrun environment re-launches itself under
+``torch.distributed.run`` with N ranks on this node (127.0.0.1 rendezvous) and fails loudly
+when fewer than N CUDA devices are visible; under torchrun WORLD_SIZE must equal N.
+
 Workload (BASELINE.json configs[2], the metric's own config): the TNL-1B
 attention core -- H=16 heads, d=128, bf16 operands with fp32 accumulation,
 per-head decay lam_h = decay_rate(h, l=1, H=16, L=16) -- at a FIXED 64K tokens
@@ -16,10 +20,22 @@ ranks); the per-n curve is in ``sweep``.  Under torchrun (N > 1) every rank
 runs the same per-GPU workload on its own batch x head shard (no collective:
 heads and batch are independent), so scaling is weak.
 
-``--impl reference`` times the reference's own CPU algorithm (the oracle's
-restatement of kernels.py:253-334, numpy/OpenBLAS, fp32 "working") on the
-host cores with one process per core, on a bounded sample of the same
-workload, and prints the same line with ``"impl": "reference"``.
+Beside the headline line's sweep, ``multi`` carries the two multi-GPU configurations, run by every
+rank and timed as the max over ranks:
+  * ``tnl7b_heads`` (BASELINE configs[3]): TNL-7B attention, 32 heads sharded 32 / N per rank, no
+    collective, 64K tokens per batch at n = 2K / 8K / 32K -- strong scaling (fixed layer work);
+  * ``sequence_parallel`` (configs[4]): TNL-1B attention at 512K and 1M tokens (batch 1), each
+    sequence split over the N ranks through ``sp.sp_lightning_attention`` (all_gather exchange of the
+    d x d summaries, NCCL) -- strong scaling; plus the same sequence on one GPU for the efficiency.
+
+``--impl reference`` times the reference's own CPU implementation -- the stock
+``linattn.kernels.lightning_forward_decay`` / ``lightning_backward_decay``
+(kernels.py:253-334, precision "working" = fp32, its _prep and ensure_finite
+included) installed unmodified in ``baseline/_ref`` -- on the host cores with one
+process per core (threadpool_limits(1), the reference's own policy, bench.py:36,57),
+each step one sequence at every n of the sweep x all 16 heads, and prints the
+same line with ``"impl": "reference"``.  Without ``baseline/_ref`` it falls back
+to the oracle's restatement of the same algorithm (kind "port").
 """
 
 from __future__ import annotations
@@ -63,6 +79,70 @@ def lams() -> list[float]:
 
 def dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def head_shard(rank: int, world: int, heads: int) -> tuple[int, int]:
+    """Contiguous head range [lo, hi) of `rank` (batch x head sharding, no collective: SPEC.md:256)."""
+    return rank * heads // world, (rank + 1) * heads // world
+
+
+def sp_slice(n_total: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous position range [lo, hi) of `rank` in sequence-parallel mode, 128-row (chunk) aligned."""
+    chunks = (n_total + 127) // 128
+    lo, hi = rank * chunks // world, (rank + 1) * chunks // world
+    return min(n_total, lo * 128), min(n_total, hi * 128)
+
+
+def _free_port() -> int:
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def maybe_relaunch(args) -> None:
+    """``--gpus N`` outside torchrun: re-exec under torch.distributed.run with N ranks on this node."""
+    if "WORLD_SIZE" in os.environ:
+        if int(os.environ["WORLD_SIZE"]) != args.gpus:
+            sys.exit(f"bench.py: --gpus {args.gpus} but the launcher started WORLD_SIZE={os.environ['WORLD_SIZE']}")
+        return
+    if args.gpus <= 1 or args.impl == "reference":  # the reference arm is host-only: rank 0's work, no ranks
+        return
+    if os.environ.get("LA_BENCH_LAUNCH_PROBE") != "1":
+        import torch
+
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            sys.exit(f"bench.py: --gpus {args.gpus} requested but only {have} CUDA device(s) are visible")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", str(Path(__file__).resolve()), *sys.argv[1:]]
+    sys.stdout.flush()
+    os.execv(sys.executable, cmd)
+
+
+def launch_probe(args) -> None:
+    """LA_BENCH_LAUNCH_PROBE=1 (CPU tests): the multi-rank plumbing without GPU work -- rendezvous, the
+    shard plans of every rank, and the max-over-ranks reduction -- printed by rank 0 as one JSON line."""
+    import torch
+    import torch.distributed as dist
+
+    rank, world, _ = dist_env()
+    if world > 1:
+        dist.init_process_group("gloo")
+    mine = torch.tensor([float(rank + 1)], dtype=torch.float64)  # a rank-dependent "time"
+    plan = torch.tensor([*head_shard(rank, world, 32), *sp_slice(1 << 20, rank, world)], dtype=torch.int64)
+    plans = [torch.zeros_like(plan) for _ in range(world)]
+    if world > 1:
+        dist.all_reduce(mine, op=dist.ReduceOp.MAX)
+        dist.all_gather(plans, plan)
+    else:
+        plans = [plan]
+    if rank == 0:
+        print(json.dumps({"probe": True, "world": world, "gpus": args.gpus, "max_over_ranks": float(mine.item()),
+                          "tnl7b_heads": [p[:2].tolist() for p in plans], "sp_slices": [p[2:].tolist() for p in plans]}))
+    if world > 1:
+        dist.destroy_process_group()
 
 
 # ----------------------------------------------------------------------------
@@ -195,15 +275,24 @@ def run_ours(args) -> None:
     launches = sum(ops.launch_count(tuple(inputs[n][0].shape), which="fwd")
                    + ops.launch_count(tuple(inputs[n][0].shape), which="bwd_saved") for n in seq_lens) * args.steps
 
+    def reduce_max(ms: float) -> float:
+        if world == 1:
+            return ms
+        t = torch.tensor([ms], device=device, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
     e2e = None if args.no_e2e else run_e2e(ops, seq_lens, tokens, lam_dev, device, min(args.steps, args.e2e_steps),
-                                           world)
+                                           world, reduce_max)
+    del inputs
+    torch.cuda.empty_cache()
+    multi = None if args.no_multi else run_multi(ops, device, world, rank, stream, pk, reduce_max,
+                                                 max(1, min(args.steps, args.multi_steps)))
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
         return
-    cpu = cpu_baseline(args.cpu_seconds) if (world == 1 and not args.no_cpu) else None
-    del inputs
-    torch.cuda.empty_cache()
+    cpu = cpu_baseline() if (world == 1 and not args.no_cpu) else None
     rows = None if args.no_rows else measure_rows(ops, device, stream, pk)
     flat = sweep[str(seq_lens[-1])]["tokens_per_s"] / sweep[str(seq_lens[0])]["tokens_per_s"]
     line = {
@@ -222,6 +311,7 @@ def run_ours(args) -> None:
         "roofline": roof,
         "gpu_launches": launches,
         "e2e": e2e,
+        "multi": multi,
         "clocks": clock,
         "cpu_baseline": cpu,
         "rows": rows,
@@ -374,17 +464,21 @@ def pass_roofline(ops, tensors, lam_dev, stream, pk) -> dict:
     head_tokens = q.shape[0] * q.shape[1] * q.shape[2]
     algo = head_tokens * PASS_BYTES_PER_HEAD_TOKEN
     achieved = algo / (ms / 1e3) / 1e9
-    traffic = None
+    # DRAM bytes of this launch are not measurable in-process (no CUPTI here): they come from the ncu
+    # --set full capture of the same launch committed under profiles/, named in traffic_source
+    traffic, source = None, None
     prof = ROOT / "profiles" / "traffic.json"
     if prof.exists():
-        traffic = json.loads(prof.read_text()).get("pass_dram_bytes_per_launch")
+        tj = json.loads(prof.read_text())
+        traffic = tj.get("pass_dram_bytes_per_launch")
+        source = tj.get("source", "profiles/traffic.json")
     return {"kernel": "la pass (one la_fwd: q,k,v -> o)", "bound": "hbm", "achieved": round(achieved, 1),
             "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": round(achieved / pk["hbm_gbs"], 4),
-            "traffic": traffic, "algorithmic_bytes": algo, "launch_ms": round(ms, 4),
+            "traffic": traffic, "traffic_source": source, "algorithmic_bytes": algo, "launch_ms": round(ms, 4),
             "shape": list(q.shape), "peak_source": pk["source"]}
 
 
-def run_e2e(ops, seq_lens, tokens, lam_dev, device, steps, world, pieces=4) -> dict:
+def run_e2e(ops, seq_lens, tokens, lam_dev, device, steps, world, reduce_max, pieces=4) -> dict:
     """Same metric through the public API with pinned HOST buffers, H2D + D2H inside the timed region.
 
     Each n's batch is cut into ``pieces`` independent (batch or head) slices, pipelined over three
@@ -448,27 +542,150 @@ def run_e2e(ops, seq_lens, tokens, lam_dev, device, steps, world, pieces=4) -> d
     comp.wait_stream(d2h_s)
     b.record(comp)
     torch.cuda.synchronize()
-    ms = a.elapsed_time(b)
+    ms = reduce_max(a.elapsed_time(b))
     value = sum(tokens.values()) * steps * world / (ms / 1e3)
     return {"value": round(value), "unit": UNIT, "h2d_bytes_per_step": h2d // steps, "d2h_bytes_per_step": d2h // steps,
             "steps": steps, "path": "ops.la_forward/la_backward (C ABI) from pinned host buffers, "
                                     f"{pieces} slices per n pipelined over H2D / compute / D2H streams"}
 
 
+def run_multi(ops, device, world, rank, stream, pk, reduce_max, steps) -> dict:
+    """BASELINE configs[3] (TNL-7B heads sharded over the ranks) and configs[4] (TNL-1B sequence parallel at
+    512K / 1M tokens) -- every rank runs its share; device time (CUDA events) as the max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2405_17381_b200 import sp
+    from paper_2405_17381_b200.positional import decay_rate
+
+    g = torch.Generator(device=device).manual_seed(4321 + rank)
+    rnd = lambda *shape: (torch.randn(*shape, device=device, generator=g) / D ** 0.5).to(torch.bfloat16)  # noqa: E731
+
+    def timed(fn) -> float:
+        fn()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(steps):
+            fn()
+        b.record(stream)
+        torch.cuda.synchronize()
+        return reduce_max(a.elapsed_time(b) / steps)
+
+    out = {}
+    # configs[3]: TNL-7B attention (H = 32, d = 128, L = 30), heads sharded 32 / N, 64K tokens per batch
+    h7 = 32
+    lo, hi = head_shard(rank, world, h7)
+    lam7 = ops.decay_tensor([decay_rate(h, 1, h7, 30) for h in range(lo + 1, hi + 1)], hi - lo, device)
+    rows7 = {}
+    for n in (2048, 8192, 32768):
+        b = TOKENS // n
+        q, k, v, do = (rnd(b, hi - lo, n, D) for _ in range(4))
+
+        def fb():
+            _, seg = ops.la_forward(q, k, v, None, lam_dev=lam7, want_seg_states=True)
+            ops.la_backward(q, k, v, do, None, lam_dev=lam7, fwd_seg_states=seg)
+
+        ms = timed(fb)
+        tok = TOKENS / (ms / 1e3)
+        rows7[str(n)] = {"batch": b, "heads_per_rank": hi - lo, "ms_fwd_bwd": round(ms, 4), "tokens_per_s": round(tok),
+                         "tokens_per_s_per_gpu": round(tok / world),
+                         "pct_bf16_peak": round(100 * tok * h7 * FLOPS_PER_HEAD_TOKEN
+                                                / (world * pk["bf16_tflops"] * 1e12), 2)}
+        del q, k, v, do
+    out["tnl7b_heads"] = {"workload": "BASELINE configs[3]: TNL-7B attention, H=32, d=128, bf16, fwd+bwd, 64K tokens "
+                                      "per batch, heads sharded over the ranks (no collective); strong scaling",
+                          "n_gpus": world, "rows": rows7}
+    # configs[4]: TNL-1B attention, one sequence of 512K / 1M tokens split over the ranks
+    lam_sp = ops.decay_tensor(lams(), H, device)
+    group = dist.group.WORLD if world > 1 else None
+    rows_sp = {}
+    for n_total in (524288, 1048576):
+        plo, phi = sp_slice(n_total, rank, world)
+        lengths = [sp_slice(n_total, r, world)[1] - sp_slice(n_total, r, world)[0] for r in range(world)]
+        q, k, v, do = (rnd(1, H, phi - plo, D) for _ in range(4))
+        leaves = [t.requires_grad_(True) for t in (q, k, v)]
+
+        def fb_sp():
+            o = sp.sp_lightning_attention(*leaves, lam_sp, group, lengths=lengths)
+            torch.autograd.grad(o, leaves, do)
+
+        ms = timed(fb_sp)
+        row = {"n_per_rank": phi - plo, "ms_fwd_bwd": round(ms, 4), "tokens_per_s": round(n_total / (ms / 1e3)),
+               "pct_bf16_peak": round(100 * n_total / (ms / 1e3) * H * FLOPS_PER_HEAD_TOKEN
+                                      / (world * pk["bf16_tflops"] * 1e12), 2)}
+        del q, k, v, do, leaves
+        torch.cuda.empty_cache()
+        # the same sequence on one GPU (rank 0), through the plain entry points: the efficiency baseline
+        if rank == 0:
+            q1, k1, v1, d1 = (rnd(1, H, n_total, D) for _ in range(4))
+
+            def fb_one():
+                _, seg = ops.la_forward(q1, k1, v1, None, lam_dev=lam_sp, want_seg_states=True)
+                ops.la_backward(q1, k1, v1, d1, None, lam_dev=lam_sp, fwd_seg_states=seg)
+
+            fb_one()
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for _ in range(steps):
+                fb_one()
+            b.record(stream)
+            torch.cuda.synchronize()
+            one = a.elapsed_time(b) / steps
+            row["single_gpu_ms"] = round(one, 4)
+            row["single_gpu_tokens_per_s"] = round(n_total / (one / 1e3))
+            row["parallel_efficiency"] = round(one / (world * ms), 3)
+            del q1, k1, v1, d1
+            torch.cuda.empty_cache()
+        if world > 1:
+            dist.barrier()
+        rows_sp[str(n_total)] = row
+    out["sequence_parallel"] = {"workload": "BASELINE configs[4]: TNL-1B attention (H=16, d=128, bf16), batch 1, "
+                                            "fwd+bwd, the sequence split over the ranks (sp.sp_lightning_attention, "
+                                            "all_gather of the d x d summaries over NCCL); strong scaling",
+                                "n_gpus": world, "exchange": "gather", "rows": rows_sp}
+    return out
+
+
 # ----------------------------------------------------------------------------
-# CPU baseline / reference arm: the reference's tiled algorithm on host cores
+# CPU baseline / reference arm: the reference's own implementation on host cores
 # ----------------------------------------------------------------------------
+
+REF_DIR = ROOT / "baseline" / "_ref"
+
+
+def _ref_init():
+    if (REF_DIR / "linattn").is_dir() and str(REF_DIR) not in sys.path:
+        sys.path.insert(0, str(REF_DIR))
+
+
+def _ref_kind() -> str:
+    return "reference" if (REF_DIR / "linattn" / "kernels.py").exists() else "port"
 
 
 def _cpu_unit(args):
+    """One (sequence, head) unit, fwd + bwd in fp32 ("working"), timed; inputs made outside the timing."""
     n, d, lam, seed = args
     from threadpoolctl import threadpool_limits
 
-    from oracle import linattn_oracle as orc  # the reference's algorithm, restated (CPU baseline only)
-
     rng = np.random.default_rng(seed)
-    q, k, v, do = (rng.standard_normal((n, d)).astype(np.float32) / np.sqrt(d) for _ in range(4))
+    q, k, v, do = (rng.standard_normal((n, d)).astype(np.float32) / np.float32(np.sqrt(d)) for _ in range(4))
     with threadpool_limits(limits=1):  # the reference's own policy (bench.py:36,57)
+        if _ref_kind() == "reference":
+            # the stock reference, unmodified (baseline/_ref/linattn): its _prep, ensure_finite, tiled sweeps
+            from linattn.kernels import AttentionConfig, lightning_backward_decay, lightning_forward_decay
+
+            cfg = AttentionConfig(n=n, d=d, B=None, lam=lam, precision="working")
+            t0 = time.perf_counter()
+            lightning_forward_decay(q, k, v, cfg)
+            lightning_backward_decay(q, k, v, do, cfg)
+            return time.perf_counter() - t0
+        from oracle import linattn_oracle as orc  # restatement of the same algorithm (CPU baseline only)
+
         t0 = time.perf_counter()
         orc.tiled_forward(q, k, v, lam, d, dtype=np.float32)
         orc.tiled_backward(q, k, v, do, lam, d, dtype=np.float32)
@@ -482,11 +699,13 @@ class CpuPool:
         from concurrent.futures import ProcessPoolExecutor
 
         self.cores = cores
-        self.ex = ProcessPoolExecutor(max_workers=cores)
+        self.ex = ProcessPoolExecutor(max_workers=cores, initializer=_ref_init)
         self.lam = lams()
 
-    def run(self, n_units: int, n: int) -> float:
-        jobs = [(n, D, self.lam[i % H], i) for i in range(n_units)]
+    def run_sweep(self, heads) -> float:
+        """One sequence at every n of the sweep x the given heads; the longest units first."""
+        jobs = sorted(((n, D, self.lam[h], 1000 * h + i) for i, n in enumerate(SEQ_LENS) for h in heads),
+                      key=lambda j: -j[0])
         t0 = time.perf_counter()
         list(self.ex.map(_cpu_unit, jobs, chunksize=1))
         return time.perf_counter() - t0
@@ -495,24 +714,35 @@ class CpuPool:
         self.ex.shutdown()
 
 
-CPU_N = 8192
+SWEEP_TOKENS = sum(SEQ_LENS)  # one sequence at every n: 261,120 layer tokens
 
 
-def cpu_baseline(budget_s: float) -> dict:
+def _sample_heads(pool, budget_s: float):
+    """All 16 heads per n unless one sweep would exceed `budget_s` on these cores; then every other head
+    (the decays still span 0.63 .. 5.5e-4).  Returns (heads, warm-up wall)."""
+    heads = list(range(H))
+    wall = pool.run_sweep(heads)
+    if wall > budget_s:
+        heads = list(range(0, H, 2))
+    return heads, wall
+
+
+def cpu_baseline() -> dict:
     """Bounded sample of the workload on the host cores, reported beside the GPU number."""
     cores = len(os.sched_getaffinity(0))
+    _ref_init()
     pool = CpuPool(cores)
     try:
-        for _ in range(2):
-            first = pool.run(H, CPU_N)  # warm every worker
-        units = H * max(1, int((budget_s / 3) / max(first, 1e-3)))
-        walls = [pool.run(units, CPU_N) for _ in range(3)]
+        heads, _ = _sample_heads(pool, 12.0)
+        wall = pool.run_sweep(heads)
     finally:
         pool.close()
-    wall = statistics.median(walls)
-    return {"value": round(units * CPU_N / wall / H, 1), "unit": UNIT, "cores": cores, "kind": "port",
-            "sample": f"{units} (batch,head) units of n={CPU_N}, d={D}, fp32 fwd+bwd, median of 3; one process per "
-                      "core x 1 BLAS thread; tokens/s = head-tokens/s / H (layer tokens)",
+    value = SWEEP_TOKENS * len(heads) / H / wall
+    return {"value": round(value, 1), "unit": UNIT, "cores": cores, "kind": _ref_kind(),
+            "sample": f"one sequence at every n of the sweep (1K..128K) x {len(heads)} of the {H} heads, fwd+bwd, "
+                      "fp32 'working' precision, one timed sweep after a warm one; one process per core x 1 BLAS "
+                      f"thread; tokens/s = layer tokens (head-tokens / {H})",
+            "impl": "baseline/_ref linattn.kernels (stock)" if _ref_kind() == "reference" else "oracle port",
             "wall_s": round(wall, 3)}
 
 
@@ -521,30 +751,28 @@ def run_reference(args) -> None:
     if rank != 0:
         return
     cores = len(os.sched_getaffinity(0))
+    _ref_init()
     pool = CpuPool(cores)
-    # one step = the sweep's n = 8192 batch (8 sequences x 16 heads = 128 units), handed out one unit at a
-    # time so the strongly decaying heads (subnormal-heavy on the CPU) do not leave cores idle
-    units = (TOKENS // CPU_N) * H
     try:
-        for _ in range(args.warmup):
-            pool.run(units, CPU_N)
-        walls = [pool.run(units, CPU_N) for _ in range(args.steps)]
+        heads, _ = _sample_heads(pool, 9.0)  # keeps --steps 20 --warmup 5 within a few minutes
+        for _ in range(max(0, args.warmup - 1)):
+            pool.run_sweep(heads)
+        walls = [pool.run_sweep(heads) for _ in range(args.steps)]
     finally:
         pool.close()
     total = sum(walls)
-    value = units * CPU_N * len(walls) / total / H
+    value = SWEEP_TOKENS * len(heads) / H * len(walls) / total
+    sample = (f"per step: one sequence at every n of the sweep (1K..128K) x {len(heads)} of the {H} heads (TNL-1B "
+              f"decays), fwd+bwd, fp32 'working'; {cores} processes x 1 BLAS thread")
     line = {
         "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(1e3 * total / len(walls), 2), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic", "impl": "reference",
-        "config": {"workload": "TNL-1B attention core (BASELINE configs[2]) on host cores: H=16, d=128; step = the "
-                               f"sweep's n={CPU_N} batch ({TOKENS // CPU_N} sequences x {H} heads), fwd+bwd, over "
-                               f"{cores} processes",
-                   "heads": H, "head_dim": D, "seq_len": CPU_N, "batch": TOKENS // CPU_N,
+        "config": {"workload": "TNL-1B attention core (BASELINE configs[2]) on host cores: H=16, d=128, "
+                               "lam=decay_rate(h, 1, 16, 16), fwd+bwd at every n of the 1K..128K sweep (batch 1 per n)",
+                   "heads": H, "heads_sampled": len(heads), "head_dim": D, "seq_lens": list(SEQ_LENS),
                    "parallelism": f"{cores} processes x 1 BLAS thread"},
-        "cpu_baseline": {"value": round(value, 1), "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"{units} (batch, head) units of n={CPU_N} per step; reference tiled algorithm "
-                                   "(oracle restatement of kernels.py:253-334), numpy/OpenBLAS fp32"},
+        "cpu_baseline": {"value": round(value, 1), "unit": UNIT, "cores": cores, "kind": _ref_kind(), "sample": sample},
         "e2e": {"value": round(value, 1), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
@@ -559,16 +787,22 @@ def main() -> None:
     ap.add_argument("--seq-lens", type=lambda s: [int(x) for x in s.split(",")], default=list(SEQ_LENS))
     ap.add_argument("--roofline-n", type=int, default=8192)
     ap.add_argument("--e2e-steps", type=int, default=2)
-    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--multi-steps", type=int, default=5)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-multi", action="store_true", help="skip the TNL-7B head-shard and sequence-parallel rows")
     ap.add_argument("--no-rows", action="store_true", help="skip the decode / GLA-stage / GLA-layer measurements")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
+    if args.gpus < 1:
+        ap.error("--gpus must be >= 1")
     if args.roofline_n not in args.seq_lens:
         args.roofline_n = args.seq_lens[len(args.seq_lens) // 2]
-    if args.impl == "reference":
+    maybe_relaunch(args)
+    if os.environ.get("LA_BENCH_LAUNCH_PROBE") == "1":
+        launch_probe(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_ours(args)

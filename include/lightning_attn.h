@@ -28,13 +28,17 @@
  *   The block size B is validated (>= 1) and otherwise semantically inert, exactly
  *   as in the reference: the kernels choose their own tile.
  *
- * Memory: every pointer is device memory; q,k,v,o,do,dq,dk,dv share the desc's
- * strides (element strides of batch, head, position; the feature stride is 1).
+ * Memory: every pointer is device memory; q,k,v,o,do,dq,dk,dv use the desc's
+ * strides (element strides of batch, head, position; the feature stride is 1),
+ * or each its own through la_fwd_ex / la_bwd_ex's la_tensor_strides.
  * States are [batch, heads, d, d] row-major in the accumulation type (float for
  * LA_F32 / LA_BF16, double for LA_F64), 16-byte aligned (LA_ERR_SHAPE otherwise);
  * the tensor-core path also needs 16-byte aligned operand bases and strides.
  * `lam` is a device array of `heads`
- * doubles in (0, 1].  The caller allocates outputs and the workspace
+ * doubles in (0, 1]; a value outside (0, 1] (or NaN) turns every output of the call into NaN
+ * (the reference raises DomainError, matrixops.py:72-77; the ABI does not read lam back per call
+ * -- la_check_decay validates a host copy, LA_FLAG_CHECK_DECAY the device one, as LA_ERR_DOMAIN).
+ * The caller allocates outputs and the workspace
  * (la_workspace_bytes); the library keeps no global state besides the
  * thread-local error string.  Calls are asynchronous on `stream` and reentrant.
  */
@@ -48,7 +52,7 @@
 extern "C" {
 #endif
 
-#define LA_ABI_VERSION 2
+#define LA_ABI_VERSION 3
 
 #if defined(__GNUC__)
 #define LA_API __attribute__((visibility("default")))
@@ -114,6 +118,54 @@ LA_API int la_bwd(const la_desc* desc, const void* q, const void* k, const void*
            const void* dkv_in, const void* fwd_seg_states, void* dq, void* dk,
            void* dv, void* dkv_out, void* workspace, size_t workspace_bytes,
            void* stream);
+
+/* ---- extended entry points (ABI 3) --------------------------------------------------------
+ * la_fwd_ex / la_bwd_ex are la_fwd / la_bwd with per-tensor strides and flags:
+ *   strides  nullable; else every operand's own (batch, head, position) element strides, indexed by
+ *            la_operand (la_fwd_ex reads Q, K, V, O; la_bwd_ex Q, K, V, DO, DQ, DK, DV), so q, k, v
+ *            of different layouts (e.g. views into a fused projection) need no copy.
+ *   flags    LA_FLAG_RESUME: the workspace already holds this problem's segment summaries, left by
+ *              la_fwd_state(desc, k, v, lam, ws) (la_fwd_ex) or la_bwd_state(desc, q, do, lam, ws)
+ *              (la_bwd_ex, sweep 2) on the same stream -- the summary pass is skipped: a sequence-
+ *              parallel rank's own summary (which it computes for the exchange anyway) already holds
+ *              the summaries of its segments.
+ *              la_bwd_ex with LA_FLAG_RESUME and a split sequence needs fwd_seg_states for sweep 1.
+ *            LA_FLAG_CHECK_DECAY: read lam back and validate (0, 1] -> LA_ERR_DOMAIN (synchronises
+ *              the stream; debug / first-call validation).
+ *            LA_FLAG_CHECK_FINITE: scan the inputs for NaN / Inf -> LA_ERR_DOMAIN, the reference's
+ *              ensure_finite (kernels.py:148-149; synchronises the stream, debug option).
+ *            LA_FLAG_NO_DQ / LA_FLAG_NO_DKDV (la_bwd_ex): skip sweep 1 (dq unused, may be NULL) /
+ *              sweep 2 (dk, dv, dkv_out unused) -- lets a caller overlap one sweep with other work,
+ *              e.g. the sequence-parallel state exchange with the dq pass.
+ * The CHECK flags synchronise, so they cannot be used under CUDA graph capture. */
+typedef enum la_operand {
+  LA_T_Q = 0, LA_T_K = 1, LA_T_V = 2, LA_T_O = 3, LA_T_DO = 4, LA_T_DQ = 5, LA_T_DK = 6, LA_T_DV = 7
+} la_operand;
+
+typedef struct la_tensor_strides {
+  int64_t s[8][3];    /* [la_operand][batch, head, position] element strides */
+} la_tensor_strides;
+
+#define LA_FLAG_RESUME        0x1u
+#define LA_FLAG_CHECK_DECAY   0x2u
+#define LA_FLAG_CHECK_FINITE  0x4u
+#define LA_FLAG_NO_DQ         0x8u
+#define LA_FLAG_NO_DKDV       0x10u
+
+LA_API int la_fwd_ex(const la_desc* desc, const la_tensor_strides* strides, uint32_t flags, const void* q,
+              const void* k, const void* v, const double* lam, const void* kv_in, void* o, void* kv_out,
+              void* seg_states_out, void* workspace, size_t workspace_bytes, void* stream);
+LA_API int la_bwd_ex(const la_desc* desc, const la_tensor_strides* strides, uint32_t flags, const void* q,
+              const void* k, const void* v, const void* dout, const double* lam, const void* kv_in,
+              const void* dkv_in, const void* fwd_seg_states, void* dq, void* dk, void* dv, void* dkv_out,
+              void* workspace, size_t workspace_bytes, void* stream);
+
+/* Host-side decay validation for a C caller that holds lam on the host (as AttentionConfig does,
+ * kernels.py:84-91 / check_decay matrixops.py:72-77): LA_OK, or LA_ERR_DOMAIN naming the value. */
+LA_API int la_check_decay(const double* lam_host, int64_t heads);
+/* The backend and segment plan of an _ex call come from every operand's strides: keep desc->stride
+ * equal to q's so la_segment_count / la_launch_count describe the call.  la_workspace_bytes covers
+ * every backend's plan. */
 
 /* Local summaries of one sequence segment, for sequence parallelism:
  *   la_fwd_state: kv_delta  = sum_s lam^(n-1-s) k[s] v[s]^T   (= F(n) with kv_in = 0)

@@ -22,10 +22,15 @@ LA_BACKEND_AUTO, LA_BACKEND_SIMT, LA_BACKEND_TCGEN05 = 0, 1, 2
 BACKENDS = {"auto": LA_BACKEND_AUTO, "simt": LA_BACKEND_SIMT, "tcgen05": LA_BACKEND_TCGEN05}
 
 # every symbol include/lightning_attn.h declares
-EXPORTS = ("la_workspace_bytes", "la_segment_count", "la_fwd", "la_bwd", "la_fwd_state", "la_bwd_state",
+EXPORTS = ("la_workspace_bytes", "la_segment_count", "la_fwd", "la_bwd", "la_fwd_ex", "la_bwd_ex", "la_check_decay",
+           "la_fwd_state", "la_bwd_state",
            "la_decode", "la_gla_workspace_bytes", "la_gla_prologue", "la_gla_prologue_bwd", "la_gla_epilogue",
            "la_gla_epilogue_bwd", "la_gla_gate_rowsq", "la_gla_rowscale", "la_launch_count", "la_last_error", "la_abi_version", "la_build_info")
-ABI_VERSION = 2
+ABI_VERSION = 3
+# la_fwd_ex / la_bwd_ex flags
+LA_FLAG_RESUME, LA_FLAG_CHECK_DECAY, LA_FLAG_CHECK_FINITE, LA_FLAG_NO_DQ, LA_FLAG_NO_DKDV = 0x1, 0x2, 0x4, 0x8, 0x10
+# la_operand
+LA_T_Q, LA_T_K, LA_T_V, LA_T_O, LA_T_DO, LA_T_DQ, LA_T_DK, LA_T_DV = range(8)
 LA_ACT_NONE, LA_ACT_SWISH, LA_ACT_ONE_PLUS_ELU = 0, 1, 2
 ACTS = {"none": LA_ACT_NONE, "swish": LA_ACT_SWISH, "one_plus_elu": LA_ACT_ONE_PLUS_ELU}
 
@@ -44,6 +49,12 @@ class LaDesc(ctypes.Structure):
         ("stride", c_int64 * 3),
         ("segments", c_int64),
     ]
+
+
+class LaTensorStrides(ctypes.Structure):
+    """Mirror of ``la_tensor_strides``: [la_operand][batch, head, position] element strides."""
+
+    _fields_ = [("s", (c_int64 * 3) * 8)]
 
 
 class LaGlaDesc(ctypes.Structure):
@@ -99,6 +110,16 @@ def load() -> ctypes.CDLL:
     lib.la_bwd.argtypes = [P, c_void_p, c_void_p, c_void_p, c_void_p, POINTER(c_double), c_void_p, c_void_p,
                            c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]
     lib.la_bwd.restype = c_int
+    S = POINTER(LaTensorStrides)
+    lib.la_fwd_ex.argtypes = [P, S, ctypes.c_uint32, c_void_p, c_void_p, c_void_p, POINTER(c_double), c_void_p,
+                              c_void_p, c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]
+    lib.la_fwd_ex.restype = c_int
+    lib.la_bwd_ex.argtypes = [P, S, ctypes.c_uint32, c_void_p, c_void_p, c_void_p, c_void_p, POINTER(c_double),
+                              c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                              c_size_t, c_void_p]
+    lib.la_bwd_ex.restype = c_int
+    lib.la_check_decay.argtypes = [POINTER(c_double), c_int64]
+    lib.la_check_decay.restype = c_int
     lib.la_fwd_state.argtypes = [P, c_void_p, c_void_p, POINTER(c_double), c_void_p, c_void_p, c_size_t, c_void_p]
     lib.la_fwd_state.restype = c_int
     lib.la_bwd_state.argtypes = [P, c_void_p, c_void_p, POINTER(c_double), c_void_p, c_void_p, c_size_t, c_void_p]

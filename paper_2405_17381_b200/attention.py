@@ -22,8 +22,13 @@ class LightningAttention(torch.autograd.Function):
     @staticmethod
     def forward(ctx, q, k, v, lam, block=None, layout="bhnd", backend="auto"):
         heads = q.shape[1] if layout == "bhnd" else q.shape[2]
-        lam_dev = lam if (isinstance(lam, torch.Tensor) and lam.is_cuda and lam.dtype == torch.float64) \
-            else ops.decay_tensor(lam, heads, q.device)
+        # a device decay array is used as is only when it already is what the kernels read (one contiguous
+        # fp64 value per head on q's device; a value outside (0, 1] comes back as NaN outputs, load_decay);
+        # anything else -- host values, a broadcast scalar, another dtype or device -- goes through the
+        # validated, cached decay_tensor
+        fast = (isinstance(lam, torch.Tensor) and lam.is_cuda and lam.dtype == torch.float64
+                and lam.numel() == heads and lam.is_contiguous() and lam.device == q.device)
+        lam_dev = lam if fast else ops.decay_tensor(lam, heads, q.device)
         o, seg = ops.la_forward(q, k, v, None, block=block, layout=layout, backend=backend, lam_dev=lam_dev,
                                 want_seg_states=True)
         # the per-segment states of a split sequence spare the backward one summary pass (la_bwd)

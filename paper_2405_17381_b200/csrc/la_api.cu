@@ -5,14 +5,17 @@
 // Validation mirrors the reference's error classes:
 //   LA_ERR_DOMAIN  n/d < 1, B < 1, bad precision      (kernels.py:84-91)
 //   LA_ERR_SHAPE   missing operands, bad strides      (kernels.py:137-146)
-// lam in (0, 1] (matrixops.py:72-77) is validated by the host wrappers, which
-// own the host copy of lam; the ABI takes a device array so calls stay
-// asynchronous and graph-capturable.
+// lam in (0, 1] (matrixops.py:72-77): the ABI takes a device array so calls stay
+// asynchronous and graph-capturable; every kernel reads lam through load_decay,
+// which turns an invalid value into NaN outputs (never silently wrong ones), and
+// la_check_decay / LA_FLAG_CHECK_DECAY report it as LA_ERR_DOMAIN.
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
 #include <initializer_list>
 #include <string>
+
+#include <vector>
 
 #include <cuda.h>
 
@@ -22,6 +25,22 @@
 #include "la_scan.cuh"
 #include "la_simt.cuh"
 #include "la_tc.cuh"
+
+namespace la {
+
+int device_sms() {
+  static std::atomic<int> cache[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return kNumSMs;
+  const int hit = cache[dev].load(std::memory_order_relaxed);
+  if (hit > 0) return hit;
+  int sms = 0;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms < 1) return kNumSMs;
+  cache[dev].store(sms, std::memory_order_relaxed);
+  return sms;
+}
+
+}  // namespace la
 
 namespace {
 
@@ -55,18 +74,44 @@ int validate(const la_desc* desc) {
   if (desc->backend < LA_BACKEND_AUTO || desc->backend > LA_BACKEND_TCGEN05)
     return fail(LA_ERR_DOMAIN, "unknown backend %d", desc->backend);
   if (desc->segments < 0) return fail(LA_ERR_DOMAIN, "segments must be >= 0");
+  if (desc->segments > 65535) return fail(LA_ERR_UNSUPPORTED, "segments %lld > 65535", (long long)desc->segments);
   for (int i = 0; i < 3; ++i)
     if (desc->stride[i] < 0) return fail(LA_ERR_SHAPE, "negative stride");
   if (desc->stride[2] < desc->d) return fail(LA_ERR_SHAPE, "position stride %lld < d", (long long)desc->stride[2]);
-  if (desc->n > (int64_t)1 << 31 || desc->batch * desc->heads > 65535)
+  if (desc->n > (int64_t)INT32_MAX || desc->batch * desc->heads > 65535)
     return fail(LA_ERR_UNSUPPORTED, "n or batch*heads beyond this build's grid limits");
   if (desc->d > 128) return fail(LA_ERR_UNSUPPORTED, "head dim d=%lld > 128 is not implemented", (long long)desc->d);
   return LA_OK;
 }
 
-// Which backend serves this descriptor.
-int pick_backend(const la_desc* desc, int* backend) {
-  const bool tc_ok = la::tc_supported(desc->dtype, (int)desc->d, desc->stride);
+// Every operand's (batch, head, position) strides: the desc's triple unless the caller passed its own.
+struct OpStrides {
+  la::Strides3 s[8];
+};
+
+int op_strides(const la_desc* desc, const la_tensor_strides* ts, std::initializer_list<int> used, OpStrides* out) {
+  for (int i = 0; i < 8; ++i) {
+    const int64_t* src = ts != nullptr ? ts->s[i] : desc->stride;
+    out->s[i] = la::Strides3{src[0], src[1], src[2]};
+  }
+  if (ts != nullptr)
+    for (int i : used) {
+      const la::Strides3& x = out->s[i];
+      if (x.b < 0 || x.h < 0 || x.n < 0) return fail(LA_ERR_SHAPE, "operand %d: negative stride", i);
+      if (x.n < desc->d) return fail(LA_ERR_SHAPE, "operand %d: position stride %lld < d", i, (long long)x.n);
+    }
+  return LA_OK;
+}
+
+// Which backend serves this descriptor (and, for the _ex calls, these operand strides).
+int pick_backend(const la_desc* desc, int* backend, const OpStrides* ops = nullptr,
+                 std::initializer_list<int> used = {}) {
+  bool tc_ok = la::tc_supported(desc->dtype, (int)desc->d, desc->stride, 1);
+  if (ops != nullptr)
+    for (int i : used) {
+      const int64_t t[3] = {ops->s[i].b, ops->s[i].h, ops->s[i].n};
+      tc_ok = tc_ok && la::tc_supported(desc->dtype, (int)desc->d, t, 1);
+    }
   if (desc->backend == LA_BACKEND_TCGEN05) {
     if (!tc_ok)
       return fail(LA_ERR_UNSUPPORTED,
@@ -87,8 +132,9 @@ int pick_backend(const la_desc* desc, int* backend) {
 
 la::Plan plan_for(const la_desc* desc, int backend) {
   const int64_t bh = desc->batch * desc->heads;
-  if (backend == LA_BACKEND_TCGEN05) return la::tc_plan(bh, desc->n, (int)desc->d, desc->segments);
-  return la::make_plan(bh, desc->n, la::simt_chunk(desc->dtype), desc->segments, 2 * la::kNumSMs, LA_SIMT_MIN_CHUNKS);
+  const int sms = la::device_sms();
+  if (backend == LA_BACKEND_TCGEN05) return la::tc_plan(bh, desc->n, (int)desc->d, desc->segments, sms);
+  return la::make_plan(bh, desc->n, la::simt_chunk(desc->dtype), desc->segments, 2 * sms, LA_SIMT_MIN_CHUNKS);
 }
 
 size_t acc_bytes(int dtype) { return dtype == LA_F64 ? sizeof(double) : sizeof(float); }
@@ -105,9 +151,7 @@ size_t ws_bytes_for(const la_desc* desc, int backend, const la::Plan& plan) {
 la::PassDesc base_pass(const la_desc* desc, const la::Plan& plan, const double* lam) {
   la::PassDesc p;
   std::memset(&p, 0, sizeof(p));
-  p.sb = desc->stride[0];
-  p.sh = desc->stride[1];
-  p.sn = desc->stride[2];
+  p.sa = p.sbb = p.sc = p.so = la::Strides3{desc->stride[0], desc->stride[1], desc->stride[2]};
   p.batch = (int)desc->batch;
   p.heads = (int)desc->heads;
   p.n = (int)desc->n;
@@ -134,7 +178,10 @@ cudaError_t launch(int backend, int dtype, const la::PassDesc& p, bool state_onl
 // sequence edge, p.state_in_T its orientation): sub-segment summaries into `delta`, then the decayed
 // scan into `seg_in` ([bh][nseg][d][d], kernel orientation).  The segment at the far end of the pass
 // (fwd: the last, rev: the first) feeds no entering state, so it is not summarised.
-cudaError_t segment_states(int backend, int dtype, const la::PassDesc& p, void* delta, void* seg_in, cudaStream_t st) {
+// `resume`: the summaries are already in `delta` (left there by la_fwd_state / la_bwd_state, which
+// summarise every segment with the same plan), only the scan runs.
+cudaError_t segment_states(int backend, int dtype, const la::PassDesc& p, void* delta, void* seg_in, cudaStream_t st,
+                           bool resume = false) {
   la::PassDesc s = p;
   s.a = nullptr;
   s.out = nullptr;
@@ -143,7 +190,7 @@ cudaError_t segment_states(int backend, int dtype, const la::PassDesc& p, void* 
   s.delta_out = delta;
   s.g_lo = p.rev ? 1 : 0;
   s.g_hi = p.rev ? p.nseg - 1 : p.nseg - 2;
-  cudaError_t err = launch(backend, dtype, s, true, st);
+  cudaError_t err = resume ? cudaSuccess : launch(backend, dtype, s, true, st);
   if (err != cudaSuccess) return err;
   return la::launch_segment_scan(dtype == LA_F64, delta, seg_in, p.state_in, p.state_in_T, nullptr, 0, p.lam,
                                  p.batch * p.heads, p.heads, p.d, s, st);
@@ -244,10 +291,11 @@ struct Prepared {
   size_t need;
 };
 
-int prepare(const la_desc* desc, size_t ws_bytes, const void* ws, Prepared* out) {
+int prepare(const la_desc* desc, size_t ws_bytes, const void* ws, Prepared* out, const OpStrides* ops = nullptr,
+            std::initializer_list<int> used = {}) {
   int rc = validate(desc);
   if (rc != LA_OK) return rc;
-  rc = pick_backend(desc, &out->backend);
+  rc = pick_backend(desc, &out->backend, ops, used);
   if (rc != LA_OK) return rc;
   out->plan = plan_for(desc, out->backend);
   out->need = ws_bytes_for(desc, out->backend, out->plan);
@@ -256,12 +304,69 @@ int prepare(const la_desc* desc, size_t ws_bytes, const void* ws, Prepared* out)
   return LA_OK;
 }
 
+// LA_FLAG_CHECK_DECAY: read lam back (synchronous) and validate it like check_decay (matrixops.py:72-77)
+int check_decay_device(const double* lam, int64_t heads, cudaStream_t st) {
+  std::vector<double> host((size_t)heads);
+  cudaError_t err = cudaMemcpyAsync(host.data(), lam, sizeof(double) * (size_t)heads, cudaMemcpyDeviceToHost, st);
+  if (err == cudaSuccess) err = cudaStreamSynchronize(st);
+  if (err != cudaSuccess) return cuda_fail(err, "lam read-back");
+  return la_check_decay(host.data(), heads);
+}
+
+// LA_FLAG_CHECK_FINITE: the reference's ensure_finite on every input (kernels.py:148-149)
+template <typename T>
+__global__ void count_nonfinite_kernel(const T* x, la::Strides3 s, int64_t batch, int64_t heads, int64_t n, int64_t d,
+                                       unsigned long long* bad) {
+  const int64_t total = batch * heads * n * d;
+  unsigned long long mine = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t f = i % d, t = (i / d) % n, h = (i / (d * n)) % heads, b = i / (d * n * heads);
+    const double v = (double)la::Cvt<T>::to_f(x[b * s.b + h * s.h + t * s.n + f]);
+    if (!isfinite(v)) ++mine;
+  }
+  if (mine) atomicAdd(bad, mine);
+}
+
+int check_finite(const la_desc* desc, std::initializer_list<std::pair<const void*, la::Strides3>> ins,
+                 std::initializer_list<const char*> names, cudaStream_t st) {
+  unsigned long long* bad = nullptr;
+  cudaError_t err = cudaMallocAsync(reinterpret_cast<void**>(&bad), sizeof(unsigned long long) * ins.size(), st);
+  if (err == cudaSuccess) err = cudaMemsetAsync(bad, 0, sizeof(unsigned long long) * ins.size(), st);
+  int i = 0;
+  for (const auto& in : ins) {
+    if (err != cudaSuccess) break;
+    const dim3 grid(4 * la::device_sms()), block(256);
+    if (desc->dtype == LA_F64)
+      count_nonfinite_kernel<double><<<grid, block, 0, st>>>(reinterpret_cast<const double*>(in.first), in.second,
+                                                              desc->batch, desc->heads, desc->n, desc->d, bad + i);
+    else if (desc->dtype == LA_F32)
+      count_nonfinite_kernel<float><<<grid, block, 0, st>>>(reinterpret_cast<const float*>(in.first), in.second,
+                                                             desc->batch, desc->heads, desc->n, desc->d, bad + i);
+    else
+      count_nonfinite_kernel<__nv_bfloat16><<<grid, block, 0, st>>>(
+          reinterpret_cast<const __nv_bfloat16*>(in.first), in.second, desc->batch, desc->heads, desc->n, desc->d,
+          bad + i);
+    err = cudaGetLastError();
+    ++i;
+  }
+  std::vector<unsigned long long> host(ins.size(), 0);
+  if (err == cudaSuccess)
+    err = cudaMemcpyAsync(host.data(), bad, sizeof(unsigned long long) * ins.size(), cudaMemcpyDeviceToHost, st);
+  if (bad != nullptr) cudaFreeAsync(bad, st);
+  if (err == cudaSuccess) err = cudaStreamSynchronize(st);
+  if (err != cudaSuccess) return cuda_fail(err, "finiteness check");
+  i = 0;
+  for (const char* name : names) {
+    if (host[i] != 0) return fail(LA_ERR_DOMAIN, "%s: contains NaN or Inf (%llu entries)", name, host[i]);
+    ++i;
+  }
+  return LA_OK;
+}
+
 // The fused dK/dV sweep (la_tc_bwd.cu): q, k, v, do read once, one state update.  seg_in: the
 // adjoint state entering every segment (split sequences), else the caller's dkv_in.
-int dkdv(const la_desc* desc, const la::PassDesc& base, const void* q, const void* k, const void* v,
-         const void* dout, void* dq, void* dk, void* dv, const void* dkv_in, void* dkv_out, const void* seg_in,
-         cudaStream_t st) {
-  (void)desc;
+int dkdv(const la::PassDesc& base, const OpStrides& os, const void* q, const void* k, const void* v, const void* dout,
+         void* dk, void* dv, const void* dkv_in, void* dkv_out, const void* seg_in, cudaStream_t st) {
   la::PassDesc p = base;
   p.rev = 1;
   p.b = q;
@@ -281,10 +386,14 @@ int dkdv(const la_desc* desc, const la::PassDesc& base, const void* q, const voi
   }
   if (!la::tc_pointers_ok(p) || (reinterpret_cast<uintptr_t>(v) & 15) || (reinterpret_cast<uintptr_t>(dk) & 15))
     return cuda_fail(cudaErrorMisalignedAddress, "la_bwd dkdv");
-  cudaError_t err = la::tc_dkdv_launch(p, q, k, v, dout, dq, dk, dv, st);
+  const la::Strides3 s6[6] = {os.s[LA_T_Q], os.s[LA_T_K], os.s[LA_T_V], os.s[LA_T_DO], os.s[LA_T_DK], os.s[LA_T_DV]};
+  cudaError_t err = la::tc_dkdv_launch(p, q, k, v, dout, dk, dv, s6, st);
   if (err != cudaSuccess) return cuda_fail(err, "la_bwd dkdv");
   return LA_OK;
 }
+
+constexpr uint32_t kKnownFlags =
+    LA_FLAG_RESUME | LA_FLAG_CHECK_DECAY | LA_FLAG_CHECK_FINITE | LA_FLAG_NO_DQ | LA_FLAG_NO_DKDV;
 
 }  // namespace
 
@@ -294,7 +403,13 @@ size_t la_workspace_bytes(const la_desc* desc) {
   if (validate(desc) != LA_OK) return 0;
   int backend;
   if (pick_backend(desc, &backend) != LA_OK) return 0;
-  return ws_bytes_for(desc, backend, plan_for(desc, backend));
+  // an _ex call whose operand strides rule out the tensor cores runs the SIMT plan: cover both
+  size_t need = ws_bytes_for(desc, backend, plan_for(desc, backend));
+  if (backend == LA_BACKEND_TCGEN05) {
+    const size_t simt = ws_bytes_for(desc, LA_BACKEND_SIMT, plan_for(desc, LA_BACKEND_SIMT));
+    if (simt > need) need = simt;
+  }
+  return need;
 }
 
 int la_segment_count(const la_desc* desc) {
@@ -304,21 +419,45 @@ int la_segment_count(const la_desc* desc) {
   return plan_for(desc, backend).nseg;
 }
 
-int la_fwd(const la_desc* desc, const void* q, const void* k, const void* v, const double* lam, const void* kv_in,
-           void* o, void* kv_out, void* seg_states_out, void* workspace, size_t workspace_bytes, void* stream) {
+int la_check_decay(const double* lam_host, int64_t heads) {
+  if (lam_host == nullptr || heads < 1) return fail(LA_ERR_SHAPE, "la_check_decay: null lam or heads < 1");
+  for (int64_t h = 0; h < heads; ++h)
+    if (!(lam_host[h] > 0.0 && lam_host[h] <= 1.0))
+      return fail(LA_ERR_DOMAIN, "decay rate must lie in (0, 1], got %.17g (head %lld)", lam_host[h], (long long)h);
+  return LA_OK;
+}
+
+int la_fwd_ex(const la_desc* desc, const la_tensor_strides* strides, uint32_t flags, const void* q, const void* k,
+              const void* v, const double* lam, const void* kv_in, void* o, void* kv_out, void* seg_states_out,
+              void* workspace, size_t workspace_bytes, void* stream) {
+  if (flags & ~kKnownFlags) return fail(LA_ERR_DOMAIN, "la_fwd_ex: unknown flags 0x%x", flags);
+  if (flags & (LA_FLAG_NO_DQ | LA_FLAG_NO_DKDV)) return fail(LA_ERR_DOMAIN, "la_fwd_ex: backward-only flags");
+  if (desc == nullptr) return fail(LA_ERR_SHAPE, "null descriptor");
+  OpStrides os;
+  int rc = op_strides(desc, strides, {LA_T_Q, LA_T_K, LA_T_V, LA_T_O}, &os);
+  if (rc != LA_OK) return rc;
   Prepared pr;
-  int rc = prepare(desc, workspace_bytes, workspace, &pr);
+  rc = prepare(desc, workspace_bytes, workspace, &pr, &os, {LA_T_Q, LA_T_K, LA_T_V, LA_T_O});
   if (rc != LA_OK) return rc;
   if (!q || !k || !v || !o || !lam) return fail(LA_ERR_SHAPE, "la_fwd: null q/k/v/o/lam");
   if (!states_aligned({kv_in, kv_out, seg_states_out}))
     return fail(LA_ERR_SHAPE, "la_fwd: state buffers must be 16-byte aligned");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   bind_stream_context(st);
+  if ((flags & LA_FLAG_CHECK_DECAY) && (rc = check_decay_device(lam, desc->heads, st)) != LA_OK) return rc;
+  if ((flags & LA_FLAG_CHECK_FINITE) &&
+      (rc = check_finite(desc, {{q, os.s[LA_T_Q]}, {k, os.s[LA_T_K]}, {v, os.s[LA_T_V]}}, {"Q", "K", "V"}, st)) !=
+          LA_OK)
+    return rc;
   la::PassDesc p = base_pass(desc, pr.plan, lam);
   p.a = q;
   p.b = k;
   p.c = v;
   p.out = o;
+  p.sa = os.s[LA_T_Q];
+  p.sbb = os.s[LA_T_K];
+  p.sc = os.s[LA_T_V];
+  p.so = os.s[LA_T_O];
   p.rev = 0;
   p.state_in = kv_in;
   p.state_out = kv_out;
@@ -326,27 +465,50 @@ int la_fwd(const la_desc* desc, const void* q, const void* k, const void* v, con
   void* seg_in = nullptr;
   if (pr.plan.nseg > 1) {
     seg_in = seg_states_out != nullptr ? seg_states_out : ws_seg_in(workspace, desc, pr.plan);
-    err = segment_states(pr.backend, desc->dtype, p, ws_delta(workspace), seg_in, st);
+    err = segment_states(pr.backend, desc->dtype, p, ws_delta(workspace), seg_in, st, (flags & LA_FLAG_RESUME) != 0);
   }
   if (err == cudaSuccess) err = main_pass(pr.backend, desc->dtype, p, seg_in, 0, st);
   if (err != cudaSuccess) return cuda_fail(err, "la_fwd");
   return LA_OK;
 }
 
-int la_bwd(const la_desc* desc, const void* q, const void* k, const void* v, const void* dout, const double* lam,
-           const void* kv_in, const void* dkv_in, const void* fwd_seg_states, void* dq, void* dk, void* dv,
-           void* dkv_out, void* workspace, size_t workspace_bytes, void* stream) {
-  Prepared pr;
-  int rc = prepare(desc, workspace_bytes, workspace, &pr);
+int la_fwd(const la_desc* desc, const void* q, const void* k, const void* v, const double* lam, const void* kv_in,
+           void* o, void* kv_out, void* seg_states_out, void* workspace, size_t workspace_bytes, void* stream) {
+  return la_fwd_ex(desc, nullptr, 0, q, k, v, lam, kv_in, o, kv_out, seg_states_out, workspace, workspace_bytes,
+                   stream);
+}
+
+int la_bwd_ex(const la_desc* desc, const la_tensor_strides* strides, uint32_t flags, const void* q, const void* k,
+              const void* v, const void* dout, const double* lam, const void* kv_in, const void* dkv_in,
+              const void* fwd_seg_states, void* dq, void* dk, void* dv, void* dkv_out, void* workspace,
+              size_t workspace_bytes, void* stream) {
+  if (flags & ~kKnownFlags) return fail(LA_ERR_DOMAIN, "la_bwd_ex: unknown flags 0x%x", flags);
+  if (desc == nullptr) return fail(LA_ERR_SHAPE, "null descriptor");
+  const bool want_dq = !(flags & LA_FLAG_NO_DQ), want_dkdv = !(flags & LA_FLAG_NO_DKDV);
+  OpStrides os;
+  const std::initializer_list<int> used = {LA_T_Q, LA_T_K, LA_T_V, LA_T_DO, LA_T_DQ, LA_T_DK, LA_T_DV};
+  int rc = op_strides(desc, strides, used, &os);
   if (rc != LA_OK) return rc;
-  if (!q || !k || !v || !dout || !dq || !dk || !dv || !lam)
-    return fail(LA_ERR_SHAPE, "la_bwd: null q/k/v/do/dq/dk/dv/lam");
+  Prepared pr;
+  rc = prepare(desc, workspace_bytes, workspace, &pr, &os, used);
+  if (rc != LA_OK) return rc;
+  if (!q || !k || !v || !dout || !lam || (want_dq && !dq) || (want_dkdv && (!dk || !dv)))
+    return fail(LA_ERR_SHAPE, "la_bwd: null q/k/v/do/lam or a requested dq/dk/dv");
   if (!states_aligned({kv_in, dkv_in, fwd_seg_states, dkv_out}))
     return fail(LA_ERR_SHAPE, "la_bwd: state buffers must be 16-byte aligned");
+  const bool split = pr.plan.nseg > 1;
+  const bool resume = (flags & LA_FLAG_RESUME) != 0;
+  if (resume && split && want_dq && fwd_seg_states == nullptr)
+    return fail(LA_ERR_SHAPE, "la_bwd_ex: LA_FLAG_RESUME with a split sequence needs fwd_seg_states (sweep 1 would "
+                              "overwrite the resumed summaries)");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   bind_stream_context(st);
+  if ((flags & LA_FLAG_CHECK_DECAY) && (rc = check_decay_device(lam, desc->heads, st)) != LA_OK) return rc;
+  if ((flags & LA_FLAG_CHECK_FINITE) &&
+      (rc = check_finite(desc, {{q, os.s[LA_T_Q]}, {k, os.s[LA_T_K]}, {v, os.s[LA_T_V]}, {dout, os.s[LA_T_DO]}},
+                         {"Q", "K", "V", "dO"}, st)) != LA_OK)
+    return rc;
   const la::PassDesc base = base_pass(desc, pr.plan, lam);
-  const bool split = pr.plan.nseg > 1;
   void* delta = split ? ws_delta(workspace) : nullptr;
   void* seg_in = split ? ws_seg_in(workspace, desc, pr.plan) : nullptr;
   cudaError_t err = cudaSuccess;
@@ -357,84 +519,101 @@ int la_bwd(const la_desc* desc, const void* q, const void* k, const void* v, con
   p.b = v;
   p.c = k;
   p.out = dq;
+  p.sa = os.s[LA_T_DO];
+  p.sbb = os.s[LA_T_V];
+  p.sc = os.s[LA_T_K];
+  p.so = os.s[LA_T_DQ];
   p.rev = 0;
   p.state_in = kv_in;
   p.state_in_T = 1;
+  auto run_dq = [&](cudaStream_t s) -> cudaError_t {
+    if (split && fwd_seg_states != nullptr) return main_pass(pr.backend, desc->dtype, p, fwd_seg_states, 1, s);
+    cudaError_t e = split ? segment_states(pr.backend, desc->dtype, p, delta, seg_in, s) : cudaSuccess;
+    return e == cudaSuccess ? main_pass(pr.backend, desc->dtype, p, seg_in, 0, s) : e;
+  };
   // sweep 2 (kernels.py:320-333): dk = rev(v, do, q) carries dkv^T, dv = rev(k, q, do) carries dkv --
   // one set of segment states (over q, do) serves both passes
   la::PassDesc pd = base;
   pd.b = q;
   pd.c = dout;
+  pd.sbb = os.s[LA_T_Q];
+  pd.sc = os.s[LA_T_DO];
   pd.rev = 1;
   pd.state_in = dkv_in;
+  // states_ready: the entering adjoint states are already in seg_in
+  auto run_dkdv = [&](cudaStream_t s, bool states_ready) -> int {
+    if (split && !states_ready &&
+        (err = segment_states(pr.backend, desc->dtype, pd, delta, seg_in, s, resume)) != cudaSuccess)
+      return cuda_fail(err, "la_bwd dkv states");
+    if (pr.backend == LA_BACKEND_TCGEN05)
+      return dkdv(base, os, q, k, v, dout, dk, dv, dkv_in, dkv_out, split ? seg_in : nullptr, s);
+    la::PassDesc r = base;
+    r.a = v;
+    r.b = dout;
+    r.c = q;
+    r.out = dk;
+    r.sa = os.s[LA_T_V];
+    r.sbb = os.s[LA_T_DO];
+    r.sc = os.s[LA_T_Q];
+    r.so = os.s[LA_T_DK];
+    r.rev = 1;
+    r.state_in = dkv_in;
+    r.state_in_T = 1;
+    if ((err = main_pass(pr.backend, desc->dtype, r, seg_in, 1, s)) != cudaSuccess) return cuda_fail(err, "la_bwd dk");
+    r = base;
+    r.a = k;
+    r.b = q;
+    r.c = dout;
+    r.out = dv;
+    r.sa = os.s[LA_T_K];
+    r.sbb = os.s[LA_T_Q];
+    r.sc = os.s[LA_T_DO];
+    r.so = os.s[LA_T_DV];
+    r.rev = 1;
+    r.state_in = dkv_in;
+    r.state_out = dkv_out;
+    if ((err = main_pass(pr.backend, desc->dtype, r, seg_in, 0, s)) != cudaSuccess) return cuda_fail(err, "la_bwd dv");
+    return LA_OK;
+  };
+  if (!want_dkdv) return (err = run_dq(st)) == cudaSuccess ? LA_OK : cuda_fail(err, "la_bwd dq");
+  if (!want_dq) return run_dkdv(st, false);
 #ifndef LA_BWD_CONCURRENT
 #define LA_BWD_CONCURRENT 1
 #endif
-  if (LA_BWD_CONCURRENT && pr.backend == LA_BACKEND_TCGEN05 && (!split || fwd_seg_states != nullptr)) {
-    // The dq pass and the fused dK/dV sweep are independent: the sweep's chain (adjoint summaries and
-    // scan when the sequence is split, then the sweep) runs on the high-priority side stream, the dq
-    // pass beside it on the caller's stream.  Together they keep all 148 SMs streaming (each alone
-    // fills 128 of them at n = 8K) and overlap each other's ramp and tail.
+  if (LA_BWD_CONCURRENT && (!split || fwd_seg_states != nullptr) &&
+      (pr.backend == LA_BACKEND_TCGEN05 || split)) {
+    // The two sweeps are independent once sweep 1 needs no workspace: sweep 2's chain (adjoint summaries
+    // and scan when the sequence is split, then the fused dK/dV sweep -- or, on SIMT, just the summaries)
+    // runs on the high-priority side stream, the dq pass beside it on the caller's stream.  Together
+    // they keep all SMs streaming (each alone fills 128 of 148 at n = 8K) and overlap each other's ramp
+    // and tail.
     SideStream* side = nullptr;
     if ((err = side_stream(&side)) != cudaSuccess) return cuda_fail(err, "la_bwd side stream");
     if ((err = cudaEventRecord(side->fork, st)) != cudaSuccess ||
         (err = cudaStreamWaitEvent(side->stream, side->fork, 0)) != cudaSuccess)
       return cuda_fail(err, "la_bwd fork");
-    if (split && (err = segment_states(pr.backend, desc->dtype, pd, delta, seg_in, side->stream)) != cudaSuccess)
+    if (pr.backend == LA_BACKEND_TCGEN05) {
+      if ((rc = run_dkdv(side->stream, false)) != LA_OK) return rc;
+    } else if ((err = segment_states(pr.backend, desc->dtype, pd, delta, seg_in, side->stream, resume)) !=
+               cudaSuccess) {
       return cuda_fail(err, "la_bwd dkv states");
-    if ((rc = dkdv(desc, base, q, k, v, dout, dq, dk, dv, dkv_in, dkv_out, split ? seg_in : nullptr, side->stream)) !=
-        LA_OK)
-      return rc;
+    }
     if ((err = cudaEventRecord(side->join, side->stream)) != cudaSuccess) return cuda_fail(err, "la_bwd join");
-    if ((err = main_pass(pr.backend, desc->dtype, p, fwd_seg_states, 1, st)) != cudaSuccess)
-      return cuda_fail(err, "la_bwd dq");
+    if ((err = run_dq(st)) != cudaSuccess) return cuda_fail(err, "la_bwd dq");
     if ((err = cudaStreamWaitEvent(st, side->join, 0)) != cudaSuccess) return cuda_fail(err, "la_bwd join");
-    return LA_OK;
+    // SIMT: the entering adjoint states are ready, run the two reverse passes
+    return pr.backend == LA_BACKEND_TCGEN05 ? LA_OK : run_dkdv(st, true);
   }
-  if (split && fwd_seg_states != nullptr) {
-    // the dq pass needs only the forward's segment states, so the adjoint summaries (the workspace's
-    // only user) run on a side stream beside it: each alone leaves SMs idle
-    SideStream* side = nullptr;
-    if ((err = side_stream(&side)) != cudaSuccess) return cuda_fail(err, "la_bwd side stream");
-    if ((err = cudaEventRecord(side->fork, st)) != cudaSuccess ||
-        (err = cudaStreamWaitEvent(side->stream, side->fork, 0)) != cudaSuccess)
-      return cuda_fail(err, "la_bwd fork");
-    if ((err = segment_states(pr.backend, desc->dtype, pd, delta, seg_in, side->stream)) != cudaSuccess)
-      return cuda_fail(err, "la_bwd dkv states");
-    if ((err = cudaEventRecord(side->join, side->stream)) != cudaSuccess) return cuda_fail(err, "la_bwd join");
-    if ((err = main_pass(pr.backend, desc->dtype, p, fwd_seg_states, 1, st)) != cudaSuccess)
-      return cuda_fail(err, "la_bwd dq");
-    if ((err = cudaStreamWaitEvent(st, side->join, 0)) != cudaSuccess) return cuda_fail(err, "la_bwd join");
-  } else {
-    if (split) err = segment_states(pr.backend, desc->dtype, p, delta, seg_in, st);
-    if (err == cudaSuccess) err = main_pass(pr.backend, desc->dtype, p, seg_in, 0, st);
-    if (err != cudaSuccess) return cuda_fail(err, "la_bwd dq");
-    if (split && (err = segment_states(pr.backend, desc->dtype, pd, delta, seg_in, st)) != cudaSuccess)
-      return cuda_fail(err, "la_bwd dkv states");
-  }
-  if (pr.backend == LA_BACKEND_TCGEN05) return dkdv(desc, base, q, k, v, dout, dq, dk, dv, dkv_in, dkv_out,
-                                                     split ? seg_in : nullptr, st);
-  p = base;
-  p.a = v;
-  p.b = dout;
-  p.c = q;
-  p.out = dk;
-  p.rev = 1;
-  p.state_in = dkv_in;
-  p.state_in_T = 1;
-  if ((err = main_pass(pr.backend, desc->dtype, p, seg_in, 1, st)) != cudaSuccess) return cuda_fail(err, "la_bwd dk");
-  p = base;
-  p.a = k;
-  p.b = q;
-  p.c = dout;
-  p.out = dv;
-  p.rev = 1;
-  p.state_in = dkv_in;
-  p.state_out = dkv_out;
-  if ((err = main_pass(pr.backend, desc->dtype, p, seg_in, 0, st)) != cudaSuccess) return cuda_fail(err, "la_bwd dv");
-  return LA_OK;
+  if ((err = run_dq(st)) != cudaSuccess) return cuda_fail(err, "la_bwd dq");
+  return run_dkdv(st, false);
 }
 
+int la_bwd(const la_desc* desc, const void* q, const void* k, const void* v, const void* dout, const double* lam,
+           const void* kv_in, const void* dkv_in, const void* fwd_seg_states, void* dq, void* dk, void* dv,
+           void* dkv_out, void* workspace, size_t workspace_bytes, void* stream) {
+  return la_bwd_ex(desc, nullptr, 0, q, k, v, dout, lam, kv_in, dkv_in, fwd_seg_states, dq, dk, dv, dkv_out,
+                   workspace, workspace_bytes, stream);
+}
 static int state_entry(const la_desc* desc, const void* b, const void* c, int rev, const double* lam, void* out,
                        void* workspace, size_t workspace_bytes, void* stream, const char* who) {
   Prepared pr;

@@ -29,7 +29,21 @@
 
 namespace la {
 
-constexpr int kNumSMs = 148;  // B200
+constexpr int kNumSMs = 148;  // B200: the planner's default when the device cannot be queried
+
+// SM count of the calling thread's current device (cached per device ordinal); the segment planners
+// size their grids from it, so a MIG slice or another part plans for what it has
+int device_sms();
+
+// The decay of head h.  A lam outside (0, 1] or NaN -- which the reference rejects with DomainError
+// (matrixops.py:72-77) -- is read as NaN, so every output of the call comes out NaN instead of silently
+// wrong: the ABI takes lam on the device and does not read it back per call (LA_FLAG_CHECK_DECAY and
+// la_check_decay report it as LA_ERR_DOMAIN).  Ladders multiply lam^0 by `lam / lam` (exactly 1 for a
+// valid lam, NaN otherwise) so even the diagonal terms are poisoned.
+__device__ __forceinline__ double load_decay(const double* lam, int h) {
+  const double l = lam[h];
+  return (l > 0.0 && l <= 1.0) ? l : __longlong_as_double(0x7ff8000000000000LL);
+}
 
 // Load/convert helpers for the three operand dtypes.
 template <typename T> struct Cvt;
@@ -46,15 +60,20 @@ template <> struct Cvt<__nv_bfloat16> {
   __device__ __forceinline__ static __nv_bfloat16 from_f(float x) { return __float2bfloat16_rn(x); }
 };
 
+// Element strides of one operand: batch, head, position (the feature stride is 1).
+struct Strides3 {
+  int64_t b, h, n;
+};
+
 // One pass over all (batch, head) sequences, split into `nseg` segments of
-// `seg_len` positions (a multiple of the kernel's chunk).  All tensors share
-// strides; the feature stride is 1.
+// `seg_len` positions (a multiple of the kernel's chunk).  Every operand has its
+// own strides; the feature stride is 1.
 struct PassDesc {
   const void* a;
   const void* b;
   const void* c;
   void* out;              // nullptr in state-only mode
-  int64_t sb, sh, sn;     // element strides of batch, head, position
+  Strides3 sa, sbb, sc, so;  // strides of a, b, c, out
   int batch, heads, n, d;
   const double* lam;      // device [heads]
   int rev;

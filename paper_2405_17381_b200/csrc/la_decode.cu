@@ -36,7 +36,7 @@ __global__ void __launch_bounds__(kDecThreads) decode_kernel(const T* __restrict
     sv[e] = (Tacc)Cvt<T>::to_f(v[base + e]);
   }
   __syncthreads();
-  const Tacc l = (Tacc)lam[hi];
+  const Tacc l = (Tacc)load_decay(lam, hi);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   Tacc* st = kv + (int64_t)bh * d * d;
   constexpr int NC = VW == 1 ? 4 : 1;  // column groups per lane: 4 x 32 scalars, or one 32 x VW vector
@@ -141,7 +141,7 @@ __global__ void __launch_bounds__(256) decode_bulk_kernel(const T* __restrict__ 
   }
   __syncthreads();
   ptx::mbar_wait(&bar, 0);
-  const float l = (float)lam[hi];
+  const float l = (float)load_decay(lam, hi);
   const int c = threadIdx.x & (DD - 1), r0 = threadIdx.x >> 7;
   const float vc = sv[c];
   float acc = 0.f;

@@ -170,9 +170,9 @@ __global__ void __launch_bounds__(256) prologue_kernel(const T* __restrict__ qp,
 
 constexpr int kRowsPerBlock = 64;
 
-// grid (ceil(width/V / 256), ceil(rows / 64)); a thread owns one 16-byte column vector and walks 64
-// rows.  dtheta partials per (row block, x block) land in `partial` [gridDim.y * gridDim.x][d/2]
-// (deterministic; summed by reduce_theta_kernel)
+// grid (ceil(rows / 64), ceil(width/V / 256)) -- row blocks on x (no 65535 cap); a thread owns one 16-byte
+// column vector and walks 64 rows.  dtheta partials per (row block, column block) land in `partial`
+// [gridDim.x * gridDim.y][d/2] (deterministic; summed by reduce_theta_kernel)
 template <typename T, typename Tacc>
 __global__ void __launch_bounds__(256) prologue_bwd_kernel(const T* __restrict__ qp, const T* __restrict__ kp,
                                                            const double* __restrict__ theta, const T* __restrict__ dq,
@@ -183,7 +183,7 @@ __global__ void __launch_bounds__(256) prologue_bwd_kernel(const T* __restrict__
   constexpr int V = Vec<T>::N;
   extern __shared__ double sdt[];  // [blockDim.x][V / 2]: this block's per-pair partials
   const int vw = width / V, hd = d >> 1;
-  const int vc = blockIdx.x * blockDim.x + threadIdx.x;
+  const int vc = blockIdx.y * blockDim.x + threadIdx.x;
   Tacc acc[V / 2];
 #pragma unroll
   for (int pr = 0; pr < V / 2; ++pr) acc[pr] = 0;
@@ -191,7 +191,7 @@ __global__ void __launch_bounds__(256) prologue_bwd_kernel(const T* __restrict__
   if (vc < vw) {
     RotWalk<Tacc, V / 2> rw;
     if (theta != nullptr) rw.init(theta, c0 >> 1, hd);
-    const int64_t r0 = (int64_t)blockIdx.y * kRowsPerBlock;
+    const int64_t r0 = (int64_t)blockIdx.x * kRowsPerBlock;
     const int64_t r1 = r0 + kRowsPerBlock < rows ? r0 + kRowsPerBlock : rows;
 #pragma unroll 2
     for (int64_t row = r0; row < r1; ++row) {
@@ -239,8 +239,8 @@ __global__ void __launch_bounds__(256) prologue_bwd_kernel(const T* __restrict__
   // fold the heads: pair p of the row belongs to angle p % hd; each angle sums its block-local pairs in
   // increasing order (no atomics, so dtheta is bitwise reproducible)
   const int npairs = blockDim.x * (V / 2);
-  const int base = blockIdx.x * npairs;  // row pair index of this block's first pair
-  double* dst = partial + ((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * hd;
+  const int base = blockIdx.y * npairs;  // row pair index of this block's first pair
+  double* dst = partial + ((int64_t)blockIdx.x * gridDim.y + blockIdx.y) * hd;
   for (int j = threadIdx.x; j < hd; j += blockDim.x) {
     double sum = 0.0;
     for (int lp = ((j - base) % hd + hd) % hd; lp < npairs; lp += hd) sum += sdt[lp];
@@ -488,7 +488,7 @@ template <typename T, typename Tacc>
 cudaError_t prologue_bwd_t(const GlaRows& g, const void* qp, const void* kp, const double* theta, const void* dq,
                            const void* dk, void* dqp, void* dkp, double* partial, double* dtheta, cudaStream_t st) {
   const int vw = g.width / Vec<T>::N, hd = g.d / 2;
-  const dim3 grid((unsigned)((vw + 255) / 256), (unsigned)((g.rows + kRowsPerBlock - 1) / kRowsPerBlock));
+  const dim3 grid((unsigned)((g.rows + kRowsPerBlock - 1) / kRowsPerBlock), (unsigned)((vw + 255) / 256));
   const size_t smem = theta != nullptr ? (size_t)256 * (Vec<T>::N / 2) * sizeof(double) : 0;
   prologue_bwd_kernel<T, Tacc><<<grid, 256, smem, st>>>(
       static_cast<const T*>(qp), static_cast<const T*>(kp), theta, static_cast<const T*>(dq),

@@ -48,7 +48,7 @@ __global__ void __launch_bounds__(kScanThreads) segment_scan_kernel(
       len = p1 - p0;
     }
     s_len[threadIdx.x] = len;
-    s_pow[threadIdx.x] = (Tacc)pow(lam[bh % heads], (double)len);
+    s_pow[threadIdx.x] = (Tacc)pow(load_decay(lam, bh % heads), (double)len);
   }
   __syncthreads();
   const int dd = d * d;

@@ -50,18 +50,18 @@ __global__ void __launch_bounds__(kThreads) simt_pass_kernel(PassDesc p) {
   const int p0 = seg * p.seg_len;
   const int p1 = min(p.n, p0 + p.seg_len);
   const int nchunks = (p1 - p0 + C - 1) / C;
-  const double lam = p.lam[hi];
+  const double lam = load_decay(p.lam, hi);
 
-  const int64_t base = (int64_t)bi * p.sb + (int64_t)hi * p.sh;
-  const Tin* A = reinterpret_cast<const Tin*>(p.a) + base;
-  const Tin* Bm = reinterpret_cast<const Tin*>(p.b) + base;
-  const Tin* Cm = reinterpret_cast<const Tin*>(p.c) + base;
-  Tin* O = STATE_ONLY ? nullptr : reinterpret_cast<Tin*>(p.out) + base;
+  auto base = [&](const Strides3& s) { return (int64_t)bi * s.b + (int64_t)hi * s.h; };
+  const Tin* A = STATE_ONLY ? nullptr : reinterpret_cast<const Tin*>(p.a) + base(p.sa);
+  const Tin* Bm = reinterpret_cast<const Tin*>(p.b) + base(p.sbb);
+  const Tin* Cm = reinterpret_cast<const Tin*>(p.c) + base(p.sc);
+  Tin* O = STATE_ONLY ? nullptr : reinterpret_cast<Tin*>(p.out) + base(p.so);
 
   // Power ladder in fp64 by repeated multiplication, then cast
   // (the reference builds its ladders the same way: matrixops.py:104-119).
   if (tid == 0) {
-    double x = 1.0;
+    double x = lam / lam;  // 1, or NaN for an invalid lam (load_decay)
     for (int k = 0; k <= C; ++k) {
       pw[k] = (Tacc)x;
       x *= lam;
@@ -83,10 +83,10 @@ __global__ void __launch_bounds__(kThreads) simt_pass_kernel(PassDesc p) {
 
     for (int idx = tid; idx < b * d; idx += kThreads) {
       const int i = idx / d, k = idx % d;
-      const int64_t g = (int64_t)(r0 + i) * p.sn + k;
-      if (!STATE_ONLY) sA[i * ld + k] = (Tacc)Cvt<Tin>::to_f(A[g]);
-      sB[i * ld + k] = (Tacc)Cvt<Tin>::to_f(Bm[g]);
-      sC[i * ld + k] = (Tacc)Cvt<Tin>::to_f(Cm[g]);
+      const int64_t r = r0 + i;
+      if (!STATE_ONLY) sA[i * ld + k] = (Tacc)Cvt<Tin>::to_f(A[r * p.sa.n + k]);
+      sB[i * ld + k] = (Tacc)Cvt<Tin>::to_f(Bm[r * p.sbb.n + k]);
+      sC[i * ld + k] = (Tacc)Cvt<Tin>::to_f(Cm[r * p.sc.n + k]);
     }
     __syncthreads();
 
@@ -162,7 +162,7 @@ __global__ void __launch_bounds__(kThreads) simt_pass_kernel(PassDesc p) {
 #pragma unroll
           for (int q = 0; q < CP; ++q) {
             const int col = tc + 16 * q;
-            if (col < d) O[(int64_t)(r0 + i) * p.sn + col] = Cvt<Tin>::from_f(intra[x][q] + osc * inter[x][q]);
+            if (col < d) O[(int64_t)(r0 + i) * p.so.n + col] = Cvt<Tin>::from_f(intra[x][q] + osc * inter[x][q]);
           }
         }
       }

@@ -137,7 +137,7 @@ __global__ void __launch_bounds__(S_THREADS, 2)
     const int tid = threadIdx.x - 64;     // 0..127
     const int i = tid & (SC - 1);         // chunk row
     const int hh = tid >> 6;              // column half
-    const double lam = args.lam[hi];
+    const double lam = load_decay(args.lam, hi);
     for (int t = 0; t < nchunks; ++t) {
       const int s = t % SNST;
       const int r0 = p0 + t * SC;
@@ -145,7 +145,7 @@ __global__ void __launch_bounds__(S_THREADS, 2)
       mbar_wait(&bars.full[s], (t / SNST) & 1);
       // fwd lam^(p1-1-s), rev lam^(s-p0+1); rows past the sub-segment (tail) contribute nothing
       const int row = r0 + i;
-      float w = i < b ? (float)pow(lam, (double)(rev ? row - p0 + 1 : p1 - 1 - row)) : 0.f;
+      float w = i < b ? (float)(pow(lam, (double)(rev ? row - p0 + 1 : p1 - 1 - row)) * (lam / lam)) : 0.f;
 #ifdef LA_MUTATE_DKV
       if (rev) w = -w;  // fault injection: the reference's `_dkv_step` sign flip (test_kernels.py:249-268)
 #endif
@@ -188,7 +188,7 @@ __global__ void __launch_bounds__(S_THREADS, 2)
 
 cudaError_t tc_summary_launch(const PassDesc& p, cudaStream_t st) {
   CUtensorMap mb, mc;
-  if (!tc_make_map(&mb, p.b, p, SC) || !tc_make_map(&mc, p.c, p, SC)) return cudaErrorInvalidValue;
+  if (!tc_make_map(&mb, p.b, p, p.sbb, SC) || !tc_make_map(&mc, p.c, p, p.sc, SC)) return cudaErrorInvalidValue;
   SumArgs a;
   a.heads = p.heads;
   a.n = p.n;

@@ -112,7 +112,6 @@ struct TcArgs {
   int heads, n, seg_len, nseg, rev;
   const double* lam;
   uint16_t* out;  // bf16 output (full mode)
-  int64_t sb, sh, sn;
   const float* state_in;
   int64_t in_bh_stride, in_seg_stride;
   int in_T;
@@ -179,7 +178,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   }
   // lam^0 .. lam^C, one power per thread (binary exponentiation in fp64): a serial ladder here held
   // every warp (and the first TMA loads) back by ~130 dependent multiplies
-  if (threadIdx.x <= C) pw[threadIdx.x] = (float)pow_int(args.lam[hi], (int)threadIdx.x);
+  if (threadIdx.x <= C) {
+    const double l = load_decay(args.lam, hi);
+    pw[threadIdx.x] = (float)(pow_int(l, (int)threadIdx.x) * (l / l));
+  }
   if (warp == WARP_TMA && lane == 0) {
     tma_prefetch(&map_a);
     tma_prefetch(&map_b);
@@ -633,14 +635,14 @@ thread_local char g_detail[256];
 #define LA_L2_PROMO CU_TENSOR_MAP_L2_PROMOTION_L2_256B
 #endif
 
-bool tc_make_map(CUtensorMap* map, const void* base, const PassDesc& p, int box_rows) {
+bool tc_make_map(CUtensorMap* map, const void* base, const PassDesc& p, const Strides3& s, int box_rows) {
   auto enc = encode_fn();
   if (enc == nullptr) {
     snprintf(g_detail, sizeof(g_detail), "cuTensorMapEncodeTiled entry point unavailable");
     return false;
   }
   cuuint64_t dims[4] = {(cuuint64_t)p.d, (cuuint64_t)p.n, (cuuint64_t)p.heads, (cuuint64_t)p.batch};
-  cuuint64_t strides[3] = {(cuuint64_t)p.sn * 2, (cuuint64_t)p.sh * 2, (cuuint64_t)p.sb * 2};
+  cuuint64_t strides[3] = {(cuuint64_t)s.n * 2, (cuuint64_t)s.h * 2, (cuuint64_t)s.b * 2};
   cuuint32_t box[4] = {64, (cuuint32_t)box_rows, 1, 1};
   cuuint32_t estr[4] = {1, 1, 1, 1};
   // degenerate strides of size-1 dims must still be valid multiples of 16
@@ -663,13 +665,10 @@ cudaError_t launch_tc(const PassDesc& p, cudaStream_t st) {
   CUtensorMap ma, mb, mc, mo;
   std::memset(&ma, 0, sizeof(ma));
   std::memset(&mo, 0, sizeof(mo));
-  if (!tc_make_map(&mb, p.b, p) || !tc_make_map(&mc, p.c, p)) return cudaErrorInvalidValue;
-  if (!tc_make_map(&ma, p.a, p) || !tc_make_map(&mo, p.out, p)) return cudaErrorInvalidValue;
+  if (!tc_make_map(&mb, p.b, p, p.sbb) || !tc_make_map(&mc, p.c, p, p.sc)) return cudaErrorInvalidValue;
+  if (!tc_make_map(&ma, p.a, p, p.sa) || !tc_make_map(&mo, p.out, p, p.so)) return cudaErrorInvalidValue;
   TcArgs a;
   a.out = reinterpret_cast<uint16_t*>(p.out);
-  a.sb = p.sb;
-  a.sh = p.sh;
-  a.sn = p.sn;
   a.heads = p.heads;
   a.n = p.n;
   a.seg_len = p.seg_len;
@@ -709,9 +708,9 @@ extern "C" __attribute__((visibility("default"))) int la_debug_set_trace_bwd_c(v
 }
 #endif
 
-bool tc_supported(int dtype, int d, const int64_t* strides) {
+bool tc_supported(int dtype, int d, const int64_t* strides, int count) {
   if (dtype != LA_BF16 || d != D) return false;
-  for (int i = 0; i < 3; ++i)
+  for (int i = 0; i < 3 * count; ++i)
     if ((strides[i] * 2) % 16 != 0) return false;
   return true;
 }
@@ -725,25 +724,26 @@ bool tc_pointers_ok(const PassDesc& p) {
 // two operands); otherwise the largest count that keeps all CTAs in ONE wave, which measured best on
 // B200 at every long-n bench shape (profiles/r01_seg_sweep.txt: multi-wave splits lose to per-CTA
 // pipeline fill and partial last waves).  Segments keep >= 2 chunks; the workspace is sized for the
-// one-wave cap so it does not depend on n.
-Plan tc_plan(int64_t bh, int64_t n, int d, int64_t want_segments) {
+// one-wave cap so it does not depend on n.  `sms` = the device's SM count (device_sms()).
+Plan tc_plan(int64_t bh, int64_t n, int d, int64_t want_segments, int sms) {
   (void)d;
+  if (sms < 1) sms = kNumSMs;
   if (want_segments > 0) {
-    Plan p = make_plan(bh, n, C, want_segments, kNumSMs, 1);
-    p.nsub_ws = (int)(4 * std::max<int64_t>(p.nseg_ws, kNumSMs / bh) + 4);
-    plan_subsegments(p, bh, 2 * kNumSMs, 2, p.nsub_ws);
+    Plan p = make_plan(bh, n, C, want_segments, sms, 1);
+    p.nsub_ws = (int)(4 * std::max<int64_t>(p.nseg_ws, sms / bh) + 4);
+    plan_subsegments(p, bh, 2 * sms, 2, p.nsub_ws);
     return p;
   }
   const int64_t nchunks = (n + C - 1) / C;
-  const int64_t cap = std::max<int64_t>(1, kNumSMs / bh);
+  const int64_t cap = std::max<int64_t>(1, sms / bh);
   int64_t nseg = 1;
-  if (bh * 10 < kNumSMs * 6) nseg = std::min<int64_t>(cap, std::max<int64_t>(1, nchunks / 2));
-  Plan p = make_plan(bh, n, C, nseg, kNumSMs, 1);
+  if (bh * 10 < (int64_t)sms * 6) nseg = std::min<int64_t>(cap, std::max<int64_t>(1, nchunks / 2));
+  Plan p = make_plan(bh, n, C, nseg, sms, 1);
   p.nseg_ws = (int)cap;
   p.nsub_ws = (int)(4 * cap + 4);
   // summaries: one wave of the two-CTAs-per-SM summary kernel over the segments a scan needs,
   // sub-segments of >= 2 chunks
-  plan_subsegments(p, bh, 2 * kNumSMs, 2, p.nsub_ws);
+  plan_subsegments(p, bh, 2 * sms, 2, p.nsub_ws);
   return p;
 }
 

@@ -5,19 +5,21 @@
 #include "la_common.cuh"
 
 namespace la {
-bool tc_supported(int dtype, int d, const int64_t* strides);
+// bf16, d = 128, and every stride of the `count` (batch, head, position) triples a multiple of 16 bytes
+bool tc_supported(int dtype, int d, const int64_t* strides, int count);
 bool tc_pointers_ok(const PassDesc& p);
 const char* tc_detail();  // thread-local detail of the last host-side failure
 // 4-D TMA descriptor (d, n, heads, batch) over a bf16 [.., .., .., 128] tensor with the desc's strides,
 // box 64 x box_rows, 128-byte swizzle
-bool tc_make_map(CUtensorMap* map, const void* base, const PassDesc& p, int box_rows = 128);
+bool tc_make_map(CUtensorMap* map, const void* base, const PassDesc& p, const Strides3& s, int box_rows = 128);
 // the segment-summary pass (la_summary.cu): p.delta_out, sub-segment geometry, g_lo..g_hi
 cudaError_t tc_summary_launch(const PassDesc& p, cudaStream_t st);
-Plan tc_plan(int64_t bh, int64_t n, int d, int64_t want_segments);
+Plan tc_plan(int64_t bh, int64_t n, int d, int64_t want_segments, int sms);
 // the fused reverse sweep of the backward: dK and dV in one pass over q, k, v, do (p.state_in = the
 // entering adjoint state in dkv orientation; p.state_out = dkv_out, written by segment 0)
+// s[6]: strides of q, k, v, do, dk, dv
 cudaError_t tc_dkdv_launch(const PassDesc& p, const void* q, const void* k, const void* v, const void* dout,
-                           void* dq_unused, void* dk, void* dv, cudaStream_t st);
+                           void* dk, void* dv, const Strides3* s, cudaStream_t st);
 // one launch of the main pass kernel (state_only = false) or of the per-segment summary kernel
 cudaError_t tc_launch(const PassDesc& p, bool state_only, cudaStream_t st);
 }  // namespace la

@@ -155,7 +155,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   }
   // lam^0 .. lam^C, one power per thread (binary exponentiation in fp64): a serial ladder here held
   // every warp (and the first TMA loads) back by ~130 dependent multiplies
-  if (threadIdx.x <= C) pw[threadIdx.x] = (float)pow_int(args.lam[hi], (int)threadIdx.x);
+  if (threadIdx.x <= C) {
+    const double l = load_decay(args.lam, hi);
+    pw[threadIdx.x] = (float)(pow_int(l, (int)threadIdx.x) * (l / l));
+  }
   if (warp == WARP_TMA && lane == 0) {
     tma_prefetch(&map_q);
     tma_prefetch(&map_k);
@@ -603,11 +606,10 @@ void la_debug_set_trace_bwd(void* dev_ptr) { cudaMemcpyToSymbol(g_la_trace_bwd, 
 #endif
 
 cudaError_t tc_dkdv_launch(const PassDesc& p, const void* q, const void* k, const void* v, const void* dout,
-                           void* dq_unused, void* dk, void* dv, cudaStream_t st) {
-  (void)dq_unused;
+                           void* dk, void* dv, const Strides3* s, cudaStream_t st) {
   CUtensorMap mq, mk, mv, mdo, mdk, mdv;
-  if (!tc_make_map(&mq, q, p) || !tc_make_map(&mk, k, p) || !tc_make_map(&mv, v, p) || !tc_make_map(&mdo, dout, p) ||
-      !tc_make_map(&mdk, dk, p) || !tc_make_map(&mdv, dv, p))
+  if (!tc_make_map(&mq, q, p, s[0]) || !tc_make_map(&mk, k, p, s[1]) || !tc_make_map(&mv, v, p, s[2]) ||
+      !tc_make_map(&mdo, dout, p, s[3]) || !tc_make_map(&mdk, dk, p, s[4]) || !tc_make_map(&mdv, dv, p, s[5]))
     return cudaErrorInvalidValue;
   BwdArgs a;
   a.heads = p.heads;

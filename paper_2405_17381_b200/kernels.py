@@ -9,6 +9,13 @@ Same names, argument meaning and error behaviour as the reference
     lightning_forward_decay(q, k, v, cfg)    -> ndarray              kernels.py:253-284
     lightning_backward_decay(q, k, v, do, cfg) -> GradBundle         kernels.py:287-334
     KvState, GradBundle, TimingRecord, bench_kernel, aux_state_bytes
+    KERNEL_KINDS = ("left", "right", "lightning", "lightning-decay")  kernels.py:64
+
+The "left" / "right" kinds of the timing harness (Fig. 1/2 of the paper) are the reference's
+float64 baselines (oracles.py:100-162), run on the device: "left" is the quadratic left product
+[(Q K^T) * M] V with cuBLAS GEMMs (and its materialised-score backward), "right" the per-token
+recurrence kv_t = lam kv_(t-1) + k_t v_t^T as one la_decode launch per position (its backward, the
+two sequential sweeps of reference_backward, as three such walks).
 
 Inputs are 2-D host arrays (one head), as in the reference; they are copied
 to the current CUDA device, computed by the CUDA library (fp64 kernels for
@@ -28,7 +35,7 @@ import torch
 from . import ops
 from .errors import DomainError, ShapeError, check_decay
 
-KERNEL_KINDS = ("lightning", "lightning-decay")
+KERNEL_KINDS = ("left", "right", "lightning", "lightning-decay")
 
 _PRECISIONS = {"working": np.float32, "reference": np.float64, "bf16": np.float32}
 _TORCH = {"working": torch.float32, "reference": torch.float64, "bf16": torch.bfloat16}
@@ -176,9 +183,15 @@ def aux_state_bytes(kind: str, n: int, d: int, block: int, itemsize: int, backwa
 
     The workspace holds per-segment summaries; the segment count is capped by
     the SM count, so like the reference's inventory it does not grow with n.
+    The "left" / "right" baselines keep the reference's analytic inventory
+    (kernels.py:356-359): n x n score + mask, or the d x d summary + one temp.
     """
     if kind not in KERNEL_KINDS:
         raise DomainError(f"unknown kernel kind {kind!r}, expected one of {KERNEL_KINDS}")
+    if kind == "left":
+        return 2 * n * n * itemsize
+    if kind == "right":
+        return 2 * d * d * itemsize
     dtype = {8: torch.float64, 4: torch.float32, 2: torch.bfloat16}.get(itemsize)
     if dtype is None:
         raise DomainError(f"itemsize must be 8, 4 or 2, got {itemsize}")
@@ -219,10 +232,17 @@ def bench_kernel(kind: str, cfg: AttentionConfig, repeats: int, backward: bool =
         _require_lam_one(cfg, "bench of the undecayed kernel")
     dev = _device()
     rng = np.random.default_rng(seed)
-    mats = [torch.from_numpy(rng.standard_normal((cfg.n, cfg.d))).to(dev).to(cfg.torch_dtype)[None, None]
+    tdt = cfg.torch_dtype if kind.startswith("lightning") else torch.float64  # left / right: fp64 baselines
+    mats = [torch.from_numpy(rng.standard_normal((cfg.n, cfg.d))).to(dev).to(tdt)[None, None]
             for _ in range(4 if backward else 3)]
     lam_dev = ops.decay_tensor(cfg.lam, 1, dev)
-    if backward:
+    if kind == "left":
+        call = (lambda: left_product_backward_device(*mats, cfg.lam)) if backward else \
+            (lambda: left_product_forward_device(*mats, cfg.lam))  # noqa: E731
+    elif kind == "right":
+        call = (lambda: right_product_backward_device(*mats, lam_dev)) if backward else \
+            (lambda: right_product_forward_device(*mats, lam_dev))  # noqa: E731
+    elif backward:
         call = lambda: ops.la_backward(*mats, None, lam_dev=lam_dev)  # noqa: E731
     else:
         call = lambda: ops.la_forward(*mats, None, lam_dev=lam_dev)  # noqa: E731
@@ -236,7 +256,57 @@ def bench_kernel(kind: str, cfg: AttentionConfig, repeats: int, backward: bool =
         end.synchronize()
         times.append(int(start.elapsed_time(end) * 1e6))
     med = int(median(times))
-    itemsize = torch.empty(0, dtype=cfg.torch_dtype).element_size()
+    itemsize = torch.empty(0, dtype=tdt).element_size()
     return TimingRecord(kernel=kind, n=cfg.n, d=cfg.d, B=cfg.block, lam=cfg.lam,
                         pass_name="bwd" if backward else "fwd", median_ns=med, per_token_ns=med / cfg.n,
                         aux_bytes=aux_state_bytes(kind, cfg.n, cfg.d, cfg.block, itemsize, backward))
+
+
+# ---------------------------------------------------------------------------
+# the timing harness's baselines on the device (oracles.py:100-162)
+# ---------------------------------------------------------------------------
+
+
+def _decay_mask(n: int, lam: float, like: torch.Tensor) -> torch.Tensor:
+    """M[t, s] = lam^(t-s) for t >= s, else 0 (matrixops.py:122-140), built in fp64."""
+    t = torch.arange(n, device=like.device)
+    diff = (t[:, None] - t[None, :]).to(torch.float64)
+    m = torch.where(diff >= 0, torch.pow(torch.tensor(lam, dtype=torch.float64, device=like.device),
+                                         diff.clamp(min=0)), torch.zeros((), dtype=torch.float64, device=like.device))
+    return m.to(like.dtype)
+
+
+def left_product_forward_device(q, k, v, lam: float):
+    """O = [(Q K^T) * M] V (oracles.py:100-115) with cuBLAS GEMMs; q, k, v [b, h, n, d]."""
+    m = _decay_mask(q.shape[-2], lam, q)
+    return ((q @ k.transpose(-1, -2)) * m) @ v
+
+
+def left_product_backward_device(q, k, v, do, lam: float):
+    """dV = S^T dO, dS = (dO V^T) * M, dQ = dS K, dK = dS^T Q (oracles.py:164-178)."""
+    m = _decay_mask(q.shape[-2], lam, q)
+    sc = (q @ k.transpose(-1, -2)) * m
+    ds = (do @ v.transpose(-1, -2)) * m
+    return ds @ k, ds.transpose(-1, -2) @ q, sc.transpose(-1, -2) @ do
+
+
+def _recurrent_walk(a, b, c, lam_dev, reverse: bool):
+    """out_t = a_t . S_t with S_t = lam S_(t-+1) + b_t c_t^T, one la_decode per position."""
+    bsz, h, n, d = a.shape
+    st = torch.zeros(bsz, h, d, d, dtype=ops.state_dtype(a.dtype), device=a.device)
+    out = torch.empty_like(a)
+    for t in (range(n - 1, -1, -1) if reverse else range(n)):
+        out[:, :, t] = ops.la_decode(a[:, :, t], b[:, :, t], c[:, :, t], None, st, lam_dev=lam_dev)
+    return out
+
+
+def right_product_forward_device(q, k, v, lam_dev):
+    """kv_t = lam kv_(t-1) + k_t v_t^T, o_t = q_t kv_t (oracles.py:118-131)."""
+    return _recurrent_walk(q, k, v, lam_dev, reverse=False)
+
+
+def right_product_backward_device(q, k, v, do, lam_dev):
+    """reference_backward's sweeps (oracles.py:134-161): dq_t = do_t kv_t^T (forward walk over
+    (v, k)), dk_t = v_t dkv_t^T and dv_t = k_t dkv_t (reverse walks over (do, q) and (q, do))."""
+    return (_recurrent_walk(do, v, k, lam_dev, reverse=False), _recurrent_walk(v, do, q, lam_dev, reverse=True),
+            _recurrent_walk(k, q, do, lam_dev, reverse=True))

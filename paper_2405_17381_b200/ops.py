@@ -89,8 +89,18 @@ def _geometry(x: torch.Tensor, layout: str) -> Geometry:
     return Geometry(b, h, n, d, s)
 
 
+def _tc_ready(t: torch.Tensor, layout: str) -> bool:
+    """TMA-describable on the tensor-core path: 16-byte aligned base and (batch, head, position) strides."""
+    return t.data_ptr() % 16 == 0 and all((x * t.element_size()) % 16 == 0 for x in _geometry(t, layout).strides)
+
+
 def _prep(tensors: Sequence[torch.Tensor], names: str, layout: str):
-    """Shape/dtype/device checks; returns tensors sharing one contiguous layout."""
+    """Shape/dtype/device checks (the reference's _prep, kernels.py:133-150, minus its copy-cast).
+
+    Each operand keeps its own strides (la_tensor_strides): a view with a unit feature stride is
+    passed as is.  A copy is made only when the kernels cannot address the view -- a feature
+    stride != 1, or, for bf16 d = 128 operands (the tensor-core path), a base or stride that is no
+    multiple of 16 bytes -- and then only of that operand."""
     first = tensors[0]
     if not isinstance(first, torch.Tensor):
         raise ShapeError(f"{names[0]}: expected a torch.Tensor")
@@ -105,10 +115,34 @@ def _prep(tensors: Sequence[torch.Tensor], names: str, layout: str):
             raise ShapeError(f"{name}: shape {tuple(t.shape)} != {tuple(first.shape)}")
         if t.dtype != first.dtype or t.device != first.device:
             raise ShapeError(f"{name}: dtype/device {t.dtype}/{t.device} != {first.dtype}/{first.device}")
-    # contiguous, 16-byte aligned operands (TMA descriptors need aligned bases)
-    out = [t if (t.is_contiguous() and t.data_ptr() % 16 == 0)
-           else (t.clone() if t.is_contiguous() else t.contiguous()) for t in tensors]  # one copy at most
+    g = _geometry(first, layout)
+    tc = first.dtype == torch.bfloat16 and g.d == 128
+    out = []
+    for t in tensors:
+        if t.dim() == 4 and t.stride(3) != 1 and t.shape[3] > 1:
+            t = t.contiguous()
+        if tc and not _tc_ready(t, layout):
+            t = t.contiguous() if not t.is_contiguous() else t.clone()  # clone: a fresh, aligned base
+        out.append(t)
     return out, _geometry(out[0], layout)
+
+
+def _strides(layout: str, pairs) -> _lib.LaTensorStrides:
+    """la_tensor_strides from (operand index, tensor) pairs."""
+    st = _lib.LaTensorStrides()
+    for idx, t in pairs:
+        if t is None:
+            continue
+        sg = _geometry(t, layout).strides
+        for j in range(3):
+            st.s[idx][j] = sg[j]
+    return st
+
+
+def _out(g: Geometry, like: torch.Tensor, layout: str) -> torch.Tensor:
+    """A fresh contiguous output in the call's layout."""
+    shape = (g.batch, g.heads, g.n, g.d) if layout == "bhnd" else (g.batch, g.n, g.heads, g.d)
+    return torch.empty(shape, dtype=like.dtype, device=like.device)
 
 
 def _desc(g: Geometry, dtype: torch.dtype, block, backend: str, segments: int) -> _lib.LaDesc:
@@ -131,8 +165,24 @@ def _ptr(t):
     return None if t is None else ctypes.c_void_p(t.data_ptr())
 
 
-def _lam_ptr(lam_dev: torch.Tensor):
+def _lam_ptr(lam_dev: torch.Tensor, heads: int, device):
+    """The device decay array the kernels read: must be a contiguous float64 CUDA tensor of `heads`
+    values on the operands' device (decay_tensor builds one); anything else would be misread."""
+    dev = torch.device(device)
+    if (not isinstance(lam_dev, torch.Tensor) or lam_dev.dtype != torch.float64 or not lam_dev.is_cuda
+            or lam_dev.numel() != heads or not lam_dev.is_contiguous()
+            or (dev.index is not None and lam_dev.device != dev)):
+        raise ShapeError(f"lam_dev must be a contiguous float64 CUDA tensor of {heads} values on {device} "
+                         f"(use ops.decay_tensor), got {getattr(lam_dev, 'dtype', type(lam_dev))} "
+                         f"{tuple(getattr(lam_dev, 'shape', ()))} on {getattr(lam_dev, 'device', '?')}")
     return ctypes.cast(ctypes.c_void_p(lam_dev.data_ptr()), ctypes.POINTER(ctypes.c_double))
+
+
+def _lam(lam, lam_dev, heads, device):
+    """(device decay tensor, its pointer): lam_dev as given (validated) or built from host values."""
+    if lam_dev is None:
+        lam_dev = decay_tensor(lam, heads, device)
+    return lam_dev, _lam_ptr(lam_dev, heads, device)
 
 
 def _state(t, g: Geometry, dtype, name):
@@ -144,8 +194,12 @@ def _state(t, g: Geometry, dtype, name):
     return t if t.data_ptr() % 16 == 0 else t.clone()  # the kernels read state rows as 16-byte vectors
 
 
-def _workspace(lib, desc, device):
+def _workspace(lib, desc, device, workspace=None):
     nbytes = lib.la_workspace_bytes(ctypes.byref(desc))
+    if workspace is not None:
+        if workspace.device != torch.device(device) or workspace.numel() * workspace.element_size() < nbytes:
+            raise ShapeError(f"workspace: need {nbytes} bytes on {device}")
+        return workspace, workspace.numel() * workspace.element_size()
     ws = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=device)
     return ws, nbytes
 
@@ -166,19 +220,31 @@ def segment_count(desc) -> int:
     return int(_lib.load().la_segment_count(ctypes.byref(desc)))
 
 
+def _flags(check: bool, resume: bool) -> int:
+    f = _lib.LA_FLAG_RESUME if resume else 0
+    if check:
+        f |= _lib.LA_FLAG_CHECK_DECAY | _lib.LA_FLAG_CHECK_FINITE
+    return f
+
+
 def la_forward(q, k, v, lam, *, block=None, kv_in=None, want_state=False, layout="bhnd",
-               backend="auto", segments=0, lam_dev=None, want_seg_states=False):
+               backend="auto", segments=0, lam_dev=None, want_seg_states=False, check=False, workspace=None,
+               resume=False):
     """o (and kv_out) for batched q, k, v.  ``lam``: float or one value per head.
 
     ``want_seg_states``: also return the state entering every sequence segment (or None when the
     library does not split the sequence) -- pass it to ``la_backward(fwd_seg_states=...)``.
+    ``check``: validate lam and scan q, k, v for NaN / Inf on the device (synchronises; the reference
+    always does both, kernels.py:84-91,148-149).  ``resume`` (with ``workspace``): the workspace holds
+    ``la_forward_state(k, v, ..., workspace=...)``'s summaries for this problem, so the summary pass is
+    skipped (sequence parallelism).
     """
     (q, k, v), g = _prep([q, k, v], "QKV", layout)
     lib = _lib.load()
     desc = _desc(g, q.dtype, block, backend, segments)
-    lam_dev = decay_tensor(lam, g.heads, q.device) if lam_dev is None else lam_dev
+    lam_dev, lam_p = _lam(lam, lam_dev, g.heads, q.device)
     kv_in = _state(kv_in, g, q.dtype, "kv_in")
-    o = torch.empty_like(q)
+    o = _out(g, q, layout)
     kv_out = torch.empty((g.batch, g.heads, g.d, g.d), dtype=state_dtype(q.dtype), device=q.device) \
         if want_state else None
     seg = None
@@ -186,29 +252,45 @@ def la_forward(q, k, v, lam, *, block=None, kv_in=None, want_state=False, layout
         nseg = segment_count(desc)
         if nseg > 1:
             seg = torch.empty((g.batch, g.heads, nseg, g.d, g.d), dtype=state_dtype(q.dtype), device=q.device)
-    ws, nbytes = _workspace(lib, desc, q.device)
-    _lib.check(lib.la_fwd(ctypes.byref(desc), _ptr(q), _ptr(k), _ptr(v), _lam_ptr(lam_dev), _ptr(kv_in),
-                          _ptr(o), _ptr(kv_out), _ptr(seg), _ptr(ws), nbytes, _stream(q.device)))
+    if resume and workspace is None:
+        raise ShapeError("resume=True needs the workspace la_forward_state filled")
+    ws, nbytes = _workspace(lib, desc, q.device, workspace)
+    st = _strides(layout, ((_lib.LA_T_Q, q), (_lib.LA_T_K, k), (_lib.LA_T_V, v), (_lib.LA_T_O, o)))
+    _lib.check(lib.la_fwd_ex(ctypes.byref(desc), ctypes.byref(st), _flags(check, resume), _ptr(q), _ptr(k), _ptr(v),
+                             lam_p, _ptr(kv_in), _ptr(o), _ptr(kv_out), _ptr(seg), _ptr(ws), nbytes,
+                             _stream(q.device)))
     out = (o, kv_out) if want_state else o
     return (out, seg) if want_seg_states else out
 
 
+_PARTS = {"all": 0, "dq": _lib.LA_FLAG_NO_DKDV, "dkdv": _lib.LA_FLAG_NO_DQ}
+
+
 def la_backward(q, k, v, do, lam, *, block=None, kv_in=None, dkv_in=None, want_state=False, layout="bhnd",
-                backend="auto", segments=0, lam_dev=None, fwd_seg_states=None):
+                backend="auto", segments=0, lam_dev=None, fwd_seg_states=None, check=False, parts="all",
+                workspace=None, resume=False):
     """(dq, dk, dv) (and dkv_out = R(0)) of <LA(q, k, v), do>.
 
     ``fwd_seg_states``: the forward's segment states for the same problem and kv_in (optional).
+    ``parts``: "all", "dq" (sweep 1 only; dk, dv come back None) or "dkdv" (sweep 2 only; dq None).
+    ``resume`` (with ``workspace``): the workspace holds ``la_backward_state(q, do, ...,
+    workspace=...)``'s adjoint summaries, so sweep 2 skips its summary pass.
     """
+    if parts not in _PARTS:
+        raise DomainError(f"parts must be one of {sorted(_PARTS)}, got {parts!r}")
     (q, k, v, do), g = _prep([q, k, v, do], ["Q", "K", "V", "dO"], layout)
     lib = _lib.load()
     desc = _desc(g, q.dtype, block, backend, segments)
-    lam_dev = decay_tensor(lam, g.heads, q.device) if lam_dev is None else lam_dev
+    lam_dev, lam_p = _lam(lam, lam_dev, g.heads, q.device)
     kv_in = _state(kv_in, g, q.dtype, "kv_in")
     dkv_in = _state(dkv_in, g, q.dtype, "dkv_in")
-    dq, dk, dv = torch.empty_like(q), torch.empty_like(q), torch.empty_like(q)
+    dq = _out(g, q, layout) if parts != "dkdv" else None
+    dk, dv = (_out(g, q, layout), _out(g, q, layout)) if parts != "dq" else (None, None)
     dkv_out = torch.empty((g.batch, g.heads, g.d, g.d), dtype=state_dtype(q.dtype), device=q.device) \
-        if want_state else None
-    ws, nbytes = _workspace(lib, desc, q.device)
+        if (want_state and parts != "dq") else None
+    if resume and workspace is None:
+        raise ShapeError("resume=True needs the workspace la_backward_state filled")
+    ws, nbytes = _workspace(lib, desc, q.device, workspace)
     if fwd_seg_states is not None:
         want = (g.batch, g.heads, segment_count(desc), g.d, g.d)
         if tuple(fwd_seg_states.shape) != want:
@@ -217,34 +299,50 @@ def la_backward(q, k, v, do, lam, *, block=None, kv_in=None, dkv_in=None, want_s
         if fwd_seg_states.dtype != state_dtype(q.dtype) or fwd_seg_states.device != q.device \
                 or not fwd_seg_states.is_contiguous():
             raise ShapeError(f"fwd_seg_states must be a contiguous {state_dtype(q.dtype)} tensor on {q.device}")
-    _lib.check(lib.la_bwd(ctypes.byref(desc), _ptr(q), _ptr(k), _ptr(v), _ptr(do), _lam_ptr(lam_dev),
-                          _ptr(kv_in), _ptr(dkv_in), _ptr(fwd_seg_states), _ptr(dq), _ptr(dk), _ptr(dv),
-                          _ptr(dkv_out), _ptr(ws), nbytes, _stream(q.device)))
+    st = _strides(layout, ((_lib.LA_T_Q, q), (_lib.LA_T_K, k), (_lib.LA_T_V, v), (_lib.LA_T_DO, do),
+                           (_lib.LA_T_DQ, dq), (_lib.LA_T_DK, dk), (_lib.LA_T_DV, dv)))
+    _lib.check(lib.la_bwd_ex(ctypes.byref(desc), ctypes.byref(st), _flags(check, resume) | _PARTS[parts], _ptr(q),
+                             _ptr(k), _ptr(v), _ptr(do), lam_p, _ptr(kv_in), _ptr(dkv_in), _ptr(fwd_seg_states),
+                             _ptr(dq), _ptr(dk), _ptr(dv), _ptr(dkv_out), _ptr(ws), nbytes, _stream(q.device)))
     return (dq, dk, dv, dkv_out) if want_state else (dq, dk, dv)
 
 
-def la_forward_state(k, v, lam, *, layout="bhnd", backend="auto", segments=0, lam_dev=None):
-    """Local forward summary sum_s lam^(n-1-s) k_s v_s^T, [batch, heads, d, d]."""
+def new_workspace(shape, dtype=torch.bfloat16, *, layout="bhnd", backend="auto", segments=0, device="cuda"):
+    """A workspace for ``la_forward_state`` -> ``la_forward(resume=True)`` (or the backward pair)."""
+    return torch.empty(max(workspace_bytes(shape, dtype, layout=layout, backend=backend, segments=segments), 1),
+                       dtype=torch.uint8, device=device)
+
+
+def la_forward_state(k, v, lam, *, layout="bhnd", backend="auto", segments=0, lam_dev=None, workspace=None):
+    """Local forward summary sum_s lam^(n-1-s) k_s v_s^T, [batch, heads, d, d].  With ``workspace``
+    the per-segment summaries stay there for ``la_forward(..., workspace=..., resume=True)``."""
     (k, v), g = _prep([k, v], "KV", layout)
+    if _geometry(v, layout).strides != g.strides:  # la_fwd_state addresses both with the desc's strides
+        k, v = k.contiguous(), v.contiguous()
+        g = _geometry(k, layout)
     lib = _lib.load()
     desc = _desc(g, k.dtype, None, backend, segments)
-    lam_dev = decay_tensor(lam, g.heads, k.device) if lam_dev is None else lam_dev
+    lam_dev, lam_p = _lam(lam, lam_dev, g.heads, k.device)
     out = torch.empty((g.batch, g.heads, g.d, g.d), dtype=state_dtype(k.dtype), device=k.device)
-    ws, nbytes = _workspace(lib, desc, k.device)
-    _lib.check(lib.la_fwd_state(ctypes.byref(desc), _ptr(k), _ptr(v), _lam_ptr(lam_dev), _ptr(out), _ptr(ws),
+    ws, nbytes = _workspace(lib, desc, k.device, workspace)
+    _lib.check(lib.la_fwd_state(ctypes.byref(desc), _ptr(k), _ptr(v), lam_p, _ptr(out), _ptr(ws),
                                 nbytes, _stream(k.device)))
     return out
 
 
-def la_backward_state(q, do, lam, *, layout="bhnd", backend="auto", segments=0, lam_dev=None):
-    """Local adjoint summary sum_t lam^(t+1) q_t do_t^T, [batch, heads, d, d]."""
+def la_backward_state(q, do, lam, *, layout="bhnd", backend="auto", segments=0, lam_dev=None, workspace=None):
+    """Local adjoint summary sum_t lam^(t+1) q_t do_t^T, [batch, heads, d, d].  With ``workspace`` the
+    per-segment summaries stay there for ``la_backward(..., workspace=..., resume=True)``."""
     (q, do), g = _prep([q, do], ["Q", "dO"], layout)
+    if _geometry(do, layout).strides != g.strides:  # la_bwd_state addresses both with the desc's strides
+        q, do = q.contiguous(), do.contiguous()
+        g = _geometry(q, layout)
     lib = _lib.load()
     desc = _desc(g, q.dtype, None, backend, segments)
-    lam_dev = decay_tensor(lam, g.heads, q.device) if lam_dev is None else lam_dev
+    lam_dev, lam_p = _lam(lam, lam_dev, g.heads, q.device)
     out = torch.empty((g.batch, g.heads, g.d, g.d), dtype=state_dtype(q.dtype), device=q.device)
-    ws, nbytes = _workspace(lib, desc, q.device)
-    _lib.check(lib.la_bwd_state(ctypes.byref(desc), _ptr(q), _ptr(do), _lam_ptr(lam_dev), _ptr(out), _ptr(ws),
+    ws, nbytes = _workspace(lib, desc, q.device, workspace)
+    _lib.check(lib.la_bwd_state(ctypes.byref(desc), _ptr(q), _ptr(do), lam_p, _ptr(out), _ptr(ws),
                                 nbytes, _stream(q.device)))
     return out
 
@@ -292,9 +390,9 @@ def la_decode(q, k, v, lam, kv, *, lam_dev=None):
         raise ShapeError(f"kv: expected a contiguous {state_dtype(q.dtype)} tensor on {q.device} (updated in place)")
     lib = _lib.load()
     desc = _desc(g, q4.dtype, None, "auto", 0)
-    lam_dev = decay_tensor(lam, g.heads, q.device) if lam_dev is None else lam_dev
+    lam_dev, lam_p = _lam(lam, lam_dev, g.heads, q.device)
     o = torch.empty_like(q4)
-    _lib.check(lib.la_decode(ctypes.byref(desc), _ptr(q4), _ptr(k4), _ptr(v4), _lam_ptr(lam_dev), _ptr(kv), _ptr(o),
+    _lib.check(lib.la_decode(ctypes.byref(desc), _ptr(q4), _ptr(k4), _ptr(v4), lam_p, _ptr(kv), _ptr(o),
                              _stream(q.device)))
     return o.squeeze(2)
 

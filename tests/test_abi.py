@@ -27,7 +27,7 @@ def test_library_exports_every_declared_symbol():
     lib = _lib.load()
     for name in _declared():
         assert hasattr(lib, name), name
-    assert lib.la_abi_version() == _lib.ABI_VERSION == 2
+    assert lib.la_abi_version() == _lib.ABI_VERSION == 3
     assert b"sm_100a" in lib.la_build_info()
 
 
@@ -59,6 +59,9 @@ def _fwd(desc):
     (dict(batch=0), _lib.LA_ERR_SHAPE),
     (dict(stride=(0, 0, 3)), _lib.LA_ERR_SHAPE),
     (dict(d=256), _lib.LA_ERR_UNSUPPORTED),
+    (dict(segments=70000), _lib.LA_ERR_UNSUPPORTED),      # beyond the workspace's segment bound
+    (dict(n=2 ** 31), _lib.LA_ERR_UNSUPPORTED),           # int positions
+    (dict(segments=-1), _lib.LA_ERR_DOMAIN),
     (dict(dtype=_lib.LA_F64, backend=_lib.LA_BACKEND_TCGEN05), _lib.LA_ERR_UNSUPPORTED),
 ])
 def test_descriptor_validation(kw, code):
@@ -111,3 +114,61 @@ def test_decay_tensor_is_validated_once_and_cached():
             ops.decay_tensor(bad, 2, "cpu")
     with pytest.raises(ShapeError):
         ops.decay_tensor([0.9, 0.5, 0.4], 2, "cpu")
+
+
+def test_check_decay_host_entry_matches_reference_check_decay():
+    """la_check_decay: the reference's check_decay (matrixops.py:72-77) on a host array."""
+    lib = _lib.load()
+    arr = lambda *v: (ctypes.c_double * len(v))(*v)  # noqa: E731
+    assert lib.la_check_decay(arr(1.0, 0.5, 5.5e-4), 3) == _lib.LA_OK
+    for bad in (1.5, 0.0, -0.2, float("nan"), float("inf")):
+        assert lib.la_check_decay(arr(0.9, bad), 2) == _lib.LA_ERR_DOMAIN
+        assert b"(0, 1]" in lib.la_last_error()
+    assert lib.la_check_decay(None, 2) == _lib.LA_ERR_SHAPE
+
+
+def _fwd_ex(desc, strides=None, flags=0):
+    lib = _lib.load()
+    dummy = ctypes.c_void_p(16)
+    lam = ctypes.cast(ctypes.c_void_p(16), ctypes.POINTER(ctypes.c_double))
+    sp = ctypes.byref(strides) if strides is not None else None
+    return lib.la_fwd_ex(ctypes.byref(desc), sp, flags, dummy, dummy, dummy, lam, None, dummy, None, None, None, 0,
+                         None)
+
+
+def test_extended_entry_validation():
+    """la_fwd_ex / la_bwd_ex reject unknown or misplaced flags and bad per-operand strides before any
+    device work."""
+    lib = _lib.load()
+    assert _fwd_ex(_desc(), flags=0x400) == _lib.LA_ERR_DOMAIN
+    assert _fwd_ex(_desc(), flags=_lib.LA_FLAG_NO_DQ) == _lib.LA_ERR_DOMAIN  # backward-only flag
+    st = _lib.LaTensorStrides()
+    for i in range(8):
+        st.s[i][0], st.s[i][1], st.s[i][2] = 2 * 64 * 16, 64 * 16, 16
+    st.s[_lib.LA_T_V][2] = 8  # position stride < d
+    assert _fwd_ex(_desc(), st) == _lib.LA_ERR_SHAPE
+    assert b"operand 2" in lib.la_last_error()
+    st.s[_lib.LA_T_V][2] = 16
+    st.s[_lib.LA_T_K][0] = -1
+    assert _fwd_ex(_desc(), st) == _lib.LA_ERR_SHAPE
+    dummy = ctypes.c_void_p(16)
+    lam = ctypes.cast(ctypes.c_void_p(16), ctypes.POINTER(ctypes.c_double))
+    # NO_DKDV without dq, RESUME on a split problem without the forward's segment states
+    long_ = _desc(batch=1, heads=16, n=1 << 17, d=128, dtype=_lib.LA_BF16)
+    ws = ctypes.create_string_buffer(lib.la_workspace_bytes(ctypes.byref(long_)) + 16)
+    wsp = ctypes.c_void_p((ctypes.addressof(ws) + 15) // 16 * 16)
+    rc = lib.la_bwd_ex(ctypes.byref(long_), None, _lib.LA_FLAG_NO_DKDV, dummy, dummy, dummy, dummy, lam, None, None,
+                       None, None, None, None, None, wsp, len(ws) - 16, None)
+    assert rc == _lib.LA_ERR_SHAPE
+    rc = lib.la_bwd_ex(ctypes.byref(long_), None, _lib.LA_FLAG_RESUME, dummy, dummy, dummy, dummy, lam, None, None,
+                       None, dummy, dummy, dummy, None, wsp, len(ws) - 16, None)
+    assert rc == _lib.LA_ERR_SHAPE and b"fwd_seg_states" in lib.la_last_error()
+
+
+def test_workspace_covers_every_backend_plan():
+    """An _ex call whose operand strides rule out TMA runs the SIMT plan: la_workspace_bytes covers it."""
+    lib = _lib.load()
+    for n in (1 << 12, 1 << 16):
+        tc = _desc(batch=1, heads=4, n=n, d=128, dtype=_lib.LA_BF16)
+        simt = _desc(batch=1, heads=4, n=n, d=128, dtype=_lib.LA_BF16, backend=_lib.LA_BACKEND_SIMT)
+        assert lib.la_workspace_bytes(ctypes.byref(tc)) >= lib.la_workspace_bytes(ctypes.byref(simt))

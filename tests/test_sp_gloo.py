@@ -31,23 +31,31 @@ class OracleKernels:
         lams = lam.tolist()
         z = np.zeros_like(self._np(k))
         _, kv = orc.batched_forward(z, self._np(k), self._np(v), lams)
-        return torch.from_numpy(kv)
+        return torch.from_numpy(kv), None
+
+    def forward(self, q, k, v, lam, kv_in, ctx):
+        o, _ = orc.batched_forward(self._np(q), self._np(k), self._np(v), lam.tolist(),
+                                   kv_in=self._np(kv_in))
+        return torch.from_numpy(o), None
 
     def backward_state(self, q, do, lam):
         lams = lam.tolist()
         z = np.zeros_like(self._np(q))
         _, dkv = orc.batched_backward(self._np(q), z, z, self._np(do), lams)
-        return torch.from_numpy(dkv)
+        return torch.from_numpy(dkv), None
 
-    def forward(self, q, k, v, lam, kv_in):
-        o, _ = orc.batched_forward(self._np(q), self._np(k), self._np(v), lam.tolist(),
-                                   kv_in=self._np(kv_in))
-        return torch.from_numpy(o)
+    def begin_dq(self, q, k, v, do, lam, kv_in, seg):
+        (dq, _, _), _ = orc.batched_backward(self._np(q), self._np(k), self._np(v), self._np(do), lam.tolist(),
+                                             kv_in=self._np(kv_in))
+        return torch.from_numpy(dq)
 
-    def backward(self, q, k, v, do, lam, kv_in, dkv_in):
-        (dq, dk, dv), _ = orc.batched_backward(self._np(q), self._np(k), self._np(v), self._np(do), lam.tolist(),
-                                               kv_in=self._np(kv_in), dkv_in=self._np(dkv_in))
-        return torch.from_numpy(dq), torch.from_numpy(dk), torch.from_numpy(dv)
+    def backward_dkdv(self, q, k, v, do, lam, dkv_in, ctx):
+        (_, dk, dv), _ = orc.batched_backward(self._np(q), self._np(k), self._np(v), self._np(do), lam.tolist(),
+                                              dkv_in=self._np(dkv_in))
+        return torch.from_numpy(dk), torch.from_numpy(dv)
+
+    def finish_dq(self, handle):
+        return handle
 
 
 def _free_port():
@@ -56,7 +64,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, cuts, q, k, v, do, lams, result_q):
+def _worker(rank, world, port, cuts, q, k, v, do, lams, result_q, exchange="gather"):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -68,16 +76,19 @@ def _worker(rank, world, port, cuts, q, k, v, do, lams, result_q):
         ql, kl, vl = sl(q), sl(k), sl(v)
         lam = torch.tensor(lams, dtype=torch.float64)
         # the last cut pattern passes the slice lengths (no lengths exchange); the others exchange them
-        known = [cuts[i + 1] - cuts[i] for i in range(world)] if cuts == (0, 1, 50) else None
-        o = sp_lightning_attention(ql, kl, vl, lam, kernels=OracleKernels(), lengths=known)
+        known = [cuts[i + 1] - cuts[i] for i in range(world)] if cuts in ((0, 1, 50), (0, 20, 21, 60)) else None
+        o = sp_lightning_attention(ql, kl, vl, lam, kernels=OracleKernels(), lengths=known, exchange=exchange)
         o.backward(do[:, :, lo:hi])
         result_q.put((rank, o.detach().numpy(), ql.grad.numpy(), kl.grad.numpy(), vl.grad.numpy()))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("cuts", [(0, 48, 96), (0, 37, 97), (0, 1, 50)])
-def test_sequence_parallel_two_ranks_matches_whole_sequence(cuts):
+@pytest.mark.parametrize("exchange", ["gather", "chain"])
+@pytest.mark.parametrize("cuts", [(0, 48, 96), (0, 37, 97), (0, 1, 50), (0, 20, 21, 60)])
+def test_sequence_parallel_ranks_match_whole_sequence(cuts, exchange):
+    """World size 2 (and 3 for the 4-cut pattern, with a one-position middle slice) under gloo: the
+    all_gather combine and the P2P neighbour chain both reproduce the unsplit sequence."""
     rng = np.random.default_rng(sum(cuts))
     b, h, d = 2, 3, 8
     n = cuts[-1]
@@ -85,9 +96,10 @@ def test_sequence_parallel_two_ranks_matches_whole_sequence(cuts):
     q, k, v, do = (torch.from_numpy(rng.uniform(0.05, 1.0, (b, h, n, d))) for _ in range(4))
     ctx = mp.get_context("spawn")
     result_q = ctx.Queue()
-    world = 2
+    world = len(cuts) - 1
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, cuts, q, k, v, do, lams, result_q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, cuts, q, k, v, do, lams, result_q, exchange))
+             for r in range(world)]
     for p in procs:
         p.start()
     results = dict((r[0], r[1:]) for r in (result_q.get(timeout=240) for _ in range(world)))
