@@ -89,13 +89,15 @@ struct OpStrides {
   la::Strides3 s[8];
 };
 
-int op_strides(const la_desc* desc, const la_tensor_strides* ts, std::initializer_list<int> used, OpStrides* out) {
+// `used`: bitmask of the la_operand slots this call reads or writes
+int op_strides(const la_desc* desc, const la_tensor_strides* ts, unsigned used, OpStrides* out) {
   for (int i = 0; i < 8; ++i) {
     const int64_t* src = ts != nullptr ? ts->s[i] : desc->stride;
     out->s[i] = la::Strides3{src[0], src[1], src[2]};
   }
   if (ts != nullptr)
-    for (int i : used) {
+    for (int i = 0; i < 8; ++i) {
+      if (!(used >> i & 1u)) continue;
       const la::Strides3& x = out->s[i];
       if (x.b < 0 || x.h < 0 || x.n < 0) return fail(LA_ERR_SHAPE, "operand %d: negative stride", i);
       if (x.n < desc->d) return fail(LA_ERR_SHAPE, "operand %d: position stride %lld < d", i, (long long)x.n);
@@ -104,11 +106,11 @@ int op_strides(const la_desc* desc, const la_tensor_strides* ts, std::initialize
 }
 
 // Which backend serves this descriptor (and, for the _ex calls, these operand strides).
-int pick_backend(const la_desc* desc, int* backend, const OpStrides* ops = nullptr,
-                 std::initializer_list<int> used = {}) {
+int pick_backend(const la_desc* desc, int* backend, const OpStrides* ops = nullptr, unsigned used = 0) {
   bool tc_ok = la::tc_supported(desc->dtype, (int)desc->d, desc->stride, 1);
   if (ops != nullptr)
-    for (int i : used) {
+    for (int i = 0; i < 8; ++i) {
+      if (!(used >> i & 1u)) continue;
       const int64_t t[3] = {ops->s[i].b, ops->s[i].h, ops->s[i].n};
       tc_ok = tc_ok && la::tc_supported(desc->dtype, (int)desc->d, t, 1);
     }
@@ -292,7 +294,7 @@ struct Prepared {
 };
 
 int prepare(const la_desc* desc, size_t ws_bytes, const void* ws, Prepared* out, const OpStrides* ops = nullptr,
-            std::initializer_list<int> used = {}) {
+            unsigned used = 0) {
   int rc = validate(desc);
   if (rc != LA_OK) return rc;
   rc = pick_backend(desc, &out->backend, ops, used);
@@ -434,10 +436,11 @@ int la_fwd_ex(const la_desc* desc, const la_tensor_strides* strides, uint32_t fl
   if (flags & (LA_FLAG_NO_DQ | LA_FLAG_NO_DKDV)) return fail(LA_ERR_DOMAIN, "la_fwd_ex: backward-only flags");
   if (desc == nullptr) return fail(LA_ERR_SHAPE, "null descriptor");
   OpStrides os;
-  int rc = op_strides(desc, strides, {LA_T_Q, LA_T_K, LA_T_V, LA_T_O}, &os);
+  const unsigned used = 1u << LA_T_Q | 1u << LA_T_K | 1u << LA_T_V | 1u << LA_T_O;
+  int rc = op_strides(desc, strides, used, &os);
   if (rc != LA_OK) return rc;
   Prepared pr;
-  rc = prepare(desc, workspace_bytes, workspace, &pr, &os, {LA_T_Q, LA_T_K, LA_T_V, LA_T_O});
+  rc = prepare(desc, workspace_bytes, workspace, &pr, &os, used);
   if (rc != LA_OK) return rc;
   if (!q || !k || !v || !o || !lam) return fail(LA_ERR_SHAPE, "la_fwd: null q/k/v/o/lam");
   if (!states_aligned({kv_in, kv_out, seg_states_out}))
@@ -486,7 +489,8 @@ int la_bwd_ex(const la_desc* desc, const la_tensor_strides* strides, uint32_t fl
   if (desc == nullptr) return fail(LA_ERR_SHAPE, "null descriptor");
   const bool want_dq = !(flags & LA_FLAG_NO_DQ), want_dkdv = !(flags & LA_FLAG_NO_DKDV);
   OpStrides os;
-  const std::initializer_list<int> used = {LA_T_Q, LA_T_K, LA_T_V, LA_T_DO, LA_T_DQ, LA_T_DK, LA_T_DV};
+  const unsigned used = 1u << LA_T_Q | 1u << LA_T_K | 1u << LA_T_V | 1u << LA_T_DO | (want_dq ? 1u << LA_T_DQ : 0u) |
+                        (want_dkdv ? (1u << LA_T_DK | 1u << LA_T_DV) : 0u);
   int rc = op_strides(desc, strides, used, &os);
   if (rc != LA_OK) return rc;
   Prepared pr;

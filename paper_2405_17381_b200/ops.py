@@ -383,7 +383,9 @@ def la_decode(q, k, v, lam, kv, *, lam_dev=None):
     for t, name in ((q, "Q"), (k, "K"), (v, "V")):
         if not isinstance(t, torch.Tensor) or t.dim() != 3:
             raise ShapeError(f"{name}: expected a [batch, heads, d] tensor")
-    (q4, k4, v4), g = _prep([q.unsqueeze(2), k.unsqueeze(2), v.unsqueeze(2)], "QKV", "bhnd")
+    # la_decode addresses q, k, v and o with the desc's one (batch, head) stride pair: one dense layout
+    (q4, k4, v4), g = _prep([q.contiguous().unsqueeze(2), k.contiguous().unsqueeze(2), v.contiguous().unsqueeze(2)],
+                            "QKV", "bhnd")
     if not isinstance(kv, torch.Tensor) or kv.shape != (g.batch, g.heads, g.d, g.d):
         raise ShapeError(f"kv: expected shape {(g.batch, g.heads, g.d, g.d)}")
     if kv.dtype != state_dtype(q.dtype) or not kv.is_contiguous() or kv.device != q.device:
