@@ -60,6 +60,19 @@ template <> struct Cvt<__nv_bfloat16> {
   __device__ __forceinline__ static __nv_bfloat16 from_f(float x) { return __float2bfloat16_rn(x); }
 };
 
+// Scan-order liveness of summary sub-segment j of a segment whose last sub-segment is `last` (la_scan.cu):
+// a sub-segment reaches an entering state only through the decays lam^len of the sub-segments after it in
+// scan order (fwd: higher j, rev: lower j) within its segment.  When one of those factors is exactly 0 in
+// the accumulation type, the scan's  s = dec * s + delta  discards it exactly (states are finite), so
+// neither the summary pass nor the scan touch it.  zero_full: (Tacc)lam^sub_len == 0 (every sub-segment but
+// a segment's last is full); zero_last: (Tacc)lam^len(last) == 0.  Short-memory heads (e.g. TNL's lower
+// layers, lam <= 0.63) thereby summarise only the tail of each segment -- the same arithmetic result.
+__device__ __forceinline__ bool sub_dead(int j, int last, int rev, bool zero_full, bool zero_last) {
+  if (rev) return j > 0 && zero_full;
+  if (j >= last) return false;
+  return (j + 1 < last && zero_full) || zero_last;
+}
+
 // Element strides of one operand: batch, head, position (the feature stride is 1).
 struct Strides3 {
   int64_t b, h, n;

@@ -10,7 +10,8 @@ namespace {
 //   fwd: in[0] = user (or 0);    walking g, j upwards:   s = lam^len(g,j) s + delta[g][j]
 //   rev: in[last] = user (or 0); walking g, j downwards: same
 // seg_in[g] = s on entering segment g.  `final_out` (nullable; needs every segment summarised) receives
-// the inclusive total (F(n) / R(0)).
+// the inclusive total (F(n) / R(0)).  Sub-segments whose contribution a later factor lam^len == 0 discards
+// exactly (sub_dead, la_common.cuh) are neither summarised nor read: they count as zero.
 constexpr int kScanThreads = 128;
 constexpr int kBatch = 8;  // sub-segment loads in flight per thread
 
@@ -30,6 +31,7 @@ __global__ void __launch_bounds__(kScanThreads) segment_scan_kernel(
   // short last one -- three pow()s per block instead of one per sub-segment
   __shared__ Tacc s_pow[3];
   __shared__ int s_len[3];
+  __shared__ int s_last_full, s_last_seq, s_gl;  // last sub-segment index of a full segment / of the last one
   const int bh = blockIdx.y;
   const int nsub = nseg * sub_per_seg;
   auto sub_range = [&](int kk, int& p0, int& p1) {
@@ -49,8 +51,22 @@ __global__ void __launch_bounds__(kScanThreads) segment_scan_kernel(
     }
     s_len[threadIdx.x] = len;
     s_pow[threadIdx.x] = (Tacc)pow(load_decay(lam, bh % heads), (double)len);
+    if (threadIdx.x == 0) {
+      s_last_full = last_in_seg;
+      s_gl = (n - 1) / seg_len;
+      s_last_seq = (n - 1 - s_gl * seg_len) / sub_len;
+    }
   }
   __syncthreads();
+  const bool zero_full = s_pow[0] == (Tacc)0;
+  // slot kk contributes nothing (never summarised) -- see sub_dead
+  auto dead = [&](int kk) {
+    const int g = kk / sub_per_seg, j = kk % sub_per_seg;
+    const bool lastseg = g == s_gl;
+    const int last = lastseg ? s_last_seq : s_last_full;
+    const bool zero_last = (lastseg ? s_pow[2] : s_pow[1]) == (Tacc)0;
+    return sub_dead(j, last, rev, zero_full, zero_last);
+  };
   const int dd = d * d;
   const int e0 = (blockIdx.x * kScanThreads + threadIdx.x) * V;
   if (e0 >= dd) return;
@@ -75,7 +91,7 @@ __global__ void __launch_bounds__(kScanThreads) segment_scan_kernel(
       const int g = kk / sub_per_seg;
       int p0, p1;
       sub_range(kk, p0, p1);
-      if (k < nsub && g >= g_lo && g <= g_hi && p1 > p0)
+      if (k < nsub && g >= g_lo && g <= g_hi && p1 > p0 && !dead(kk))
         x[u] = *reinterpret_cast<const Vec*>(dcol + (int64_t)kk * dd);
       else
 #pragma unroll

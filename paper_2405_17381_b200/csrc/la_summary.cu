@@ -68,9 +68,47 @@ __global__ void __launch_bounds__(S_THREADS, 2)
   const int slot = g * args.sub_per_seg + j;
   const int p0 = g * args.seg_len + j * args.sub_len;
   const int p1 = min(min(args.n, (g + 1) * args.seg_len), p0 + args.sub_len);
-  const int nchunks = p1 > p0 ? (p1 - p0 + SC - 1) / SC : 0;
+  const int nchunks_all = p1 > p0 ? (p1 - p0 + SC - 1) / SC : 0;
   const int rev = args.rev;
-  if (nchunks == 0) return;  // uniform across the CTA: an empty sub-segment (past n) writes nothing
+  if (nchunks_all == 0) return;  // uniform across the CTA: an empty sub-segment (past n) writes nothing
+  // Work whose contribution is exactly zero is skipped (the same arithmetic result, uniform across the CTA):
+  // a sub-segment that a later factor lam^len == 0 discards in the scan (sub_dead: its slot is never read),
+  // and, in a live one, the chunks whose largest weight rounds to zero in bf16 (their B~ rows are all zero).
+  // Short-memory heads thereby summarise ~one chunk per segment instead of the whole segment.
+  const double lamv = load_decay(args.lam, hi);
+  int t_beg = 0, t_end = nchunks_all;
+  {
+    const int seg_end = min(args.n, (g + 1) * args.seg_len);
+    const int last = (seg_end - 1 - g * args.seg_len) / args.sub_len;
+    const int last_len = seg_end - (g * args.seg_len + last * args.sub_len);
+    const bool zero_full = (float)pow(lamv, (double)args.sub_len) == 0.f;
+    const bool zero_last = (float)pow(lamv, (double)last_len) == 0.f;
+    if (sub_dead(j, last, rev, zero_full, zero_last)) return;
+    // largest weight of chunk t: fwd at its last row, lam^(p1 - min(p1, r0 + SC)); rev at its first, lam^(r0 - p0 + 1)
+    auto live = [&](int t) {
+      const int r0 = p0 + t * SC;
+      const int e = rev ? r0 - p0 + 1 : p1 - min(p1, r0 + SC);
+      return (__bfloat16_as_ushort(__float2bfloat16_rn((float)pow(lamv, (double)e))) & 0x7fff) != 0;
+    };
+    // live(t) is monotone in t (rising for fwd, falling for rev): bisect the boundary
+    if (!rev) {
+      int lo = 0, hi2 = nchunks_all - 1;  // the last chunk is always live (weight 1 at the edge)
+      while (lo < hi2) {
+        const int mid = (lo + hi2) >> 1;
+        if (live(mid)) hi2 = mid; else lo = mid + 1;
+      }
+      t_beg = lo;
+    } else {
+      int lo = 0, hi2 = nchunks_all - 1;  // chunk 0 is always live
+      while (lo < hi2) {
+        const int mid = (lo + hi2 + 1) >> 1;
+        if (live(mid)) lo = mid; else hi2 = mid - 1;
+      }
+      t_end = lo + 1;
+    }
+  }
+  const int nchunks = t_end - t_beg;          // the chunks walked: t_beg .. t_end - 1
+  const int q0 = p0 + t_beg * SC;             // first row walked
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < SNST; ++s) {
@@ -86,7 +124,7 @@ __global__ void __launch_bounds__(S_THREADS, 2)
     tma_prefetch(&map_b);
     tma_prefetch(&map_c);
     for (int t = 0; t < early; ++t) {  // no empty-slot wait for the first stages
-      const int r0 = p0 + t * SC;
+      const int r0 = q0 + t * SC;
       mbar_arrive_expect_tx(&bars.full[t], 2 * STILE);
       uint8_t* gb = smem_gen + (size_t)t * 2 * STILE;
       tma_load_4d(&map_b, &bars.full[t], gb, 0, r0, hi, bi);
@@ -106,7 +144,7 @@ __global__ void __launch_bounds__(S_THREADS, 2)
       for (int t = early; t < nchunks; ++t) {
         const int s = t % SNST;
         if (t >= SNST) mbar_wait(&bars.empty[s], ((t / SNST) - 1) & 1);
-        const int r0 = p0 + t * SC;
+        const int r0 = q0 + t * SC;
         mbar_arrive_expect_tx(&bars.full[s], 2 * STILE);
         uint8_t* gb = smem_gen + (size_t)s * 2 * STILE;
         tma_load_4d(&map_b, &bars.full[s], gb, 0, r0, hi, bi);
@@ -137,10 +175,10 @@ __global__ void __launch_bounds__(S_THREADS, 2)
     const int tid = threadIdx.x - 64;     // 0..127
     const int i = tid & (SC - 1);         // chunk row
     const int hh = tid >> 6;              // column half
-    const double lam = load_decay(args.lam, hi);
+    const double lam = lamv;
     for (int t = 0; t < nchunks; ++t) {
       const int s = t % SNST;
-      const int r0 = p0 + t * SC;
+      const int r0 = q0 + t * SC;
       const int b = min(SC, p1 - r0);
       mbar_wait(&bars.full[s], (t / SNST) & 1);
       // fwd lam^(p1-1-s), rev lam^(s-p0+1); rows past the sub-segment (tail) contribute nothing
