@@ -421,6 +421,35 @@ def measure_rows(ops, device, stream, pk) -> dict:
                                                 / (pk["bf16_tflops"] * 1e12), 2)}
         del qq, kk, vv, dd
     out["tnl7b_attention_1gpu"] = cfg7
+    # the headline sweep's shape with LONG-memory decays (layer 15 of 16: lam_h = exp(-h/32), 0.97 .. 0.61):
+    # the summary pass can skip nothing for the slow heads (la_summary.cu), so this is the general-case curve
+    lam_long = ops.decay_tensor([decay_rate(h, 15, H, L_LAYERS) for h in range(1, H + 1)], H, device)
+    long_rows = {}
+    for nl in (1024, 8192, 32768, 131072):
+        bt = max(1, TOKENS // nl)
+        qq, kk, vv, dd = (rnd(bt, H, nl, D) for _ in range(4))
+
+        def fbl():
+            _, seg = ops.la_forward(qq, kk, vv, None, lam_dev=lam_long, want_seg_states=True)
+            ops.la_backward(qq, kk, vv, dd, None, lam_dev=lam_long, fwd_seg_states=seg)
+
+        t = _time_ms(fbl, stream, reps=5)
+        long_rows[str(nl)] = {"batch": bt, "ms_fwd_bwd": round(t, 4), "tokens_per_s": round(bt * nl / (t / 1e3)),
+                              "pct_bf16_peak": round(100 * bt * nl / (t / 1e3) * H * FLOPS_PER_HEAD_TOKEN
+                                                     / (pk["bf16_tflops"] * 1e12), 2)}
+        del qq, kk, vv, dd
+    out["tnl1b_long_memory_decays"] = {"lam": "decay_rate(h, 15, 16, 16)", "rows": long_rows}
+    # fp32 ("working" precision, the 1e-4 parity path: SIMT FFMA kernels) at the TNL-1B shape, n = 8K
+    q32, k32, v32, d32 = (torch.randn(8, H, 8192, D, device=device, generator=g) / D ** 0.5 for _ in range(4))
+
+    def fb32():
+        _, seg = ops.la_forward(q32, k32, v32, None, lam_dev=lam_dev, want_seg_states=True)
+        ops.la_backward(q32, k32, v32, d32, None, lam_dev=lam_dev, fwd_seg_states=seg)
+
+    t32 = _time_ms(fb32, stream, reps=3, warm=1)
+    out["fp32_tnl1b_8k"] = {"shape": [8, H, 8192, D], "ms_fwd_bwd": round(t32, 3),
+                            "tokens_per_s": round(8 * 8192 / (t32 / 1e3)), "path": "simt fp32 (1e-4 parity path)"}
+    del q32, k32, v32, d32
     # BASELINE configs[0] (the reference's CPU-runnable parity case): batch 1, H 4, n 1024, d 64, fp32 on
     # the precision (SIMT) path, lam (1, 0.99, 0.9, 0.5); latency-bound (4 sequences), so no roofline
     c1 = [torch.randn(1, 4, 1024, 64, device=device, generator=g) * 0.5 for _ in range(4)]
@@ -562,8 +591,9 @@ def run_multi(ops, device, world, rank, stream, pk, reduce_max, steps) -> dict:
     rnd = lambda *shape: (torch.randn(*shape, device=device, generator=g) / D ** 0.5).to(torch.bfloat16)  # noqa: E731
 
     def timed(fn) -> float:
-        fn()
-        torch.cuda.synchronize()
+        for _ in range(3):  # warm-up: also lets the caching allocator settle on this row's block sizes
+            fn()
+            torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
@@ -603,6 +633,7 @@ def run_multi(ops, device, world, rank, stream, pk, reduce_max, steps) -> dict:
     lam_sp = ops.decay_tensor(lams(), H, device)
     group = dist.group.WORLD if world > 1 else None
     rows_sp = {}
+    torch.cuda.empty_cache()
     for n_total in (524288, 1048576):
         plo, phi = sp_slice(n_total, rank, world)
         lengths = [sp_slice(n_total, r, world)[1] - sp_slice(n_total, r, world)[0] for r in range(world)]
@@ -627,8 +658,9 @@ def run_multi(ops, device, world, rank, stream, pk, reduce_max, steps) -> dict:
                 _, seg = ops.la_forward(q1, k1, v1, None, lam_dev=lam_sp, want_seg_states=True)
                 ops.la_backward(q1, k1, v1, d1, None, lam_dev=lam_sp, fwd_seg_states=seg)
 
-            fb_one()
-            torch.cuda.synchronize()
+            for _ in range(3):
+                fb_one()
+                torch.cuda.synchronize()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
             for _ in range(steps):

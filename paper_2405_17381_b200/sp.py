@@ -56,6 +56,19 @@ class LocalKernels(Protocol):
     def finish_dq(self, handle) -> Any: ...
 
 
+_SIDE: dict = {}
+
+
+def _side_stream(device) -> "torch.cuda.Stream":
+    """One reusable side stream per device (a fresh stream per call would also defeat the caching
+    allocator's per-stream block reuse)."""
+    key = torch.device(device).index
+    st = _SIDE.get(key)
+    if st is None:
+        st = _SIDE[key] = torch.cuda.Stream(device)
+    return st
+
+
 class CudaKernels:
     """The B200 library (ops.*) -- the production local kernels."""
 
@@ -87,7 +100,7 @@ class CudaKernels:
         """Sweep 1 on a side stream: it overlaps the adjoint exchange (NCCL on the caller's stream)."""
         from . import ops
         cur = torch.cuda.current_stream(q.device)
-        side = torch.cuda.Stream(q.device)
+        side = _side_stream(q.device)
         side.wait_stream(cur)
         with torch.cuda.stream(side):
             dq, _, _ = ops.la_backward(q, k, v, do, None, lam_dev=lam, kv_in=kv_in, layout=self.layout,

@@ -1,0 +1,6 @@
+# round-2 profiling: launch list of one bench step + ncu --set full (with source) of the hot kernels
+set -x
+timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/r02_launches.csv python bench.py --steps 1 --warmup 3 --no-cpu --no-e2e --no-rows --no-multi > gpurun_out/bench_ncu.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"tc_pass_kernel|tc_dkdv_kernel" -s 6 -c 3 -o gpurun_out/r02_full_8k python bench.py --seq-lens 8192 --steps 1 --warmup 3 --no-cpu --no-e2e --no-rows --no-multi > gpurun_out/ncu_full8k.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"tc_pass_kernel|tc_dkdv_kernel|tc_summary_kernel|segment_scan" -s 12 -c 6 -o gpurun_out/r02_full_128k python bench.py --seq-lens 131072 --steps 1 --warmup 3 --no-cpu --no-e2e --no-rows --no-multi > gpurun_out/ncu_full128k.log 2>&1
+ls -la gpurun_out/
