@@ -121,6 +121,27 @@ inline cudaError_t set_smem_once(K kernel, int bytes, std::atomic<bool> (&done)[
   return err;
 }
 
+#ifndef LA_PDL
+#define LA_PDL 1
+#endif
+// Launch with programmatic stream serialization (PDL, see griddep_wait in la_ptx.cuh) so the kernel's prologue
+// overlaps the previous kernel's tail; LA_PDL=0 builds plain launches (A/B).
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = LA_PDL;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 struct Plan {
   int chunk;        // rows per chunk in the kernel
   int nseg;         // segments per (b, h)

@@ -61,6 +61,13 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
 #endif
   return ok != 0;
 }
+// Programmatic dependent launch (PDL): a kernel launched with cudaLaunchAttributeProgrammaticStreamSerialization
+// (la::launch_pdl) may start while the previous kernel of the stream drains.  griddep_wait() blocks until that
+// kernel has completed and its writes are visible -- every thread calls it before its first global access;
+// griddep_launch() (one thread per CTA, near the CTA's end) lets the next kernel start its prologue (barrier
+// init, TMEM allocation) on the SMs this grid's tail leaves idle.  Both are no-ops without PDL.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 // x^k for k >= 0 by binary exponentiation (<= 2 log2 k + 1 roundings)
 __device__ __forceinline__ double pow_int(double x, int k) {
   double r = 1.0;

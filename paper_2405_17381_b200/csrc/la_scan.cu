@@ -1,4 +1,5 @@
 // la_scan.cu -- combine sub-segment state summaries into each segment's entering state.
+#include "la_ptx.cuh"
 #include "la_scan.cuh"
 
 namespace la {
@@ -27,6 +28,8 @@ __global__ void __launch_bounds__(kScanThreads) segment_scan_kernel(
     Tacc* final_out, int final_T, const double* lam, int heads, int d, int n, int seg_len, int nseg,
     int sub_len, int sub_per_seg, int g_lo, int g_hi, int rev) {
   using Vec = VecA<Tacc, V>;
+  ptx::griddep_wait();    // PDL: the summaries of the previous kernel are complete and visible
+  ptx::griddep_launch();  // tiny kernel: let the main pass start its prologue right away
   // lam^len of a sub-segment: len is sub_len, a segment's short last sub-segment, or the sequence's
   // short last one -- three pow()s per block instead of one per sub-segment
   __shared__ Tacc s_pow[3];
@@ -139,16 +142,13 @@ cudaError_t launch_segment_scan(bool acc_double, const void* delta, void* seg_in
   reinterpret_cast<const T*>(delta), reinterpret_cast<T*>(seg_in), user_in, user_T, reinterpret_cast<T*>(final_out), \
       final_T, lam, heads, d, p.n, p.seg_len, p.nseg, p.sub_len, p.sub_per_seg, p.g_lo, p.g_hi, p.rev
   if (acc_double) {
-    if (dd % 2 == 0)
-      segment_scan_kernel<double, 2><<<grid(2), kScanThreads, 0, st>>>(LA_SCAN_ARGS(double));
-    else
-      segment_scan_kernel<double, 1><<<grid(1), kScanThreads, 0, st>>>(LA_SCAN_ARGS(double));
-  } else {
-    if (dd % 4 == 0)
-      segment_scan_kernel<float, 4><<<grid(4), kScanThreads, 0, st>>>(LA_SCAN_ARGS(float));
-    else
-      segment_scan_kernel<float, 1><<<grid(1), kScanThreads, 0, st>>>(LA_SCAN_ARGS(float));
+    if (dd % 2 == 0) return launch_pdl(segment_scan_kernel<double, 2>, grid(2), dim3(kScanThreads), 0, st,
+                                       LA_SCAN_ARGS(double));
+    return launch_pdl(segment_scan_kernel<double, 1>, grid(1), dim3(kScanThreads), 0, st, LA_SCAN_ARGS(double));
   }
+  if (dd % 4 == 0)
+    return launch_pdl(segment_scan_kernel<float, 4>, grid(4), dim3(kScanThreads), 0, st, LA_SCAN_ARGS(float));
+  return launch_pdl(segment_scan_kernel<float, 1>, grid(1), dim3(kScanThreads), 0, st, LA_SCAN_ARGS(float));
 #undef LA_SCAN_ARGS
   return cudaGetLastError();
 }

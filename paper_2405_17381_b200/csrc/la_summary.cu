@@ -75,6 +75,7 @@ __global__ void __launch_bounds__(S_THREADS, 2)
   // a sub-segment that a later factor lam^len == 0 discards in the scan (sub_dead: its slot is never read),
   // and, in a live one, the chunks whose largest weight rounds to zero in bf16 (their B~ rows are all zero).
   // Short-memory heads thereby summarise ~one chunk per segment instead of the whole segment.
+  griddep_wait();  // PDL: the previous kernel of the stream has completed (inputs written, outputs free)
   const double lamv = load_decay(args.lam, hi);
   int t_beg = 0, t_end = nchunks_all;
   {
@@ -152,6 +153,7 @@ __global__ void __launch_bounds__(S_THREADS, 2)
         tma_load_4d(&map_c, &bars.full[s], gb + STILE, 0, r0, hi, bi);
         tma_load_4d(&map_c, &bars.full[s], gb + STILE + SHALF, 64, r0, hi, bi);
       }
+      griddep_launch();  // every load of this CTA issued: the next kernel may start its prologue
     }
   } else if (warp == 1) {
     if (lane == 0) {
@@ -242,8 +244,7 @@ cudaError_t tc_summary_launch(const PassDesc& p, cudaStream_t st) {
   cudaError_t err = set_smem_once(tc_summary_kernel, (int)S_SMEM_BYTES, smem_set);
   if (err != cudaSuccess) return err;
   dim3 grid((p.g_hi - p.g_lo + 1) * p.sub_per_seg, p.batch * p.heads);
-  tc_summary_kernel<<<grid, S_THREADS, S_SMEM_BYTES, st>>>(mb, mc, a);
-  return cudaGetLastError();
+  return launch_pdl(tc_summary_kernel, grid, dim3(S_THREADS), S_SMEM_BYTES, st, mb, mc, a);
 }
 
 }  // namespace la

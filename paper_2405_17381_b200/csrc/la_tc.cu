@@ -176,6 +176,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     mbar_init(&bars.st_ready, NUM_KV);
     fence_mbar_init();
   }
+  griddep_wait();  // PDL: the previous kernel of the stream has completed (inputs written, outputs free)
   // lam^0 .. lam^C, one power per thread (binary exponentiation in fp64): a serial ladder here held
   // every warp (and the first TMA loads) back by ~130 dependent multiplies
   if (threadIdx.x <= C) {
@@ -224,6 +225,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         tma_load_4d(map, &bars.full[x][s], g, 0, r0, hi, bi);
         tma_load_4d(map, &bars.full[x][s], g + HALF, 64, r0, hi, bi);
       }
+      if (x == 0) griddep_launch();  // every load of this CTA issued: the next kernel may start its prologue
     } else if (x == 3) {
       // store lane: bf16 O(t) is staged in C(t)'s slot (C's MMA readers are done by then); TMA-store it
       // and hand the slot back to the C ring once the store has read it
@@ -687,8 +689,7 @@ cudaError_t launch_tc(const PassDesc& p, cudaStream_t st) {
   cudaError_t err = set_smem_once(kern, (int)smem_bytes, smem_set);
   if (err != cudaSuccess) return err;
   dim3 grid(p.nseg, p.batch * p.heads);
-  kern<<<grid, NUM_THREADS, smem_bytes, st>>>(ma, mb, mc, mo, a);
-  return cudaGetLastError();
+  return launch_pdl(kern, grid, dim3(NUM_THREADS), smem_bytes, st, ma, mb, mc, mo, a);
 }
 
 bool aligned16(const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15) == 0; }

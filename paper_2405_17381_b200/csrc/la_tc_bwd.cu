@@ -153,6 +153,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     mbar_init(&bars.st_pub, NUM_KV);
     fence_mbar_init();
   }
+  griddep_wait();  // PDL: the previous kernel of the stream has completed (inputs written, outputs free)
   // lam^0 .. lam^C, one power per thread (binary exponentiation in fp64): a serial ladder here held
   // every warp (and the first TMA loads) back by ~130 dependent multiplies
   if (threadIdx.x <= C) {
@@ -265,6 +266,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           else if (clock64() - t0 > 40000000000LL) __trap();
         }
       }
+      griddep_launch();  // every load of this CTA issued: the next kernel may start its prologue
     } else if (lane == 4) {
       for (int t = 0; t < nchunks; ++t) {
         const int s = t & 1;
@@ -625,8 +627,7 @@ cudaError_t tc_dkdv_launch(const PassDesc& p, const void* q, const void* k, cons
   cudaError_t err = set_smem_once(tc_dkdv_kernel, (int)SMEM_BYTES, smem_set);
   if (err != cudaSuccess) return err;
   dim3 grid(p.nseg, p.batch * p.heads);
-  tc_dkdv_kernel<<<grid, NUM_THREADS, SMEM_BYTES, st>>>(mq, mk, mv, mdo, mdk, mdv, a);
-  return cudaGetLastError();
+  return launch_pdl(tc_dkdv_kernel, grid, dim3(NUM_THREADS), SMEM_BYTES, st, mq, mk, mv, mdo, mdk, mdv, a);
 }
 
 }  // namespace la
