@@ -9,6 +9,22 @@ for dtype, backend, n, segs in ((torch.bfloat16, "tcgen05", 300, 0), (torch.bflo
     q, k, v, do = (torch.rand(1, 2, n, 128, device="cuda", dtype=dtype) for _ in range(4))
     o, seg = ops.la_forward(q, k, v, [0.9, 0.99], backend=backend, segments=segs, want_seg_states=True)
     ops.la_backward(q, k, v, do, [0.9, 0.99], backend=backend, segments=segs, fwd_seg_states=seg)
+# round 2: short-memory decays (summary CTAs skipped / truncated, scan skips dead slots), long segments with
+# sub-segments, strided operands (per-operand TMA maps), the RESUME path, the check flags, PDL chains
+for lams in ([0.3, 0.999], [5.5e-4, 0.62]):
+    q, k, v, do = (torch.rand(1, 2, 6000, 128, device="cuda", dtype=torch.bfloat16) for _ in range(4))
+    o, seg = ops.la_forward(q, k, v, lams, want_seg_states=True)
+    ops.la_backward(q, k, v, do, lams, fwd_seg_states=seg)
+    ws = ops.new_workspace(tuple(q.shape))
+    ops.la_forward_state(k, v, lams, workspace=ws)
+    ops.la_forward(q, k, v, lams, workspace=ws, resume=True, check=True)
+    ws2 = ops.new_workspace(tuple(q.shape))
+    ops.la_backward_state(q, do, lams, workspace=ws2)
+    ops.la_backward(q, k, v, do, lams, parts="dkdv", workspace=ws2, resume=True)
+    ops.la_backward(q, k, v, do, lams, parts="dq", fwd_seg_states=seg)
+qkv = torch.rand(1, 700, 3, 2, 128, device="cuda", dtype=torch.bfloat16)
+ops.la_forward(qkv[:, :, 0], qkv[:, :, 1], qkv[:, :, 2], [0.9, 0.5], layout="bnhd")
+ops.la_backward(qkv[:, :, 0], qkv[:, :, 1], qkv[:, :, 2], qkv[:, :, 0], [0.9, 0.5], layout="bnhd")
 for dtype, d in ((torch.bfloat16, 128), (torch.float32, 128), (torch.float64, 64), (torch.float32, 40)):
     q, k, v = (torch.rand(3, 2, d, device="cuda", dtype=dtype) for _ in range(3))
     kv = torch.rand(3, 2, d, d, device="cuda", dtype=ops.state_dtype(dtype))
