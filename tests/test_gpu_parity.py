@@ -73,6 +73,13 @@ def test_config1_fp32_and_fp64():
                 ref, view = golden_array(f"config1/h{h}/{key}64", arr[0, h])
                 err = orc.max_rel_error(view(arr[0, h]), ref)
                 assert err <= TOL[dtype], f"h={h} {key} {dtype}: {err:.3e}"
+        # the stored goldens are compressed (row sums + every 97th entry): also compare every entry against
+        # the oracle (pinned to the reference by tests/test_oracle.py) on the same inputs
+        ro, _ = orc.batched_forward(q, k, v, c["lams"], c["B"])
+        (rdq, rdk, rdv), _ = orc.batched_backward(q, k, v, do, c["lams"], c["B"])
+        for key, arr, ref in (("o", o, ro), ("dq", dq, rdq), ("dk", dk, rdk), ("dv", dv, rdv)):
+            err = orc.max_rel_error(arr, ref)
+            assert err <= TOL[dtype], f"full {key} {dtype}: {err:.3e}"
 
 
 # --------------------------------------------------------------------------
@@ -212,9 +219,10 @@ def test_backward_with_edge_states_and_saved_segment_states(segments):
         assert orc.max_rel_error(host(a), r) <= TOL[torch.bfloat16]
 
 
-def test_persistent_units_with_edge_states():
-    """More (batch, head) units than one wave and an unsplit sequence: each CTA walks several units
-    of one head (la_tc.cu), exporting every unit's kv_out and loading every unit's kv_in; ragged n."""
+def test_multi_wave_units_with_edge_states():
+    """More (batch, head) units than one wave (185 CTAs on 148 SMs, two waves of one-unit CTAs) and an
+    unsplit, ragged sequence: every CTA loads its own unit's kv_in / dkv_in and exports its kv_out /
+    dkv_out."""
     b, h, n, d = 37, 5, 300, 128  # bh = 185 > 148: 95 CTAs, 1-2 units each
     lams = [1.0, 0.99, 0.9, 0.7, 0.5]
     q, k, v, do = (dev(a, torch.bfloat16) for a in _batched(b, h, n, d, seed=21))
