@@ -106,18 +106,23 @@ int op_strides(const la_desc* desc, const la_tensor_strides* ts, unsigned used, 
 }
 
 // Which backend serves this descriptor (and, for the _ex calls, these operand strides).
+// tensor-core eligibility: bf16 (la_tc.cu) or fp32 (la_tc32.cu), d = 128, 16-byte strides
+bool tc_eligible(int dtype, int64_t d, const int64_t* strides) {
+  return la::tc_supported(dtype, (int)d, strides, 1) || la::tc32_supported(dtype, (int)d, strides, 1);
+}
+
 int pick_backend(const la_desc* desc, int* backend, const OpStrides* ops = nullptr, unsigned used = 0) {
-  bool tc_ok = la::tc_supported(desc->dtype, (int)desc->d, desc->stride, 1);
+  bool tc_ok = tc_eligible(desc->dtype, desc->d, desc->stride);
   if (ops != nullptr)
     for (int i = 0; i < 8; ++i) {
       if (!(used >> i & 1u)) continue;
       const int64_t t[3] = {ops->s[i].b, ops->s[i].h, ops->s[i].n};
-      tc_ok = tc_ok && la::tc_supported(desc->dtype, (int)desc->d, t, 1);
+      tc_ok = tc_ok && tc_eligible(desc->dtype, desc->d, t);
     }
   if (desc->backend == LA_BACKEND_TCGEN05) {
     if (!tc_ok)
       return fail(LA_ERR_UNSUPPORTED,
-                  "tcgen05 backend needs bf16, d = 128, 16-byte aligned strides (dtype=%d d=%lld)",
+                  "tcgen05 backend needs bf16 or fp32, d = 128, 16-byte aligned strides (dtype=%d d=%lld)",
                   desc->dtype, (long long)desc->d);
     *backend = LA_BACKEND_TCGEN05;
   } else if (desc->backend == LA_BACKEND_SIMT) {
@@ -135,6 +140,7 @@ int pick_backend(const la_desc* desc, int* backend, const OpStrides* ops = nullp
 la::Plan plan_for(const la_desc* desc, int backend) {
   const int64_t bh = desc->batch * desc->heads;
   const int sms = la::device_sms();
+  if (backend == LA_BACKEND_TCGEN05 && desc->dtype == LA_F32) return la::tc32_plan(bh, desc->n, desc->segments, sms);
   if (backend == LA_BACKEND_TCGEN05) return la::tc_plan(bh, desc->n, (int)desc->d, desc->segments, sms);
   return la::make_plan(bh, desc->n, la::simt_chunk(desc->dtype), desc->segments, 2 * sms, LA_SIMT_MIN_CHUNKS);
 }
@@ -171,7 +177,7 @@ la::PassDesc base_pass(const la_desc* desc, const la::Plan& plan, const double* 
 cudaError_t launch(int backend, int dtype, const la::PassDesc& p, bool state_only, cudaStream_t st) {
   if (backend == LA_BACKEND_TCGEN05) {
     if (!la::tc_pointers_ok(p)) return cudaErrorMisalignedAddress;  // TMA needs 16-byte aligned bases
-    return la::tc_launch(p, state_only, st);
+    return dtype == LA_F32 ? la::tc32_launch(p, state_only, st) : la::tc_launch(p, state_only, st);
   }
   return la::simt_launch(dtype, p, state_only, st);
 }
@@ -513,6 +519,8 @@ int la_bwd_ex(const la_desc* desc, const la_tensor_strides* strides, uint32_t fl
                          {"Q", "K", "V", "dO"}, st)) != LA_OK)
     return rc;
   const la::PassDesc base = base_pass(desc, pr.plan, lam);
+  // sweep 2 as the fused dK/dV kernel (bf16 on tcgen05) or as two reverse passes (fp32 on tcgen05, SIMT)
+  const bool fused = pr.backend == LA_BACKEND_TCGEN05 && desc->dtype == LA_BF16;
   void* delta = split ? ws_delta(workspace) : nullptr;
   void* seg_in = split ? ws_seg_in(workspace, desc, pr.plan) : nullptr;
   cudaError_t err = cudaSuccess;
@@ -549,7 +557,7 @@ int la_bwd_ex(const la_desc* desc, const la_tensor_strides* strides, uint32_t fl
     if (split && !states_ready &&
         (err = segment_states(pr.backend, desc->dtype, pd, delta, seg_in, s, resume)) != cudaSuccess)
       return cuda_fail(err, "la_bwd dkv states");
-    if (pr.backend == LA_BACKEND_TCGEN05)
+    if (fused)
       return dkdv(base, os, q, k, v, dout, dk, dv, dkv_in, dkv_out, split ? seg_in : nullptr, s);
     la::PassDesc r = base;
     r.a = v;
@@ -794,8 +802,8 @@ int la_launch_count(const la_desc* desc, int which) {
   int backend;
   if (pick_backend(desc, &backend) != LA_OK) return -1;
   const la::Plan plan = plan_for(desc, backend);
-  // bwd sweep 2 is one fused dk/dv kernel on the tcgen05 backend, two passes on SIMT
-  const int sweep2 = backend == LA_BACKEND_TCGEN05 ? 1 : 2;
+  // bwd sweep 2 is one fused dk/dv kernel on the bf16 tcgen05 backend, two passes otherwise
+  const int sweep2 = backend == LA_BACKEND_TCGEN05 && desc->dtype == LA_BF16 ? 1 : 2;
   if (plan.nseg == 1) return which == 0 ? 1 : 1 + sweep2;
   // fwd: summaries + scan + main.  bwd: dq main (+ its summaries and scan unless the forward's segment
   // states are passed, which = 2) + one dkv summaries + scan + sweep 2
@@ -807,7 +815,7 @@ const char* la_last_error(void) { return g_last_error.c_str(); }
 int la_abi_version(void) { return LA_ABI_VERSION; }
 
 const char* la_build_info(void) {
-  return "lightning-attn b200: sm_100a, backends simt(f64/f32/bf16) + tcgen05(bf16); decode; GLA stages";
+  return "lightning-attn b200: sm_100a, backends simt(f64/f32/bf16) + tcgen05(bf16, f32 3xbf16 split); decode; GLA stages";
 }
 
 }  // extern "C"

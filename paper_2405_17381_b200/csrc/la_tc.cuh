@@ -22,4 +22,8 @@ cudaError_t tc_dkdv_launch(const PassDesc& p, const void* q, const void* k, cons
                            void* dk, void* dv, const Strides3* s, cudaStream_t st);
 // one launch of the main pass kernel (state_only = false) or of the per-segment summary kernel
 cudaError_t tc_launch(const PassDesc& p, bool state_only, cudaStream_t st);
+// the fp32 pass (la_tc32.cu): three-term bf16 split on tcgen05, d = 128, 16-byte strides
+bool tc32_supported(int dtype, int d, const int64_t* strides, int count);
+Plan tc32_plan(int64_t bh, int64_t n, int64_t want_segments, int sms);
+cudaError_t tc32_launch(const PassDesc& p, bool state_only, cudaStream_t st);
 }  // namespace la
