@@ -439,16 +439,19 @@ def measure_rows(ops, device, stream, pk) -> dict:
                                                      / (pk["bf16_tflops"] * 1e12), 2)}
         del qq, kk, vv, dd
     out["tnl1b_long_memory_decays"] = {"lam": "decay_rate(h, 15, 16, 16)", "rows": long_rows}
-    # fp32 ("working" precision, the 1e-4 parity path: SIMT FFMA kernels) at the TNL-1B shape, n = 8K
+    # fp32 ("working" precision, the 1e-4 parity path) at the TNL-1B shape, n = 8K: the tensor-core split pass
+    # (la_tc32.cu, the default for fp32 at d = 128) and the SIMT FFMA pass beside it
     q32, k32, v32, d32 = (torch.randn(8, H, 8192, D, device=device, generator=g) / D ** 0.5 for _ in range(4))
+    fp32_rows = {}
+    for be, path in (("tcgen05", "tcgen05 fp32 (3-term bf16 split, 1e-4 parity path)"),
+                     ("simt", "simt fp32 (FFMA)")):
+        def fb32():
+            _, seg = ops.la_forward(q32, k32, v32, None, lam_dev=lam_dev, want_seg_states=True, backend=be)
+            ops.la_backward(q32, k32, v32, d32, None, lam_dev=lam_dev, fwd_seg_states=seg, backend=be)
 
-    def fb32():
-        _, seg = ops.la_forward(q32, k32, v32, None, lam_dev=lam_dev, want_seg_states=True)
-        ops.la_backward(q32, k32, v32, d32, None, lam_dev=lam_dev, fwd_seg_states=seg)
-
-    t32 = _time_ms(fb32, stream, reps=3, warm=1)
-    out["fp32_tnl1b_8k"] = {"shape": [8, H, 8192, D], "ms_fwd_bwd": round(t32, 3),
-                            "tokens_per_s": round(8 * 8192 / (t32 / 1e3)), "path": "simt fp32 (1e-4 parity path)"}
+        t32 = _time_ms(fb32, stream, reps=3 if be == "simt" else 10, warm=1 if be == "simt" else 3)
+        fp32_rows[be] = {"ms_fwd_bwd": round(t32, 3), "tokens_per_s": round(8 * 8192 / (t32 / 1e3)), "path": path}
+    out["fp32_tnl1b_8k"] = {"shape": [8, H, 8192, D], **fp32_rows}
     del q32, k32, v32, d32
     # BASELINE configs[0] (the reference's CPU-runnable parity case): batch 1, H 4, n 1024, d 64, fp32 on
     # the precision (SIMT) path, lam (1, 0.99, 0.9, 0.5); latency-bound (4 sequences), so no roofline

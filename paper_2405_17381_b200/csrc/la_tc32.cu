@@ -25,7 +25,8 @@
 //   out  TMEM O -> fp32 rows -> global
 //
 // SMEM: 3 x 64 KB operand regions + 32 KB state half = 224 KB.  TMEM: S | A~ | O | state = 512 columns.
-// The A region is refilled as soon as S has read it, B and C once chunk t's MMAs are done.  State-only
+// S is issued once A and B are split, and runs while C is split and the first state half published.  The
+// A region is refilled as soon as S has read it, B and C once chunk t's MMAs are done.  State-only
 // mode (segment summaries, la_api.cu segment_states) runs B~ and U only.
 #include <cudaTypedefs.h>
 
@@ -277,7 +278,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       __syncthreads();
       write_split(smem + R_B, i, hh, h, l);
     }
-    {
+    auto convert_c = [&]() {
       mbar_wait(&bars.full[2], ph);
       float x[64];
       read_f32_row(smem + R_C, i, hh, x);
@@ -286,8 +287,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       for (int q = 0; q < 32; ++q) split2(x[2 * q], x[2 * q + 1], h[q], l[q]);
       __syncthreads();
       write_split(smem + R_C, i, hh, h, l);
-    }
+    };
     if (STATE_ONLY) {
+      convert_c();
       // pre-scale the state by lam^b, then state += B~^T C (whole width)
       float x[32];
 #pragma unroll
@@ -320,9 +322,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       }
       continue;
     }
-    publish_half(0, decay);
     handoff();
-    // ---------------------------------------------------------------- S = A B^T
+    // ---------------------------------------------------------------- S = A B^T (C's split and the first
+    // state publish overlap it)
     if (tid == 0) {
 #pragma unroll 1
       for (int g = 0; g < 3; ++g) {
@@ -336,6 +338,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       }
       mma_commit(&bars.s_done);
     }
+    convert_c();
+    publish_half(0, decay);
     mbar_wait(&bars.s_done, ph);
     tc_fence_after();
     if (tid == 0 && t + 1 < nchunks) load(0, t + 1);  // A's tiles are consumed (A~ lives in TMEM)

@@ -1,11 +1,13 @@
-# small runs of every kernel for compute-sanitizer (memcheck / racecheck / synccheck): the tcgen05 pass,
+# small runs of every kernel for compute-sanitizer (memcheck / racecheck / synccheck): the tcgen05 pass (bf16
+# and the fp32 split pass, full and state-only),
 # dK/dV sweep, summary and scan kernels (segmented), the SIMT path, decode (bulk and generic), the GLA
 # stages (with LRPE) and the TP stages
 import sys, torch
 sys.path.insert(0, '.')
 from paper_2405_17381_b200 import ops
 for dtype, backend, n, segs in ((torch.bfloat16, "tcgen05", 300, 0), (torch.bfloat16, "tcgen05", 1000, 3),
-                                (torch.float32, "simt", 100, 2)):
+                                (torch.float32, "simt", 100, 2), (torch.float32, "tcgen05", 300, 0),
+                                (torch.float32, "tcgen05", 1000, 3)):
     q, k, v, do = (torch.rand(1, 2, n, 128, device="cuda", dtype=dtype) for _ in range(4))
     o, seg = ops.la_forward(q, k, v, [0.9, 0.99], backend=backend, segments=segs, want_seg_states=True)
     ops.la_backward(q, k, v, do, [0.9, 0.99], backend=backend, segments=segs, fwd_seg_states=seg)

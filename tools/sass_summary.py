@@ -3,7 +3,7 @@
     python tools/sass_summary.py [lib.so] [out.txt]
 
 Runs ``cuobjdump -sass`` on the built ``libla_b200.so`` and counts, per tcgen05 kernel (the pass,
-the fused dK/dV sweep, the segment summary), the mnemonics that prove the Blackwell data path:
+the fused dK/dV sweep, the segment summary, the fp32 split pass), the mnemonics that prove the Blackwell data path:
 UTCHMMA = tcgen05.mma, UTCBAR = tcgen05.commit, LDTM / STTM = tcgen05.ld / st (TMEM), UTMALDG /
 UTMASTG = TMA tensor load / store, UTMAPF / UTMACCTL = TMA prefetch, SYNCS.* = mbarriers -- and HMMA
 (legacy mma.sync), which must be absent.  ``__graft_entry__.build()`` regenerates it on every build.
@@ -19,7 +19,7 @@ import sys
 from pathlib import Path
 
 ROOT = Path(__file__).resolve().parent.parent
-KERNELS = ("tc_pass_kernel", "tc_dkdv_kernel", "tc_summary_kernel")
+KERNELS = ("tc_pass_kernel", "tc_dkdv_kernel", "tc_summary_kernel", "tc32_pass_kernel")
 WATCH = ("UTCHMMA", "UTCBAR", "LDTM", "STTM", "UTMALDG", "UTMASTG", "UTMAPF", "UTMACCTL", "SYNCS", "HMMA",
          "ELECT", "UTCATOMSWS")
 
