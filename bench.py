@@ -386,6 +386,25 @@ def measure_rows(ops, device, stream, pk) -> dict:
     stages["prologue_bwd"] = (ms, 6 * row_bytes)
     out["gla_stages"] = {k: {"ms": round(t, 4), "gbs": round(by / (t / 1e3) / 1e9, 1),
                              "frac_hbm": round(by / (t / 1e3) / 1e9 / pk["hbm_gbs"], 3)} for k, (t, by) in stages.items()}
+    # the GLA core forward (§8(f) rank 1): fused (act + LRPE in the pass kernel, q / k written for the backward;
+    # and without them, as a prefill needs) vs the two-step path it replaces (la_gla_prologue + la_fwd)
+    vv = rnd(b, n, w)
+
+    def two_step():
+        q2, k2 = ops.gla_prologue(qp, kp, H, theta=theta)
+        ops.la_forward(*(t.view(b, n, H, D) for t in (q2, k2, vv)), None, lam_dev=lam_dev, layout="bnhd")
+
+    t_two = _time_ms(two_step, stream)
+    t_fused = _time_ms(lambda: ops.gla_core_forward(qp, kp, vv, None, H, theta=theta, lam_dev=lam_dev), stream)
+    t_fused_nq = _time_ms(lambda: ops.gla_core_forward(qp, kp, vv, None, H, theta=theta, lam_dev=lam_dev,
+                                                       want_qk=False), stream)
+    out["gla_core_fwd"] = {
+        "shape": [b, n, w], "lrpe": True, "act": "swish",
+        "two_step_ms": round(t_two, 4), "fused_ms": round(t_fused, 4), "fused_no_qk_ms": round(t_fused_nq, 4),
+        "speedup": round(t_two / t_fused, 3), "speedup_no_qk": round(t_two / t_fused_nq, 3),
+        "rows_moved": {"two_step": 8, "fused": 6, "fused_no_qk": 4},
+        "fused_frac_hbm": round(6 * row_bytes / (t_fused / 1e3) / 1e9 / pk["hbm_gbs"], 3)}
+    del vv
     # BASELINE configs[1]: the TNL-385M attention shape (H = 8, d = 128), n = 2K..16K at 64K tokens/batch
     cfg385 = {}
     lam8 = ops.decay_tensor([decay_rate(h, 1, 8, 24) for h in range(1, 9)], 8, device)

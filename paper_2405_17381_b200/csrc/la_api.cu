@@ -747,6 +747,51 @@ int la_gla_prologue_bwd(const la_gla_desc* desc, const void* qp, const void* kp,
   return err == cudaSuccess ? LA_OK : cuda_fail(err, "la_gla_prologue_bwd");
 }
 
+int la_gla_core_fwd(const la_gla_desc* gdesc, const void* qp, const void* kp, const void* v, const double* lam,
+                    const double* theta, const void* kv_in, void* o, void* q_out, void* k_out, void* kv_out,
+                    void* stream) {
+  la::GlaRows g;
+  int rc = gla_prepare(gdesc, theta != nullptr, &g);
+  if (rc != LA_OK) return rc;
+  if (!qp || !kp || !v || !o || !lam) return fail(LA_ERR_SHAPE, "la_gla_core_fwd: null qp/kp/v/o/lam");
+  if ((q_out == nullptr) != (k_out == nullptr)) return fail(LA_ERR_SHAPE, "la_gla_core_fwd: q_out and k_out go together");
+  if (!states_aligned({qp, kp, v, o, q_out, k_out, kv_in, kv_out}))
+    return fail(LA_ERR_SHAPE, "la_gla_core_fwd: operands and states must be 16-byte aligned");
+  // the attention descriptor of the model-native rows [batch, n, heads * d]
+  la_desc desc;
+  std::memset(&desc, 0, sizeof(desc));
+  desc.batch = gdesc->batch;
+  desc.heads = gdesc->heads;
+  desc.n = gdesc->n;
+  desc.d = gdesc->d;
+  desc.dtype = gdesc->dtype;
+  desc.backend = LA_BACKEND_TCGEN05;
+  desc.stride[0] = gdesc->n * gdesc->heads * gdesc->d;
+  desc.stride[1] = gdesc->d;
+  desc.stride[2] = gdesc->heads * gdesc->d;
+  if ((rc = validate(&desc)) != LA_OK) return rc;
+  if (desc.dtype != LA_BF16 || desc.d != 128 || !la::tc_supported(desc.dtype, (int)desc.d, desc.stride, 1))
+    return fail(LA_ERR_UNSUPPORTED, "la_gla_core_fwd: the fused core needs bf16 and d = 128 (use la_gla_prologue + la_fwd)");
+  const la::Plan plan = plan_for(&desc, LA_BACKEND_TCGEN05);
+  if (plan.nseg != 1)
+    return fail(LA_ERR_UNSUPPORTED, "la_gla_core_fwd: batch * heads = %lld leaves SMs idle, the plan splits the "
+                "sequence (use la_gla_prologue + la_fwd)", (long long)(desc.batch * desc.heads));
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  bind_stream_context(st);
+  la::PassDesc p = base_pass(&desc, plan, lam);
+  p.a = qp;
+  p.b = kp;
+  p.c = v;
+  p.out = o;
+  p.rev = 0;
+  p.state_in = kv_in;
+  p.state_in_bh_stride = (int64_t)desc.d * desc.d;
+  p.state_out = kv_out;
+  la::GlaPrologue pro{theta, gdesc->act, gdesc->offset, q_out, k_out};
+  cudaError_t err = la::tc_gla_fwd_launch(p, pro, st);
+  return err == cudaSuccess ? LA_OK : cuda_fail(err, "la_gla_core_fwd");
+}
+
 int la_gla_epilogue(const la_gla_desc* desc, const void* a, const void* u, void* gated, void* rawnorm, void* stream) {
   la::GlaRows g;
   int rc = gla_prepare(desc, false, &g);

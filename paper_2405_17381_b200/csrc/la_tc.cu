@@ -24,6 +24,12 @@
 //
 // Shared memory: 2 stages x {A, B, C} tiles (3 x 32 KB) + the bf16 state
 // (32 KB) = 224 KB -> one CTA per SM.  TMEM: S0 | S1 | O | state = 512 columns.
+//
+// GLA mode (template GLA, la_gla_core_fwd): the GLA prologue q = rot(act(qp)),
+// k = rot(act(kp)) (model.py:381-397, positional.py:126-150) is applied to each landed A / B tile in
+// shared memory by the state warps -- idle for most of a chunk -- before S is issued, so the pre-activation
+// projections stream straight into the core (no q / k round trip through HBM); a store lane writes the
+// transformed tiles out for the backward when asked.
 #include <cudaTypedefs.h>
 
 #include <cstdio>
@@ -87,6 +93,8 @@ constexpr uint32_t IDESC_MNMN = idesc_bf16(128, 128, 1, 1);  // A MN-major, B MN
 constexpr int NSTAGE_MAX = NSTAGE;
 
 struct Bars {
+  uint64_t xf_done[NSTAGE_MAX];   // GLA: A / B tiles of the stage transformed in place -> MMA (S), qk store lane
+  uint64_t qk_stored[NSTAGE_MAX]; // GLA: the store lane has read the transformed tiles -> B warps (B~ in place)
   uint64_t full[3][NSTAGE_MAX];   // TMA -> consumers, one ring per operand tile A, B, C (tx bytes)
   uint64_t empty[3][NSTAGE_MAX];  // MMA commit after the tile's last reader -> TMA
   uint64_t s_full[2];      // MMA: S[t%2] done                 -> P warps, state warps
@@ -117,18 +125,51 @@ struct TcArgs {
   int in_T;
   float* state_out;
   int out_T;
+  // GLA mode
+  const double* theta;  // LRPE angles [d/2] (nullable: no rotation)
+  int act;              // la_act
+  int qk_out;           // store the transformed q / k tiles (map_qo / map_ko)
+  int64_t offset;       // LRPE position of row 0
 };
+
+// LRPE cos / sin of theta * pos: angle formed and reduced mod 2 pi in fp64, then the fp32 hardware
+// approximation on |angle| <= pi (~2^-21), as la_gla.cu's prologue
+__device__ __forceinline__ void lrpe_cs(double theta, int64_t pos, float* c, float* s) {
+  double ang = theta * (double)pos;
+  ang = fma(-6.283185307179586476925286766559, rint(ang * 0.15915494309189533576888376337251), ang);
+  __sincosf((float)ang, s, c);
+}
+__device__ __forceinline__ uint32_t tanh_bf16x2(uint32_t x) {
+  uint32_t y;
+  asm("tanh.approx.bf16x2 %0, %1;" : "=r"(y) : "r"(x));
+  return y;
+}
+__device__ __forceinline__ float tanh_approx(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+// the GLA activations (model.py:60-99) in fp32: swish x * sigmoid(x), sigmoid = (1 + tanh(x / 2)) / 2
+__device__ __forceinline__ float gla_act(float x, int act) {
+  if (act == LA_ACT_SWISH) return x * fmaf(0.5f, tanh_approx(0.5f * x), 0.5f);
+  if (act == LA_ACT_ONE_PLUS_ELU) return x > 0.f ? x + 1.f : __expf(x);
+  return x;
+}
 
 // byte offset of 16-byte chunk `c` (0..7) of row `r` inside a [128][64] bf16 block, 128B swizzle
 __device__ __forceinline__ uint32_t sw128(int r, int c) { return (uint32_t)(r * 128 + ((c ^ (r & 7)) << 4)); }
 
 
+template <bool GLA>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     tc_pass_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                    const __grid_constant__ CUtensorMap map_c, const __grid_constant__ CUtensorMap map_o,
+                   const __grid_constant__ CUtensorMap map_qo, const __grid_constant__ CUtensorMap map_ko,
                    const TcArgs args) {
   extern __shared__ uint8_t smem_raw[];
   __shared__ Bars bars;
+  __shared__ float theta_s[GLA ? D / 2 : 1];           // LRPE angles (fp32: local angles theta_j * i, i < 128)
+  __shared__ float2 anchor_s[GLA ? D / 2 : 1];         // (cos, sin) of theta_j * (chunk row 0 + offset), fp64-reduced
   __shared__ __align__(16) float pw[C + 8];  // lam^0 .. lam^128
   const uint32_t smem = (smem_u32(smem_raw) + 1023u) & ~1023u;
   uint8_t* smem_gen = smem_raw + (smem - smem_u32(smem_raw));
@@ -157,9 +198,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     for (int s = 0; s < NS; ++s) {
       for (int x = 0; x < 3; ++x) {
         mbar_init(&bars.full[x][s], 1);
-        mbar_init(&bars.empty[x][s], 1);
+        // GLA with q / k out: A's slot is also released by the store lane once its TMA store read the tile
+        mbar_init(&bars.empty[x][s], (GLA && x == 0 && args.qk_out) ? 2 : 1);
       }
       mbar_init(&bars.b_scaled[s], NUM_KV);
+      mbar_init(&bars.xf_done[s], NUM_KV);
+      mbar_init(&bars.qk_stored[s], 1);
     }
     for (int s = 0; s < NSTAGE; ++s) {
       mbar_init(&bars.s_full[s], 1);
@@ -183,6 +227,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const double l = load_decay(args.lam, hi);
     pw[threadIdx.x] = (float)(pow_int(l, (int)threadIdx.x) * (l / l));
   }
+  if (GLA && args.theta != nullptr && threadIdx.x >= 160 && threadIdx.x < 160 + D / 2)
+    theta_s[threadIdx.x - 160] = (float)args.theta[threadIdx.x - 160];
   if (warp == WARP_TMA && lane == 0) {
     tma_prefetch(&map_a);
     tma_prefetch(&map_b);
@@ -241,6 +287,25 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         mbar_arrive(&bars.empty[2][s]);
       }
       tma_store_wait_all();
+    } else if (GLA && x == 4 && args.qk_out) {
+      // q / k lane: TMA-store each transformed A / B tile, then hand A's slot back to its ring and B's
+      // tile to the B warps (which scale it in place)
+      for (int t = 0; t < nchunks; ++t) {
+        const int s = t % NSTAGE;
+        mbar_wait(&bars.xf_done[s], (t / NSTAGE) & 1);
+        const int r0 = chunk_row0(t);
+        uint8_t* ga = smem_gen + (s * 3 + 0) * TILE;
+        uint8_t* gb = smem_gen + (s * 3 + 1) * TILE;
+        tma_store_4d(&map_qo, ga, 0, r0, hi, bi);
+        tma_store_4d(&map_qo, ga + HALF, 64, r0, hi, bi);
+        tma_store_4d(&map_ko, gb, 0, r0, hi, bi);
+        tma_store_4d(&map_ko, gb + HALF, 64, r0, hi, bi);
+        tma_store_commit();
+        tma_store_wait_read();
+        mbar_arrive(&bars.qk_stored[s]);
+        mbar_arrive(&bars.empty[0][s]);
+      }
+      tma_store_wait_all();
     }
   } else if (warp == WARP_MMA) {
     // ------------------------------------------------------------ MMA issuer
@@ -248,8 +313,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       auto issue_s = [&](int t) {  // S[t%2] = A B^T  (both K-major)
         const int s = t % NSTAGE;
         const uint32_t a_addr = tile_a(s), b_addr = tile_b(s);
-        mbar_wait(&bars.full[0][s], (t / NSTAGE) & 1);
-        mbar_wait(&bars.full[1][s], (t / NSTAGE) & 1);
+        if (GLA) {
+          mbar_wait(&bars.xf_done[s], (t / NSTAGE) & 1);  // the prologue transform (implies the TMA landed)
+        } else {
+          mbar_wait(&bars.full[0][s], (t / NSTAGE) & 1);
+          mbar_wait(&bars.full[1][s], (t / NSTAGE) & 1);
+        }
         // S[t%2] overwrites the TMEM columns P(t-2) / A~(t-2) were read from: those TS-MMAs must have
         // retired (in-order issue alone does not order a TMEM A-operand read before a later D write)
         if (t >= 2) mbar_wait(&bars.y_done[t & 1], ((t - 2) >> 1) & 1);
@@ -273,8 +342,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const uint32_t b_addr = tile_b(s), c_addr = tile_c(s);
         const uint32_t sbuf = tmem + TM_S0 + (t & 1) * 128;
         if (s_issued == t + 1 && t + 1 < nchunks &&
-            mbar_try_wait(smem_u32(&bars.full[0][(t + 1) % NSTAGE]), ((t + 1) / NSTAGE) & 1) &&
-            mbar_try_wait(smem_u32(&bars.full[1][(t + 1) % NSTAGE]), ((t + 1) / NSTAGE) & 1)) {
+            (GLA ? mbar_try_wait(smem_u32(&bars.xf_done[(t + 1) % NSTAGE]), ((t + 1) / NSTAGE) & 1)
+                 : (mbar_try_wait(smem_u32(&bars.full[0][(t + 1) % NSTAGE]), ((t + 1) / NSTAGE) & 1) &&
+                    mbar_try_wait(smem_u32(&bars.full[1][(t + 1) % NSTAGE]), ((t + 1) / NSTAGE) & 1)))) {
           issue_s(t + 1);  // run ahead: S(t+1) as soon as its operands landed
           s_issued = t + 2;
         }
@@ -463,6 +533,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const int b = chunk_len(t);
       mbar_wait(&bars.s_full[t & 1], (t >> 1) & 1);
       if (warp == WARP_O && lane == 0) LA_TR(t, 11);
+      if (GLA && args.qk_out) mbar_wait(&bars.qk_stored[s], (t / NS) & 1);  // k's TMA store read B first
       // B~ = in_scale * B, in place once S has consumed B (row i, this warp's 64 columns):
       // fwd lam^(b-1-i), rev lam^(i+1).  Row scaling is order-free, so visit the row's 16-byte chunks in
       // swizzled order: lane i touches physical chunk m ^ (i & 7), spreading a warp over all 32 banks.
@@ -540,6 +611,70 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars.st_ready);
     };
+    // GLA prologue on chunk t's landed A (qp) and B (kp) tiles, in place: row i, this warp's 64 columns
+    // (32 feature pairs (2j, 2j+1), j = 32 hh + 4 c + e); rows past n are zeroed
+    auto transform = [&](int t) {
+      const int s = t % NS;
+      const int r0 = chunk_row0(t);
+      const bool rot = args.theta != nullptr;
+      // the chunk's LRPE anchors cos / sin(theta_j (r0 + offset)), exact (fp64-reduced); row i then adds the
+      // local angle theta_j i < 128 rad in fp32 by the angle-addition formula
+      if (rot) {
+        named_bar_sync(1, NUM_KV * 32);  // the previous chunk's anchors are no longer read
+        if (warp == WARP_KV + 4 || warp == WARP_KV + 5) {
+          const int j = (warp - WARP_KV - 4) * 32 + lane;
+          float c0, s0;
+          lrpe_cs(args.theta[j], (int64_t)r0 + args.offset, &c0, &s0);
+          anchor_s[j] = make_float2(c0, s0);
+        }
+        named_bar_sync(1, NUM_KV * 32);
+      }
+      mbar_wait(&bars.full[0][s], (t / NS) & 1);
+      mbar_wait(&bars.full[1][s], (t / NS) & 1);
+      const bool valid = r0 + i < p1;
+      const uint32_t arow = tile_a(s) + hh * HALF + i * 128, brow = tile_b(s) + hh * HALF + i * 128;
+      const uint32_t half2 = 0x3F003F00u;  // bf16x2 (0.5, 0.5)
+#pragma unroll 2
+      for (int c = 0; c < 8; ++c) {
+        const uint32_t off = (uint32_t)((c ^ (i & 7)) << 4);
+        const uint4 xa = lds128(arow + off), xb = lds128(brow + off);
+        const uint32_t wa[4] = {xa.x, xa.y, xa.z, xa.w}, wb[4] = {xb.x, xb.y, xb.z, xb.w};
+        uint32_t ya[4], yb[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          float cs = 1.f, sn = 0.f;
+          if (rot) {
+            const int j = hh * 32 + 4 * c + e;
+            float cl, sl;
+            __sincosf(theta_s[j] * (float)i, &sl, &cl);
+            const float2 an = anchor_s[j];
+            cs = an.x * cl - an.y * sl;
+            sn = an.y * cl + an.x * sl;
+          }
+          float a0 = bf16lo(wa[e]), a1 = bf16hi(wa[e]), b0 = bf16lo(wb[e]), b1 = bf16hi(wb[e]);
+          if (args.act == LA_ACT_SWISH) {
+            // sigmoid(x) = (1 + tanh(x / 2)) / 2 with one bf16x2 tanh per feature pair (x / 2 is exact)
+            const uint32_t ta = tanh_bf16x2(mul_bf16x2(wa[e], half2)), tb = tanh_bf16x2(mul_bf16x2(wb[e], half2));
+            a0 *= fmaf(0.5f, bf16lo(ta), 0.5f);
+            a1 *= fmaf(0.5f, bf16hi(ta), 0.5f);
+            b0 *= fmaf(0.5f, bf16lo(tb), 0.5f);
+            b1 *= fmaf(0.5f, bf16hi(tb), 0.5f);
+          } else if (args.act == LA_ACT_ONE_PLUS_ELU) {
+            a0 = gla_act(a0, LA_ACT_ONE_PLUS_ELU), a1 = gla_act(a1, LA_ACT_ONE_PLUS_ELU);
+            b0 = gla_act(b0, LA_ACT_ONE_PLUS_ELU), b1 = gla_act(b1, LA_ACT_ONE_PLUS_ELU);
+          }
+          if (!valid) a0 = a1 = b0 = b1 = 0.f;
+          ya[e] = pack_bf16x2(a0 * cs - a1 * sn, a0 * sn + a1 * cs);
+          yb[e] = pack_bf16x2(b0 * cs - b1 * sn, b0 * sn + b1 * cs);
+        }
+        sts128(arow + off, make_uint4(ya[0], ya[1], ya[2], ya[3]));
+        sts128(brow + off, make_uint4(yb[0], yb[1], yb[2], yb[3]));
+      }
+      fence_proxy_async_smem();  // the tensor core and the TMA store read the tiles next
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars.xf_done[s]);
+    };
+    if (GLA && nchunks > 0) transform(0);
     if (nchunks > 0) {
       const float d0 = pw[chunk_len(0)];
 #pragma unroll 1
@@ -570,6 +705,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     for (int t = 0; t < nchunks; ++t) {
       // the tensor core accumulated this chunk: read the state, publish it for chunk t+1 once X(t)
       // has finished reading the previous bf16 copy
+      if (GLA && t + 1 < nchunks) transform(t + 1);  // overlaps chunk t's products
       mbar_wait(&bars.ds_full, t & 1);
       mbar_wait(&bars.x_done, t & 1);
       if (warp == WARP_KV && lane == 0) LA_TR(t, 13);
@@ -663,13 +799,17 @@ bool tc_make_map(CUtensorMap* map, const void* base, const PassDesc& p, const St
 
 namespace {
 
-cudaError_t launch_tc(const PassDesc& p, cudaStream_t st) {
-  CUtensorMap ma, mb, mc, mo;
+// gla: nullptr for the plain pass; else the GLA-mode prologue parameters and the q / k out maps
+cudaError_t launch_tc(const PassDesc& p, cudaStream_t st, const GlaPrologue* gla = nullptr) {
+  CUtensorMap ma, mb, mc, mo, mqo, mko;
   std::memset(&ma, 0, sizeof(ma));
   std::memset(&mo, 0, sizeof(mo));
+  std::memset(&mqo, 0, sizeof(mqo));
+  std::memset(&mko, 0, sizeof(mko));
   if (!tc_make_map(&mb, p.b, p, p.sbb) || !tc_make_map(&mc, p.c, p, p.sc)) return cudaErrorInvalidValue;
   if (!tc_make_map(&ma, p.a, p, p.sa) || !tc_make_map(&mo, p.out, p, p.so)) return cudaErrorInvalidValue;
   TcArgs a;
+  std::memset(&a, 0, sizeof(a));
   a.out = reinterpret_cast<uint16_t*>(p.out);
   a.heads = p.heads;
   a.n = p.n;
@@ -683,13 +823,24 @@ cudaError_t launch_tc(const PassDesc& p, cudaStream_t st) {
   a.in_T = p.state_in_T;
   a.state_out = reinterpret_cast<float*>(p.state_out);
   a.out_T = p.state_out_T;
-  auto kern = tc_pass_kernel;
   const size_t smem_bytes = SMEM_BYTES;
-  static std::atomic<bool> smem_set[64] = {};
-  cudaError_t err = set_smem_once(kern, (int)smem_bytes, smem_set);
-  if (err != cudaSuccess) return err;
   dim3 grid(p.nseg, p.batch * p.heads);
-  return launch_pdl(kern, grid, dim3(NUM_THREADS), smem_bytes, st, ma, mb, mc, mo, a);
+  if (gla == nullptr) {
+    static std::atomic<bool> smem_set[64] = {};
+    cudaError_t err = set_smem_once(tc_pass_kernel<false>, (int)smem_bytes, smem_set);
+    if (err != cudaSuccess) return err;
+    return launch_pdl(tc_pass_kernel<false>, grid, dim3(NUM_THREADS), smem_bytes, st, ma, mb, mc, mo, mqo, mko, a);
+  }
+  a.theta = gla->theta;
+  a.act = gla->act;
+  a.offset = gla->offset;
+  a.qk_out = gla->q_out != nullptr;
+  if (a.qk_out && (!tc_make_map(&mqo, gla->q_out, p, p.sa) || !tc_make_map(&mko, gla->k_out, p, p.sbb)))
+    return cudaErrorInvalidValue;
+  static std::atomic<bool> smem_set_gla[64] = {};
+  cudaError_t err = set_smem_once(tc_pass_kernel<true>, (int)smem_bytes, smem_set_gla);
+  if (err != cudaSuccess) return err;
+  return launch_pdl(tc_pass_kernel<true>, grid, dim3(NUM_THREADS), smem_bytes, st, ma, mb, mc, mo, mqo, mko, a);
 }
 
 bool aligned16(const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15) == 0; }
@@ -751,6 +902,11 @@ Plan tc_plan(int64_t bh, int64_t n, int d, int64_t want_segments, int sms) {
 cudaError_t tc_launch(const PassDesc& p, bool state_only, cudaStream_t st) {
   // summaries: the lean two-CTAs-per-SM kernel of la_summary.cu
   return state_only ? tc_summary_launch(p, st) : launch_tc(p, st);
+}
+
+cudaError_t tc_gla_fwd_launch(const PassDesc& p, const GlaPrologue& gla, cudaStream_t st) {
+  if (p.nseg != 1 || p.rev) return cudaErrorInvalidValue;  // the prologue runs on whole, forward sequences
+  return launch_tc(p, st, &gla);
 }
 
 }  // namespace la

@@ -22,6 +22,16 @@ cudaError_t tc_dkdv_launch(const PassDesc& p, const void* q, const void* k, cons
                            void* dk, void* dv, const Strides3* s, cudaStream_t st);
 // one launch of the main pass kernel (state_only = false) or of the per-segment summary kernel
 cudaError_t tc_launch(const PassDesc& p, bool state_only, cudaStream_t st);
+// GLA core forward (la_tc.cu GLA mode): the pass on (rot(act(a)), rot(act(b)), c) with the prologue
+// applied in shared memory; q_out / k_out (nullable together) receive the transformed tiles (strides sa / sbb)
+struct GlaPrologue {
+  const double* theta;  // [d/2] or nullptr
+  int act;
+  int64_t offset;
+  void* q_out;
+  void* k_out;
+};
+cudaError_t tc_gla_fwd_launch(const PassDesc& p, const GlaPrologue& gla, cudaStream_t st);
 // the fp32 pass (la_tc32.cu): three-term bf16 split on tcgen05, d = 128, 16-byte strides
 bool tc32_supported(int dtype, int d, const int64_t* strides, int count);
 Plan tc32_plan(int64_t bh, int64_t n, int64_t want_segments, int sms);

@@ -9,7 +9,9 @@ stage in numpy fp64; here the layer is
 with the five projections as library GEMMs (torch / cuBLAS), the element-wise stages as the
 fused CUDA kernels behind ``la_gla_*`` (one read and one write of every operand per stage), and
 the attention core as one batched ``la_fwd`` / ``la_bwd`` over all heads on the model-native
-[batch, n, heads, d] layout (no transposes).  There is no CPU fallback.
+[batch, n, heads, d] layout (no transposes).  Where batch * heads fills the GPU (bf16, d = 128) the
+forward runs the fused core instead (``la_gla_core_fwd``: act + LRPE applied to each q / k tile in the
+pass kernel's shared memory, no q / k round trip before the core).  There is no CPU fallback.
 
 Scope: ``gla_act`` swish / one_plus_elu / none, the U gate on or off, the parameter-free
 ``srmsnorm`` (the reference default ``norm``); LRPE rotation when ``theta`` is given (the
@@ -24,6 +26,7 @@ from dataclasses import dataclass
 import torch
 
 from . import ops
+from ._lib import UnsupportedError
 from .errors import ShapeError
 
 
@@ -32,13 +35,22 @@ class GlaCore(torch.autograd.Function):
 
     @staticmethod
     def forward(ctx, qp, kp, v, u, theta, lam_dev, heads, act, offset, eps, backend):
-        q, k = ops.gla_prologue(qp, kp, heads, act=act, theta=theta, offset=offset)
-        b, n, w = q.shape
-        d = w // heads
-        q4, k4, v4 = (t.view(b, n, heads, d) for t in (q, k, v.contiguous()))
-        a, seg = ops.la_forward(q4, k4, v4, None, layout="bnhd", backend=backend, lam_dev=lam_dev,
-                                want_seg_states=True)
-        a = a.view(b, n, w)
+        a = seg = None
+        if backend in ("auto", "tcgen05"):
+            # the fused core (act + LRPE in the pass kernel's load stage) where it applies
+            try:
+                a, q, k = ops.gla_core_forward(qp, kp, v, None, heads, act=act, theta=theta, offset=offset,
+                                               lam_dev=lam_dev)
+            except UnsupportedError:
+                a = None
+        if a is None:
+            q, k = ops.gla_prologue(qp, kp, heads, act=act, theta=theta, offset=offset)
+            b, n, w = q.shape
+            d = w // heads
+            q4, k4, v4 = (t.view(b, n, heads, d) for t in (q, k, v.contiguous()))
+            a, seg = ops.la_forward(q4, k4, v4, None, layout="bnhd", backend=backend, lam_dev=lam_dev,
+                                    want_seg_states=True)
+            a = a.view(b, n, w)
         gated, rawnorm = ops.gla_epilogue(a, u, heads, eps=eps)
         ctx.save_for_backward(qp, kp, q, k, v, u, a, rawnorm, theta, lam_dev, seg)
         ctx.cfg = (heads, act, offset, eps, backend)
@@ -108,11 +120,15 @@ class DecodeState:
         b, n, _ = x.shape
         qp, kp, v = x @ w.wq, x @ w.wk, x @ w.wv
         u = x @ w.wu if w.wu is not None else None
-        q, k = ops.gla_prologue(qp, kp, heads, act=act, theta=theta, offset=0)
-        wd = q.shape[-1]
+        wd = qp.shape[-1]
         d = wd // heads
-        a, kv = ops.la_forward(q.view(b, n, heads, d), k.view(b, n, heads, d), v.contiguous().view(b, n, heads, d),
-                               lam, layout="bnhd", want_state=True)
+        try:  # the fused core; a prefill needs no q / k for a backward
+            a, _, _, kv = ops.gla_core_forward(qp, kp, v, lam, heads, act=act, theta=theta, want_qk=False,
+                                               want_state=True)
+        except UnsupportedError:
+            q, k = ops.gla_prologue(qp, kp, heads, act=act, theta=theta, offset=0)
+            a, kv = ops.la_forward(q.view(b, n, heads, d), k.view(b, n, heads, d),
+                                   v.contiguous().view(b, n, heads, d), lam, layout="bnhd", want_state=True)
         gated, _ = ops.gla_epilogue(a.view(b, n, wd), u, heads, eps=eps)
         return gated @ w.wo, cls(kv, n)
 
