@@ -8,8 +8,9 @@
 // masked scores P = S * M (fp32 in TMEM, split in place) and the bf16 copy of the carried state (split
 // into a hi and a lo tile).  TF32 alone measured 5.6e-4 .. 8.5e-4, over the bar.
 //
-// One CTA per (batch, head, segment), chunks of C = 128 rows, 8 warps that all take part in every phase
-// (thread = chunk row i and a 64-column half hh; warp w owns TMEM lanes 32 (w % 4) ..):
+// One CTA per (batch, head, segment), chunks of C = 128 rows.  Warps 0-7 are workers (thread = chunk row i
+// and a 64-column half hh; warp w owns TMEM lanes 32 (w % 4) ..); warp 8 issues: lane 0 every MMA, lane 1
+// every TMA load / store, between mbarrier hand-offs with the workers:
 //
 //   TMA  A, B, C fp32 tiles (4 boxes of [128 rows][32 fp32], 128B swizzle) into 64 KB regions
 //   cvt  each region in place -> its bf16 hi tile | lo tile (the MMA's K-major / MN-major 128B-swizzle
@@ -17,17 +18,18 @@
 //   S    = A B^T                                 3 x 8 SS-MMAs (M = N = K = 128)       -> TMEM S
 //   P    = S * M, split in place (per 32-key block: 16 hi columns | 16 lo columns)
 //   B~   = in_scale * B, recombined from hi + lo, re-split in place (after S read B)
-//   for value half h = 0, 1 (the state's bf16 hi + lo copy of one half fits the 32 KB left):
-//     publish state[:, h] (hi, lo) to SMEM, pre-scale the TMEM state half by lam^b
-//     X_h  O[:, h] = A~ state[:, h]              3 x 8 TS-MMAs (M = 128, N = 64)
-//     U_h  state[:, h] += B~^T C[:, h]           3 x 8 SS-MMAs (M = 128, N = 64)
+//   X_h  O[:, h] = A~ state[:, h] for value half h = 0, 1 (the bf16 hi + lo copy of one state half fits the
+//        32 KB left; half 1's copy waits in registers until X_0 read half 0's)
+//                                                3 x 8 TS-MMAs each (M = 128, N = 64)
+//   U    state = lam^b state + B~^T C           TMEM state pre-scaled by the workers; 3 x 8 SS-MMAs (N = 128)
 //   Y    O += P C                                3 x 8 TS-MMAs (M = N = 128)
-//   out  TMEM O -> fp32 rows -> global
+//   out  TMEM O -> fp32 rows staged in C's region -> TMA store
 //
 // SMEM: 3 x 64 KB operand regions + 32 KB state half = 224 KB.  TMEM: S | A~ | O | state = 512 columns.
-// S is issued once A and B are split, and runs while C is split and the first state half published.  The
-// A region is refilled as soon as S has read it, B and C once chunk t's MMAs are done.  State-only
-// mode (segment summaries, la_api.cu segment_states) runs B~ and U only.
+// Overlap: the state is published while S runs (C is split last: its refill waits for the previous output's
+// store); the next chunk's A is split while the state update, X_1 and Y run.  The A region is refilled as soon as S has read it,
+// B after the state update, C once the output rows staged in it are stored.  State-only mode (segment summaries, la_api.cu segment_states) runs B~ and
+// U only.
 #include <cudaTypedefs.h>
 
 #include <algorithm>
@@ -44,28 +46,46 @@ namespace {
 
 using namespace ptx;
 
+#ifdef LA_TRACE
+// debug build only: thread 0 of CTA (0, 0) stamps the phases of its first 32 chunks ([chunk][16 events])
+__device__ unsigned long long* g_tc32_trace = nullptr;
+#define T32(t, ev)                                                               \
+  do {                                                                           \
+    if (t32p != nullptr && tid == 0 && (t) < 32) t32p[(t) * 16 + (ev)] = clock64(); \
+  } while (0)
+#else
+#define T32(t, ev) \
+  do {             \
+  } while (0)
+#endif
+
 constexpr int C = 128;
 constexpr int D = 128;
 constexpr int BOX = C * 32 * 4;        // 16 KB: one TMA box, 32 fp32 columns
 constexpr int REGION = 4 * BOX;        // 64 KB: one fp32 operand tile = its bf16 hi + lo tiles
 constexpr int HALF = C * 64 * 2;       // 16 KB: [128 rows][64 bf16], one 128B-swizzle column block
 constexpr int BF_TILE = 2 * HALF;      // 32 KB: one bf16 tile (hi or lo)
-constexpr int NTHREADS = 256;
+constexpr int NUM_WORKERS = 8;                  // warps 0-7: conversions (thread = row i, half hh)
+constexpr int WARP_ISSUE = NUM_WORKERS;          // warp 8: lane 0 issues the MMAs, lane 1 the TMA loads / stores
+constexpr int NTHREADS = (NUM_WORKERS + 1) * 32;
 constexpr uint32_t TM_S = 0, TM_AT = 128, TM_O = 256, TM_ST = 384, TM_COLS = 512;
 constexpr uint32_t R_A = 0, R_B = REGION, R_C = 2 * REGION, R_ST = 3 * REGION;
 constexpr size_t SMEM_BYTES = 3 * (size_t)REGION + 2 * HALF + 1024;
 
 constexpr uint32_t IDESC_S = idesc_bf16(128, 128, 0, 0);    // A, B K-major
 constexpr uint32_t IDESC_X = idesc_bf16(128, 64, 0, 1);     // A from TMEM, B (state half) MN-major
-constexpr uint32_t IDESC_U = idesc_bf16(128, 64, 1, 1);     // A = B~^T MN-major, B = C half MN-major
-constexpr uint32_t IDESC_U128 = idesc_bf16(128, 128, 1, 1); // state-only: the whole state at once
+constexpr uint32_t IDESC_U128 = idesc_bf16(128, 128, 1, 1); // A = B~^T MN-major, B = C MN-major: the whole state
 constexpr uint32_t IDESC_Y = idesc_bf16(128, 128, 0, 1);    // A = P from TMEM, B = C MN-major
 
 struct Bars {
   uint64_t full[3];   // TMA: A, B, C fp32 tiles landed
   uint64_t s_done;    // MMA: S read A, B
-  uint64_t x0_done;   // MMA: X_0 / U_0 done (the state-half SMEM copy is reusable)
+  uint64_t x0_done;   // MMA: X_0 done (the state-half SMEM copy is reusable)
+  uint64_t u1_done;   // MMA: the state update done (the last reader of B)
+  uint64_t x1_done;   // MMA: X_1 done (A~'s last reader)
   uint64_t all_done;  // MMA: every product of the chunk done
+  uint64_t go_s, go_x0, go_x1;  // workers -> issuer: operands of S / of X_0, U_0 / of X_1, U_1, Y ready
+  uint64_t o_staged;            // workers -> issuer: O(t) staged in C's region for the TMA store
   uint32_t tmem_base;
 };
 
@@ -120,7 +140,8 @@ __device__ __forceinline__ void write_split(uint32_t region, int i, int hh, cons
 template <bool STATE_ONLY>
 __global__ void __launch_bounds__(NTHREADS, 1)
     tc32_pass_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
-                     const __grid_constant__ CUtensorMap map_c, const Tc32Args args) {
+                     const __grid_constant__ CUtensorMap map_c, const __grid_constant__ CUtensorMap map_o,
+                     const Tc32Args args) {
   extern __shared__ uint8_t smem_raw[];
   __shared__ Bars bars;
   __shared__ __align__(16) float pw[C + 8];  // lam^0 .. lam^128
@@ -128,8 +149,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   uint8_t* smem_gen = smem_raw + (smem - smem_u32(smem_raw));
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int i = tid & 127;   // chunk row == TMEM lane (warp w owns lanes 32 (w % 4) ..)
-  const int hh = tid >> 7;   // 64-column half
+  const bool worker = warp < NUM_WORKERS;
+  const int i = tid & 127;   // worker: chunk row == TMEM lane (warp w owns lanes 32 (w % 4) ..)
+  const int hh = (tid >> 7) & 1;  // worker: 64-column half
   const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
   const int seg = blockIdx.x, bh = blockIdx.y;
   const int bi = bh / args.heads, hi = bh % args.heads;
@@ -139,13 +161,21 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   const int rev = args.rev;
   auto chunk_row0 = [&](int t) { return p0 + (rev ? (nchunks - 1 - t) : t) * C; };
   auto chunk_len = [&](int t) { return min(C, p1 - chunk_row0(t)); };
-  (void)lane;
+#ifdef LA_TRACE
+  unsigned long long* const t32p = (blockIdx.x == 0 && blockIdx.y == 0) ? g_tc32_trace : nullptr;
+#endif
 
   if (tid == 0) {
     for (int x = 0; x < 3; ++x) mbar_init(&bars.full[x], 1);
     mbar_init(&bars.s_done, 1);
     mbar_init(&bars.x0_done, 1);
+    mbar_init(&bars.u1_done, 1);
+    mbar_init(&bars.x1_done, 1);
     mbar_init(&bars.all_done, 1);
+    mbar_init(&bars.go_s, NUM_WORKERS);
+    mbar_init(&bars.go_x0, NUM_WORKERS);
+    mbar_init(&bars.go_x1, NUM_WORKERS);
+    mbar_init(&bars.o_staged, NUM_WORKERS);
     fence_mbar_init();
   }
   griddep_wait();  // PDL: the previous kernel of the stream has completed
@@ -160,172 +190,91 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #pragma unroll
     for (int kb = 0; kb < 4; ++kb) tma_load_4d(map, &bars.full[x], g + kb * BOX, 32 * kb, chunk_row0(t), hi, bi);
   };
-  if (tid == 0 && nchunks > 0) {
-    if (!STATE_ONLY) tma_prefetch(&map_a);
+  const bool issuer = warp == WARP_ISSUE && lane == 0;
+  if (tid == 0 && nchunks > 0) {  // the thread that initialised the barriers: chunk 0's loads before the sync
+    if (!STATE_ONLY) {
+      tma_prefetch(&map_a);
+      tma_prefetch(&map_o);
+    }
     tma_prefetch(&map_b);
     tma_prefetch(&map_c);
     for (int x = STATE_ONLY ? 1 : 0; x < 3; ++x) load(x, 0);
   }
-  if (warp == 0) tmem_alloc(&bars.tmem_base, TM_COLS);
+  if (warp == WARP_ISSUE) tmem_alloc(&bars.tmem_base, TM_COLS);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = bars.tmem_base;
-  const uint32_t st_cols = tmem + lane_off + TM_ST + 64 * hh;  // this thread's 64 state columns, row i
-
-  // entering state (row i = the b-feature, columns = c-features), or zero
-  if (nchunks > 0) {
-#pragma unroll 1
-    for (int q4 = 0; q4 < 4; ++q4) {
-      uint32_t w[16];
-      if (!STATE_ONLY && args.state_in != nullptr) {
-        const float* src = args.state_in + (int64_t)bh * args.in_bh_stride + (int64_t)seg * args.in_seg_stride;
-        if (args.in_T) {
-#pragma unroll
-          for (int j = 0; j < 16; ++j) w[j] = __float_as_uint(src[(64 * hh + 16 * q4 + j) * D + i]);
-        } else {
-          const float4* s4 = reinterpret_cast<const float4*>(src + i * D + 64 * hh + 16 * q4);
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const float4 v = s4[j];
-            w[4 * j] = __float_as_uint(v.x), w[4 * j + 1] = __float_as_uint(v.y);
-            w[4 * j + 2] = __float_as_uint(v.z), w[4 * j + 3] = __float_as_uint(v.w);
-          }
-        }
-      } else {
-#pragma unroll
-        for (int j = 0; j < 16; ++j) w[j] = 0u;
-      }
-      tmem_st16(st_cols + 16 * q4, w);
-    }
-  }
-  tmem_st_wait();  // the state columns are read back by other threads (publish_half): order the stores
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
+  const uint32_t st_cols = tmem + lane_off + TM_ST + 64 * hh;  // worker: its 64 state columns, row i
 
   const uint32_t A_HI = smem + R_A, A_LO = A_HI + BF_TILE;
   const uint32_t B_HI = smem + R_B, B_LO = B_HI + BF_TILE;
   const uint32_t C_HI = smem + R_C, C_LO = C_HI + BF_TILE;
   const uint32_t ST_HI = smem + R_ST, ST_LO = ST_HI + HALF;
 
-  // all threads: make generic SMEM writes and TMEM stores visible to the tensor core, then sync
-  auto handoff = [&]() {
-    fence_proxy_async_smem();
-    tmem_st_wait();
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-  };
-  // publish bf16 hi / lo of state columns [64 h + 32 hh, +32) (row i) and pre-scale them by `decay`
-  auto publish_half = [&](int h, float decay) {
-    float x[32];
-    tmem_ld32(tmem + lane_off + TM_ST + 64 * h + 32 * hh, x);
-    tmem_ld_wait();
-    uint32_t hw[16], lw[16], sc[32];
-#pragma unroll
-    for (int q = 0; q < 16; ++q) split2(x[2 * q], x[2 * q + 1], hw[q], lw[q]);
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      sts128(ST_HI + sw128(i, 4 * hh + c), make_uint4(hw[4 * c], hw[4 * c + 1], hw[4 * c + 2], hw[4 * c + 3]));
-      sts128(ST_LO + sw128(i, 4 * hh + c), make_uint4(lw[4 * c], lw[4 * c + 1], lw[4 * c + 2], lw[4 * c + 3]));
-    }
-#pragma unroll
-    for (int j = 0; j < 32; ++j) sc[j] = __float_as_uint(x[j] * decay);
-    tmem_st16(tmem + lane_off + TM_ST + 64 * h + 32 * hh, *reinterpret_cast<uint32_t(*)[16]>(sc));
-    tmem_st16(tmem + lane_off + TM_ST + 64 * h + 32 * hh + 16, *reinterpret_cast<uint32_t(*)[16]>(sc + 16));
-  };
-
-  for (int t = 0; t < nchunks; ++t) {
-    const uint32_t ph = t & 1;
-    const int r0 = chunk_row0(t);
-    const int b = chunk_len(t);
-    const float decay = pw[b];
-    float isc = i < b ? (rev ? pw[i + 1] : pw[b - 1 - i]) : 0.f;
-#ifdef LA_MUTATE_DKV
-    if (rev) isc = -isc;  // fault injection: the reference's `_dkv_step` sign flip (test_kernels.py:249-268)
-#endif
-    // ---------------------------------------------------------------- split the landed fp32 tiles
-    if (!STATE_ONLY) {
-      mbar_wait(&bars.full[0], ph);
-      float x[64];
-      read_f32_row(smem + R_A, i, hh, x);
-      {  // A~ = out_scale * A straight into TMEM: hi columns [32 hh, +32), lo columns [64 + 32 hh, +32)
-        const float osc = rev ? pw[max(b - 1 - i, 0)] : pw[i + 1];
-        uint32_t th[32], tl[32];
-#pragma unroll
-        for (int q = 0; q < 32; ++q) split2(osc * x[2 * q], osc * x[2 * q + 1], th[q], tl[q]);
-        const uint32_t at = tmem + lane_off + TM_AT + 32 * hh;
-        tmem_st16(at, *reinterpret_cast<uint32_t(*)[16]>(th));
-        tmem_st16(at + 16, *reinterpret_cast<uint32_t(*)[16]>(th + 16));
-        tmem_st16(at + 64, *reinterpret_cast<uint32_t(*)[16]>(tl));
-        tmem_st16(at + 80, *reinterpret_cast<uint32_t(*)[16]>(tl + 16));
-      }
-      uint32_t h[32], l[32];
-#pragma unroll
-      for (int q = 0; q < 32; ++q) split2(x[2 * q], x[2 * q + 1], h[q], l[q]);
-      __syncthreads();  // every thread has read the fp32 region
-      write_split(smem + R_A, i, hh, h, l);
-    }
-    {
-      mbar_wait(&bars.full[1], ph);
-      float x[64];
-      read_f32_row(smem + R_B, i, hh, x);
-      const float s = STATE_ONLY ? isc : 1.f;  // state-only: B~ directly (B is needed by no score)
-      uint32_t h[32], l[32];
-#pragma unroll
-      for (int q = 0; q < 32; ++q) split2(s * x[2 * q], s * x[2 * q + 1], h[q], l[q]);
-      __syncthreads();
-      write_split(smem + R_B, i, hh, h, l);
-    }
-    auto convert_c = [&]() {
-      mbar_wait(&bars.full[2], ph);
-      float x[64];
-      read_f32_row(smem + R_C, i, hh, x);
-      uint32_t h[32], l[32];
-#pragma unroll
-      for (int q = 0; q < 32; ++q) split2(x[2 * q], x[2 * q + 1], h[q], l[q]);
-      __syncthreads();
-      write_split(smem + R_C, i, hh, h, l);
-    };
-    if (STATE_ONLY) {
-      convert_c();
-      // pre-scale the state by lam^b, then state += B~^T C (whole width)
-      float x[32];
-#pragma unroll
-      for (int part = 0; part < 2; ++part) {
-        tmem_ld32(st_cols + 32 * part, x);
-        tmem_ld_wait();
-        uint32_t w[32];
-#pragma unroll
-        for (int j = 0; j < 32; ++j) w[j] = __float_as_uint(x[j] * decay);
-        tmem_st16(st_cols + 32 * part, *reinterpret_cast<uint32_t(*)[16]>(w));
-        tmem_st16(st_cols + 32 * part + 16, *reinterpret_cast<uint32_t(*)[16]>(w + 16));
-      }
-      handoff();
-      if (tid == 0) {
-#pragma unroll 1
-        for (int g = 0; g < 3; ++g) {
-          const uint32_t a = g == 2 ? B_LO : B_HI, c = g == 1 ? C_LO : C_HI;
-#pragma unroll
-          for (int kk = 0; kk < C / 16; ++kk)
-            mma_bf16_ss(tmem + TM_ST, smem_desc_sw128(a + kk * 2048, HALF, 1024),
-                        smem_desc_sw128(c + kk * 2048, HALF, 1024), IDESC_U128, 1);
+  if (warp == WARP_ISSUE && lane == 1) {
+    // ------------------------------------------------------------------ TMA lane (warp 8, lane 1): refills and
+    // the output stores, each as soon as its region is free (decoupled from the MMA lane, whose issue
+    // blocks while the tensor core's queue is full)
+    for (int t = 0; t < nchunks; ++t) {
+      if (STATE_ONLY) {
+        mbar_wait(&bars.all_done, t & 1);
+        if (t + 1 < nchunks) {
+          load(1, t + 1);
+          load(2, t + 1);
         }
-        mma_commit(&bars.all_done);
+        continue;
       }
-      mbar_wait(&bars.all_done, ph);
-      tc_fence_after();
-      if (tid == 0 && t + 1 < nchunks) {
-        load(1, t + 1);
-        load(2, t + 1);
-      }
-      continue;
+      mbar_wait(&bars.s_done, t & 1);
+      if (t + 1 < nchunks) load(0, t + 1);  // A's SMEM tiles consumed by S
+      mbar_wait(&bars.u1_done, t & 1);
+      if (t + 1 < nchunks) load(1, t + 1);  // B's by the state update
+      // out(t): staged by the workers in C's region once the chunk's products are done; store it, then
+      // refill C with the next chunk's tile
+      mbar_wait(&bars.o_staged, t & 1);
+#pragma unroll
+      for (int kb = 0; kb < 4; ++kb) tma_store_4d(&map_o, smem_gen + R_C + kb * BOX, 32 * kb, chunk_row0(t), hi, bi);
+      tma_store_commit();
+      tma_store_wait_read();
+      if (t + 1 < nchunks) load(2, t + 1);
     }
-    handoff();
-    // ---------------------------------------------------------------- S = A B^T (C's split and the first
-    // state publish overlap it)
-    if (tid == 0) {
+    tma_store_wait_all();
+    griddep_launch();
+  } else if (issuer) {
+    // ------------------------------------------------------------------ MMA lane (warp 8, lane 0)
+    auto go = [&](uint64_t* bar, int t) {
+      mbar_wait(bar, t & 1);
+      tc_fence_after();
+    };
+    auto issue_x = [&](int h) {  // O[:, h] = A~ state[:, h]
+#pragma unroll 1
+      for (int g = 0; g < 3; ++g) {
+        const uint32_t at = TM_AT + (g == 2 ? 64 : 0), st = g == 1 ? ST_LO : ST_HI;
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk)
+          mma_bf16_ts(tmem + TM_O + 64 * h, tmem + at + kk * 8, smem_desc_sw128(st + kk * 2048, HALF, 1024),
+                      IDESC_X, (g | kk) != 0);
+      }
+    };
+    auto issue_u = [&]() {  // state += B~^T C, both halves
+#pragma unroll 1
+      for (int g = 0; g < 3; ++g) {
+        const uint32_t a = g == 2 ? B_LO : B_HI, c = g == 1 ? C_LO : C_HI;
+#pragma unroll
+        for (int kk = 0; kk < C / 16; ++kk)
+          mma_bf16_ss(tmem + TM_ST, smem_desc_sw128(a + kk * 2048, HALF, 1024),
+                      smem_desc_sw128(c + kk * 2048, HALF, 1024), IDESC_U128, 1);
+      }
+    };
+    for (int t = 0; t < nchunks; ++t) {
+      if (STATE_ONLY) {
+        go(&bars.go_s, t);  // B~, C split; state pre-scaled
+        issue_u();
+        mma_commit(&bars.all_done);
+        continue;
+      }
+      // S = A B^T
+      go(&bars.go_s, t);  // A(t), B(t) split, A~(t) in TMEM; Y(t-1) done with P's columns (workers saw all_done)
 #pragma unroll 1
       for (int g = 0; g < 3; ++g) {
         const uint32_t a = g == 2 ? A_LO : A_HI, bb = g == 1 ? B_LO : B_HI;
@@ -337,77 +286,16 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
       }
       mma_commit(&bars.s_done);
-    }
-    convert_c();
-    publish_half(0, decay);
-    mbar_wait(&bars.s_done, ph);
-    tc_fence_after();
-    if (tid == 0 && t + 1 < nchunks) load(0, t + 1);  // A's tiles are consumed (A~ lives in TMEM)
-    // ---------------------------------------------------------------- P = S * M, split in place
-#pragma unroll 1
-    for (int cbi = 0; cbi < 2; ++cbi) {
-      const int cb = 2 * hh + cbi;
-      float v[32];
-      tmem_ld32(tmem + lane_off + TM_S + 32 * cb, v);
-      tmem_ld_wait();
-      uint32_t hw[16], lw[16];
-#pragma unroll
-      for (int jj = 0; jj < 32; jj += 2) {
-        const int j = 32 * cb + jj;
-        const int d0 = rev ? j - i : i - j, d1 = rev ? j + 1 - i : i - j - 1;
-        const float p0 = d0 >= 0 ? v[jj] * pw[d0] : 0.f;
-        const float p1v = d1 >= 0 ? v[jj + 1] * pw[d1] : 0.f;
-        split2(p0, p1v, hw[jj >> 1], lw[jj >> 1]);
-      }
-      tmem_st16(tmem + lane_off + TM_S + 32 * cb, hw);
-      tmem_st16(tmem + lane_off + TM_S + 32 * cb + 16, lw);
-    }
-    // ---------------------------------------------------------------- B~ = in_scale * B, in place
-    {
-      const uint32_t hb = B_HI + (uint32_t)(hh * HALF), lb = B_LO + (uint32_t)(hh * HALF);
-#pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        const uint4 xh = lds128(hb + sw128(i, c)), xl = lds128(lb + sw128(i, c));
-        const uint32_t hs[4] = {xh.x, xh.y, xh.z, xh.w}, ls[4] = {xl.x, xl.y, xl.z, xl.w};
-        uint32_t ho[4], lo[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e)
-          split2(isc * (bf16lo(hs[e]) + bf16lo(ls[e])), isc * (bf16hi(hs[e]) + bf16hi(ls[e])), ho[e], lo[e]);
-        sts128(hb + sw128(i, c), make_uint4(ho[0], ho[1], ho[2], ho[3]));
-        sts128(lb + sw128(i, c), make_uint4(lo[0], lo[1], lo[2], lo[3]));
-      }
-    }
-    handoff();
-    // ---------------------------------------------------------------- X_0, U_0
-    auto issue_xu = [&](int h) {
-#pragma unroll 1
-      for (int g = 0; g < 3; ++g) {
-        const uint32_t at = TM_AT + (g == 2 ? 64 : 0), st = g == 1 ? ST_LO : ST_HI;
-#pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk)
-          mma_bf16_ts(tmem + TM_O + 64 * h, tmem + at + kk * 8, smem_desc_sw128(st + kk * 2048, HALF, 1024), IDESC_X,
-                      (g | kk) != 0);
-      }
-#pragma unroll 1
-      for (int g = 0; g < 3; ++g) {
-        const uint32_t a = g == 2 ? B_LO : B_HI, c = (g == 1 ? C_LO : C_HI) + h * HALF;
-#pragma unroll
-        for (int kk = 0; kk < C / 16; ++kk)
-          mma_bf16_ss(tmem + TM_ST + 64 * h, smem_desc_sw128(a + kk * 2048, HALF, 1024),
-                      smem_desc_sw128(c + kk * 2048, HALF, 1024), IDESC_U, 1);
-      }
-    };
-    if (tid == 0) {
-      issue_xu(0);
+      // X_0 = A~ state[:, 0:64], the state update (B's last reader)
+      go(&bars.go_x0, t);  // P, B~, C, the first state half's copy, the state pre-scaled; O(t-1) drained
+      issue_x(0);
       mma_commit(&bars.x0_done);
-    }
-    mbar_wait(&bars.x0_done, ph);
-    tc_fence_after();
-    publish_half(1, decay);
-    handoff();
-    // ---------------------------------------------------------------- X_1, U_1, Y = P C
-    if (tid == 0) {
-      issue_xu(1);
+      issue_u();
+      mma_commit(&bars.u1_done);
+      // X_1 (A~'s last reader), Y = P C
+      go(&bars.go_x1, t);  // the second state half's copy in SMEM
+      issue_x(1);
+      mma_commit(&bars.x1_done);
 #pragma unroll 1
       for (int g = 0; g < 3; ++g) {
         const uint32_t pofs = g == 2 ? 16 : 0, c = g == 1 ? C_LO : C_HI;
@@ -419,59 +307,276 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       }
       mma_commit(&bars.all_done);
     }
-    mbar_wait(&bars.all_done, ph);
-    tc_fence_after();
-    if (tid == 0 && t + 1 < nchunks) {
-      load(1, t + 1);
-      load(2, t + 1);
+    // drain: every commit must land before the CTA retires
+    if (nchunks > 0) mbar_wait(&bars.all_done, (nchunks - 1) & 1);
+  } else if (worker) {
+    // ------------------------------------------------------------------ workers (warps 0-7): conversions
+    auto wbar = [&]() { named_bar_sync(1, NUM_WORKERS * 32); };
+    auto signal = [&](uint64_t* bar) {  // generic SMEM writes + TMEM stores -> the tensor core, then arrive
+      fence_proxy_async_smem();
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar);
+    };
+    auto await = [&](uint64_t* bar, int t) {
+      mbar_wait(bar, t & 1);
+      tc_fence_after();
+    };
+    // entering state (row i = the b-feature, columns = c-features), or zero
+    if (nchunks > 0) {
+#pragma unroll 1
+      for (int q4 = 0; q4 < 4; ++q4) {
+        uint32_t w[16];
+        if (!STATE_ONLY && args.state_in != nullptr) {
+          const float* src = args.state_in + (int64_t)bh * args.in_bh_stride + (int64_t)seg * args.in_seg_stride;
+          if (args.in_T) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) w[j] = __float_as_uint(src[(64 * hh + 16 * q4 + j) * D + i]);
+          } else {
+            const float4* s4 = reinterpret_cast<const float4*>(src + i * D + 64 * hh + 16 * q4);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const float4 v = s4[j];
+              w[4 * j] = __float_as_uint(v.x), w[4 * j + 1] = __float_as_uint(v.y);
+              w[4 * j + 2] = __float_as_uint(v.z), w[4 * j + 3] = __float_as_uint(v.w);
+            }
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) w[j] = 0u;
+        }
+        tmem_st16(st_cols + 16 * q4, w);
+      }
     }
-    // ---------------------------------------------------------------- out = O (fp32 rows)
-    {
-      float* orow = args.out + (int64_t)bi * args.so.b + (int64_t)hi * args.so.h + (int64_t)(r0 + i) * args.so.n +
-                    64 * hh;
+    tmem_st_wait();  // the state columns are read back by other workers (take_half): order the stores
+    tc_fence_before();
+    wbar();
+    tc_fence_after();
+    // fp32 region x -> its bf16 hi / lo tiles, every element scaled by `sc`
+    auto split_region = [&](uint32_t region, int x, int t, float sc) {
+      mbar_wait(&bars.full[x], t & 1);
+      float v[64];
+      read_f32_row(smem + region, i, hh, v);
+      uint32_t h[32], l[32];
+#pragma unroll
+      for (int q = 0; q < 32; ++q) split2(sc * v[2 * q], sc * v[2 * q + 1], h[q], l[q]);
+      wbar();  // every worker has read the fp32 region
+      write_split(smem + region, i, hh, h, l);
+    };
+    // A of chunk t: SMEM hi / lo tiles; A~ = out_scale A's words returned for TMEM
+    auto convert_a = [&](int t, uint32_t (&th)[32], uint32_t (&tl)[32]) {
+      const int b = chunk_len(t);
+      mbar_wait(&bars.full[0], t & 1);
+      float x[64];
+      read_f32_row(smem + R_A, i, hh, x);
+      const float osc = rev ? pw[max(b - 1 - i, 0)] : pw[i + 1];
+#pragma unroll
+      for (int q = 0; q < 32; ++q) split2(osc * x[2 * q], osc * x[2 * q + 1], th[q], tl[q]);
+      uint32_t h[32], l[32];
+#pragma unroll
+      for (int q = 0; q < 32; ++q) split2(x[2 * q], x[2 * q + 1], h[q], l[q]);
+      wbar();
+      write_split(smem + R_A, i, hh, h, l);
+    };
+    auto store_at = [&](const uint32_t (&th)[32], const uint32_t (&tl)[32]) {
+      const uint32_t at = tmem + lane_off + TM_AT + 32 * hh;  // hi columns [32 hh, +32), lo [64 + 32 hh, +32)
+      tmem_st16(at, *reinterpret_cast<const uint32_t(*)[16]>(th));
+      tmem_st16(at + 16, *reinterpret_cast<const uint32_t(*)[16]>(th + 16));
+      tmem_st16(at + 64, *reinterpret_cast<const uint32_t(*)[16]>(tl));
+      tmem_st16(at + 80, *reinterpret_cast<const uint32_t(*)[16]>(tl + 16));
+    };
+    // bf16 hi / lo of state columns [64 h + 32 hh, +32) (row i) -> hw / lw; the TMEM copy pre-scaled by `decay`
+    auto take_half = [&](int h, float decay, uint32_t (&hw)[16], uint32_t (&lw)[16]) {
+      float x[32];
+      tmem_ld32(tmem + lane_off + TM_ST + 64 * h + 32 * hh, x);
+      tmem_ld_wait();
+      uint32_t sc[32];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) split2(x[2 * q], x[2 * q + 1], hw[q], lw[q]);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) sc[j] = __float_as_uint(x[j] * decay);
+      tmem_st16(tmem + lane_off + TM_ST + 64 * h + 32 * hh, *reinterpret_cast<uint32_t(*)[16]>(sc));
+      tmem_st16(tmem + lane_off + TM_ST + 64 * h + 32 * hh + 16, *reinterpret_cast<uint32_t(*)[16]>(sc + 16));
+    };
+    auto publish = [&](const uint32_t (&hw)[16], const uint32_t (&lw)[16]) {  // -> the SMEM state-half copy
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        sts128(ST_HI + sw128(i, 4 * hh + c), make_uint4(hw[4 * c], hw[4 * c + 1], hw[4 * c + 2], hw[4 * c + 3]));
+        sts128(ST_LO + sw128(i, 4 * hh + c), make_uint4(lw[4 * c], lw[4 * c + 1], lw[4 * c + 2], lw[4 * c + 3]));
+      }
+    };
+    // the state entering chunk t: half 0's bf16 copy to SMEM, half 1's kept in registers (h1w / h1l) until X_0
+    // has read the SMEM copy; the TMEM state pre-scaled by lam^b(t) for the chunk's whole-width update
+    uint32_t h1w[16], h1l[16];
+    auto take_state = [&](int t) {
+      const float dec = pw[chunk_len(t)];
+      uint32_t hw[16], lw[16];
+      take_half(0, dec, hw, lw);
+      publish(hw, lw);
+      take_half(1, dec, h1w, h1l);
+    };
+    if (!STATE_ONLY && nchunks > 0) {  // chunk 0's A (later chunks': while the previous one's products run)
+      uint32_t th[32], tl[32];
+      convert_a(0, th, tl);
+      store_at(th, tl);
+    }
+    const int quad = warp & 3;
+    const uint32_t pw_addr = smem_u32(pw);
+    for (int t = 0; t < nchunks; ++t) {
+      const int b = chunk_len(t);
+      const float decay = pw[b];
+      float isc = i < b ? (rev ? pw[i + 1] : pw[b - 1 - i]) : 0.f;
+#ifdef LA_MUTATE_DKV
+      if (rev) isc = -isc;  // fault injection: the reference's `_dkv_step` sign flip (test_kernels.py:249-268)
+#endif
+      T32(t, 0);
+      if (STATE_ONLY) {
+        split_region(R_B, 1, t, isc);  // B~ directly (B feeds no score here)
+        split_region(R_C, 2, t, 1.f);
+#pragma unroll 1
+        for (int part = 0; part < 2; ++part) {  // pre-scale the state by lam^b
+          float x[32];
+          tmem_ld32(st_cols + 32 * part, x);
+          tmem_ld_wait();
+          uint32_t w[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) w[j] = __float_as_uint(x[j] * decay);
+          tmem_st16(st_cols + 32 * part, *reinterpret_cast<uint32_t(*)[16]>(w));
+          tmem_st16(st_cols + 32 * part + 16, *reinterpret_cast<uint32_t(*)[16]>(w + 16));
+        }
+        signal(&bars.go_s);
+        await(&bars.all_done, t);
+        continue;
+      }
+      split_region(R_B, 1, t, 1.f);
+      signal(&bars.go_s);  // A(t), A~(t), B(t)
+      T32(t, 1);
+      take_state(t);  // while S runs
+      await(&bars.s_done, t);
+      T32(t, 4);
+      // P = S * M, split in place: per 32-key block, a zero block (causality), an off-diagonal block
+      // (lam^|i-j| = per-row base x a broadcast ladder), or the diagonal block
+#pragma unroll 1
+      for (int cbi = 0; cbi < 2; ++cbi) {
+        const int cb = 2 * hh + cbi;
+        uint32_t hw[16], lw[16];
+        if (rev ? (cb < quad) : (cb > quad)) {
+#pragma unroll
+          for (int e = 0; e < 16; ++e) hw[e] = lw[e] = 0u;
+        } else {
+          float v[32];
+          tmem_ld32(tmem + lane_off + TM_S + 32 * cb, v);
+          if (cb != quad) {
+            const float base = rev ? pw[32 * cb - i] : pw[i - 32 * cb - 31];
+            tmem_ld_wait();
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              // ladder lam^(31 - jj) (fwd) or lam^jj (rev) for jj = 4q .. 4q+3, one broadcast LDS.128
+              const uint4 wq = lds128(pw_addr + 4 * (rev ? 4 * q : 28 - 4 * q));
+              float w0 = __uint_as_float(wq.x), w1 = __uint_as_float(wq.y), w2 = __uint_as_float(wq.z),
+                    w3 = __uint_as_float(wq.w);
+              if (!rev) {
+                const float t0 = w0, t1 = w1;
+                w0 = w3;
+                w1 = w2;
+                w2 = t1;
+                w3 = t0;
+              }
+              split2(v[4 * q] * (base * w0), v[4 * q + 1] * (base * w1), hw[2 * q], lw[2 * q]);
+              split2(v[4 * q + 2] * (base * w2), v[4 * q + 3] * (base * w3), hw[2 * q + 1], lw[2 * q + 1]);
+            }
+          } else {
+            tmem_ld_wait();
+#pragma unroll
+            for (int jj = 0; jj < 32; jj += 2) {
+              const int d0 = rev ? jj - lane : lane - jj, d1 = rev ? jj + 1 - lane : lane - jj - 1;
+              split2(d0 >= 0 ? v[jj] * pw[d0] : 0.f, d1 >= 0 ? v[jj + 1] * pw[d1] : 0.f, hw[jj >> 1], lw[jj >> 1]);
+            }
+          }
+        }
+        tmem_st16(tmem + lane_off + TM_S + 32 * cb, hw);
+        tmem_st16(tmem + lane_off + TM_S + 32 * cb + 16, lw);
+      }
+      // B~ = in_scale * B, in place (S has read B)
+      {
+        const uint32_t hb = B_HI + (uint32_t)(hh * HALF), lb = B_LO + (uint32_t)(hh * HALF);
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const uint4 xh = lds128(hb + sw128(i, c)), xl = lds128(lb + sw128(i, c));
+          const uint32_t hs[4] = {xh.x, xh.y, xh.z, xh.w}, ls[4] = {xl.x, xl.y, xl.z, xl.w};
+          uint32_t ho[4], lo[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            split2(isc * (bf16lo(hs[e]) + bf16lo(ls[e])), isc * (bf16hi(hs[e]) + bf16hi(ls[e])), ho[e], lo[e]);
+          sts128(hb + sw128(i, c), make_uint4(ho[0], ho[1], ho[2], ho[3]));
+          sts128(lb + sw128(i, c), make_uint4(lo[0], lo[1], lo[2], lo[3]));
+        }
+      }
+      split_region(R_C, 2, t, 1.f);  // C last: its load (after the previous output's store) had the most time
+      T32(t, 5);
+      signal(&bars.go_x0);
+      await(&bars.x0_done, t);
+      T32(t, 6);
+      publish(h1w, h1l);
+      signal(&bars.go_x1);
+      T32(t, 7);
+      // while the state update, X_1 and Y run: the next chunk's A (its SMEM tiles are free since S), its A~
+      // once X_1 has read A~
+      if (t + 1 < nchunks) {
+        uint32_t th[32], tl[32];
+        convert_a(t + 1, th, tl);
+        T32(t, 8);
+        await(&bars.x1_done, t);
+        T32(t, 9);
+        store_at(th, tl);
+      }
+      // out(t): O -> fp32 rows staged in C's region (TMA-store layout), stored by the TMA lane
+      await(&bars.all_done, t);
+      T32(t, 10);
 #pragma unroll 1
       for (int part = 0; part < 2; ++part) {
         float y[32];
         tmem_ld32(tmem + lane_off + TM_O + 64 * hh + 32 * part, y);
         tmem_ld_wait();
-        if (i < b) {
-          float4* o4 = reinterpret_cast<float4*>(orow + 32 * part);
+        const uint32_t box = smem + R_C + (uint32_t)((2 * hh + part) * BOX) + (uint32_t)(i * 128);
 #pragma unroll
-          for (int q = 0; q < 8; ++q) o4[q] = make_float4(y[4 * q], y[4 * q + 1], y[4 * q + 2], y[4 * q + 3]);
-        }
+        for (int c = 0; c < 8; ++c)
+          sts128(box + ((c ^ (i & 7)) << 4), make_uint4(__float_as_uint(y[4 * c]), __float_as_uint(y[4 * c + 1]),
+                                                         __float_as_uint(y[4 * c + 2]), __float_as_uint(y[4 * c + 3])));
       }
+      signal(&bars.o_staged);
+      T32(t, 11);
     }
-    tc_fence_before();
-  }
-  if (tid == 0) griddep_launch();
 
-  // ---------------------------------------------------------------- final state export
-  if (nchunks > 0) {
-    float* dst = nullptr;
-    int T = 0;
-    if (STATE_ONLY) {
-      dst = args.delta_out + ((int64_t)bh * args.nseg + seg) * D * D;
-    } else if (args.state_out != nullptr && (rev ? seg == 0 : seg == args.nseg - 1)) {
-      dst = args.state_out + (int64_t)bh * D * D;
-      T = args.out_T;
-    }
-    if (dst != nullptr) {
+    // ------------------------------------------------------------------ final state export
+    if (nchunks > 0) {
+      float* dst = nullptr;
+      int T = 0;
+      if (STATE_ONLY) {
+        dst = args.delta_out + ((int64_t)bh * args.nseg + seg) * D * D;
+      } else if (args.state_out != nullptr && (rev ? seg == 0 : seg == args.nseg - 1)) {
+        dst = args.state_out + (int64_t)bh * D * D;
+        T = args.out_T;
+      }
+      if (dst != nullptr) {
 #pragma unroll 1
-      for (int part = 0; part < 2; ++part) {
-        float x[32];
-        tmem_ld32(st_cols + 32 * part, x);
-        tmem_ld_wait();
+        for (int part = 0; part < 2; ++part) {
+          float x[32];
+          tmem_ld32(st_cols + 32 * part, x);
+          tmem_ld_wait();
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const int col = 64 * hh + 32 * part + j;
-          dst[T ? (col * D + i) : (i * D + col)] = x[j];
+          for (int j = 0; j < 32; ++j) {
+            const int col = 64 * hh + 32 * part + j;
+            dst[T ? (col * D + i) : (i * D + col)] = x[j];
+          }
         }
       }
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 0) {
+  if (warp == WARP_ISSUE) {
     tc_fence_after();
     tmem_dealloc(tmem, TM_COLS);
   }
@@ -507,6 +612,12 @@ bool tc32_make_map(CUtensorMap* map, const void* base, const PassDesc& p, const 
 
 }  // namespace
 
+#ifdef LA_TRACE
+extern "C" __attribute__((visibility("default"))) int la_debug_set_trace32(void* dev_ptr) {
+  return (int)cudaMemcpyToSymbol(g_tc32_trace, &dev_ptr, sizeof(dev_ptr));
+}
+#endif
+
 bool tc32_supported(int dtype, int d, const int64_t* strides, int count) {
   if (dtype != LA_F32 || d != D) return false;
   for (int x = 0; x < 3 * count; ++x)
@@ -530,10 +641,12 @@ Plan tc32_plan(int64_t bh, int64_t n, int64_t want_segments, int sms) {
 }
 
 cudaError_t tc32_launch(const PassDesc& p, bool state_only, cudaStream_t st) {
-  CUtensorMap ma, mb, mc;
+  CUtensorMap ma, mb, mc, mo;
   std::memset(&ma, 0, sizeof(ma));
+  std::memset(&mo, 0, sizeof(mo));
   if (!tc32_make_map(&mb, p.b, p, p.sbb) || !tc32_make_map(&mc, p.c, p, p.sc)) return cudaErrorInvalidValue;
-  if (!state_only && !tc32_make_map(&ma, p.a, p, p.sa)) return cudaErrorInvalidValue;
+  if (!state_only && (!tc32_make_map(&ma, p.a, p, p.sa) || !tc32_make_map(&mo, p.out, p, p.so)))
+    return cudaErrorInvalidValue;
   Tc32Args a;
   std::memset(&a, 0, sizeof(a));
   a.heads = p.heads;
@@ -542,8 +655,6 @@ cudaError_t tc32_launch(const PassDesc& p, bool state_only, cudaStream_t st) {
   a.nseg = p.nseg;
   a.rev = p.rev;
   a.lam = p.lam;
-  a.out = reinterpret_cast<float*>(p.out);
-  a.so = p.so;
   a.state_in = reinterpret_cast<const float*>(p.state_in);
   a.in_bh_stride = p.state_in_bh_stride;
   a.in_seg_stride = p.state_in_seg_stride;
@@ -556,12 +667,12 @@ cudaError_t tc32_launch(const PassDesc& p, bool state_only, cudaStream_t st) {
     static std::atomic<bool> set[64] = {};
     cudaError_t err = set_smem_once(tc32_pass_kernel<true>, (int)SMEM_BYTES, set);
     if (err != cudaSuccess) return err;
-    return launch_pdl(tc32_pass_kernel<true>, grid, dim3(NTHREADS), SMEM_BYTES, st, ma, mb, mc, a);
+    return launch_pdl(tc32_pass_kernel<true>, grid, dim3(NTHREADS), SMEM_BYTES, st, ma, mb, mc, mo, a);
   }
   static std::atomic<bool> set[64] = {};
   cudaError_t err = set_smem_once(tc32_pass_kernel<false>, (int)SMEM_BYTES, set);
   if (err != cudaSuccess) return err;
-  return launch_pdl(tc32_pass_kernel<false>, grid, dim3(NTHREADS), SMEM_BYTES, st, ma, mb, mc, a);
+  return launch_pdl(tc32_pass_kernel<false>, grid, dim3(NTHREADS), SMEM_BYTES, st, ma, mb, mc, mo, a);
 }
 
 }  // namespace la
