@@ -37,6 +37,9 @@ using namespace ptx;
 #ifndef LA_PFKV_DIST
 #define LA_PFKV_DIST 1  // chunks ahead
 #endif
+#ifndef LA_POLL_NS
+#define LA_POLL_NS 0  // back-off of the polling producer when no ring advanced (0: spin)
+#endif
 #ifndef LA_PFKV
 #define LA_PFKV 1  // L2 prefetch of the next K and V tiles (+1.2% on the bench sweep, same-box A/B)
 #endif
@@ -235,6 +238,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       long long t0 = 0;
       for (uint32_t spins = 1; next[0] < nchunks || next[1] < nchunks || next[2] < nchunks || next[3] < nchunks;
            ++spins) {
+#if LA_POLL_NS > 0
+        const int issued_before = next[0] + next[1] + next[2] + next[3];
+#endif
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
           const int t = next[r];
@@ -261,6 +267,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #endif
           next[r] = t + 1;
         }
+#if LA_POLL_NS > 0
+        if (next[0] + next[1] + next[2] + next[3] == issued_before) __nanosleep(LA_POLL_NS);  // nothing free yet
+#endif
         if ((spins & 0xFFFFF) == 0) {  // watchdog, as mbar_wait
           if (t0 == 0) t0 = clock64();
           else if (clock64() - t0 > 40000000000LL) __trap();
