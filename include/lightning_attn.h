@@ -224,16 +224,17 @@ LA_API int la_gla_prologue(const la_gla_desc* desc, const void* qp, const void* 
 LA_API int la_gla_prologue_bwd(const la_gla_desc* desc, const void* qp, const void* kp, const double* theta,
                         const void* dq, const void* dk, void* dqp, void* dkp, double* dtheta,
                         void* workspace, size_t workspace_bytes, void* stream);
-/* Fused GLA core forward: o = LA(rot(act(qp)), rot(act(kp)), v) in ONE
- * tcgen05 pass -- the prologue (act, and LRPE when theta != NULL) is applied to each q / k tile in
- * shared memory between its TMA load and the first MMA, so qp / kp stream straight into the core;
- * q_out / k_out (both or neither) receive the transformed rows for the backward (la_bwd on them).
- * kv_in / kv_out as la_fwd.  Rows are [batch, n, heads * d], contiguous.  bf16, d = 128, and a plan
- * without sequence segments (batch * heads filling >= 60% of the SMs): LA_ERR_UNSUPPORTED otherwise
- * -- then la_gla_prologue + la_fwd compute the same thing in two steps. */
+/* Fused GLA core forward: o = LA(rot(act(qp)), rot(act(kp)), v) with the
+ * prologue (act, and LRPE when theta != NULL) applied to each q / k tile in shared memory between its
+ * TMA load and the first MMA -- in the segment-summary pass too when the plan splits sequences -- so
+ * qp / kp stream straight into the core; q_out / k_out (both or neither) receive the transformed rows
+ * for the backward (la_bwd on them).  kv_in / kv_out as la_fwd.  Rows are [batch, n, heads * d],
+ * contiguous.  bf16 and d = 128 (LA_ERR_UNSUPPORTED otherwise: la_gla_prologue + la_fwd compute the
+ * same in two calls).  Workspace: la_gla_core_workspace_bytes (0 when sequences are not split). */
+LA_API size_t la_gla_core_workspace_bytes(const la_gla_desc* desc);
 LA_API int la_gla_core_fwd(const la_gla_desc* desc, const void* qp, const void* kp, const void* v,
                     const double* lam, const double* theta, const void* kv_in, void* o, void* q_out,
-                    void* k_out, void* kv_out, void* stream);
+                    void* k_out, void* kv_out, void* workspace, size_t workspace_bytes, void* stream);
 LA_API int la_gla_epilogue(const la_gla_desc* desc, const void* a, const void* u, void* gated,
                     void* rawnorm, void* stream);
 LA_API int la_gla_epilogue_bwd(const la_gla_desc* desc, const void* dgated, const void* a, const void* u,

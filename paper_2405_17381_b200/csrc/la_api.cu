@@ -747,9 +747,35 @@ int la_gla_prologue_bwd(const la_gla_desc* desc, const void* qp, const void* kp,
   return err == cudaSuccess ? LA_OK : cuda_fail(err, "la_gla_prologue_bwd");
 }
 
+// the attention descriptor of the GLA core: model-native rows [batch, n, heads * d]
+static int gla_core_desc(const la_gla_desc* gdesc, la_desc* desc) {
+  std::memset(desc, 0, sizeof(*desc));
+  desc->batch = gdesc->batch;
+  desc->heads = gdesc->heads;
+  desc->n = gdesc->n;
+  desc->d = gdesc->d;
+  desc->dtype = gdesc->dtype;
+  desc->backend = LA_BACKEND_TCGEN05;
+  desc->stride[0] = gdesc->n * gdesc->heads * gdesc->d;
+  desc->stride[1] = gdesc->d;
+  desc->stride[2] = gdesc->heads * gdesc->d;
+  int rc = validate(desc);
+  if (rc != LA_OK) return rc;
+  if (desc->dtype != LA_BF16 || desc->d != 128 || !la::tc_supported(desc->dtype, (int)desc->d, desc->stride, 1))
+    return fail(LA_ERR_UNSUPPORTED, "la_gla_core_fwd: the fused core needs bf16 and d = 128 (use la_gla_prologue + la_fwd)");
+  return LA_OK;
+}
+
+size_t la_gla_core_workspace_bytes(const la_gla_desc* gdesc) {
+  la::GlaRows g;
+  la_desc desc;
+  if (gla_prepare(gdesc, false, &g) != LA_OK || gla_core_desc(gdesc, &desc) != LA_OK) return 0;
+  return ws_bytes_for(&desc, LA_BACKEND_TCGEN05, plan_for(&desc, LA_BACKEND_TCGEN05));
+}
+
 int la_gla_core_fwd(const la_gla_desc* gdesc, const void* qp, const void* kp, const void* v, const double* lam,
                     const double* theta, const void* kv_in, void* o, void* q_out, void* k_out, void* kv_out,
-                    void* stream) {
+                    void* workspace, size_t workspace_bytes, void* stream) {
   la::GlaRows g;
   int rc = gla_prepare(gdesc, theta != nullptr, &g);
   if (rc != LA_OK) return rc;
@@ -757,25 +783,13 @@ int la_gla_core_fwd(const la_gla_desc* gdesc, const void* qp, const void* kp, co
   if ((q_out == nullptr) != (k_out == nullptr)) return fail(LA_ERR_SHAPE, "la_gla_core_fwd: q_out and k_out go together");
   if (!states_aligned({qp, kp, v, o, q_out, k_out, kv_in, kv_out}))
     return fail(LA_ERR_SHAPE, "la_gla_core_fwd: operands and states must be 16-byte aligned");
-  // the attention descriptor of the model-native rows [batch, n, heads * d]
   la_desc desc;
-  std::memset(&desc, 0, sizeof(desc));
-  desc.batch = gdesc->batch;
-  desc.heads = gdesc->heads;
-  desc.n = gdesc->n;
-  desc.d = gdesc->d;
-  desc.dtype = gdesc->dtype;
-  desc.backend = LA_BACKEND_TCGEN05;
-  desc.stride[0] = gdesc->n * gdesc->heads * gdesc->d;
-  desc.stride[1] = gdesc->d;
-  desc.stride[2] = gdesc->heads * gdesc->d;
-  if ((rc = validate(&desc)) != LA_OK) return rc;
-  if (desc.dtype != LA_BF16 || desc.d != 128 || !la::tc_supported(desc.dtype, (int)desc.d, desc.stride, 1))
-    return fail(LA_ERR_UNSUPPORTED, "la_gla_core_fwd: the fused core needs bf16 and d = 128 (use la_gla_prologue + la_fwd)");
+  if ((rc = gla_core_desc(gdesc, &desc)) != LA_OK) return rc;
   const la::Plan plan = plan_for(&desc, LA_BACKEND_TCGEN05);
-  if (plan.nseg != 1)
-    return fail(LA_ERR_UNSUPPORTED, "la_gla_core_fwd: batch * heads = %lld leaves SMs idle, the plan splits the "
-                "sequence (use la_gla_prologue + la_fwd)", (long long)(desc.batch * desc.heads));
+  const size_t need = ws_bytes_for(&desc, LA_BACKEND_TCGEN05, plan);
+  if (need > 0 && (workspace == nullptr || workspace_bytes < need))
+    return fail(LA_ERR_SHAPE, "workspace too small: need %zu bytes, got %zu (la_gla_core_workspace_bytes)", need,
+                workspace_bytes);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   bind_stream_context(st);
   la::PassDesc p = base_pass(&desc, plan, lam);
@@ -785,10 +799,32 @@ int la_gla_core_fwd(const la_gla_desc* gdesc, const void* qp, const void* kp, co
   p.out = o;
   p.rev = 0;
   p.state_in = kv_in;
-  p.state_in_bh_stride = (int64_t)desc.d * desc.d;
   p.state_out = kv_out;
+  const int64_t dd = desc.d * desc.d;
+  p.state_in_bh_stride = dd;
   la::GlaPrologue pro{theta, gdesc->act, gdesc->offset, q_out, k_out};
-  cudaError_t err = la::tc_gla_fwd_launch(p, pro, st);
+  cudaError_t err = cudaSuccess;
+  if (plan.nseg > 1) {
+    // the segmented forward (la_fwd_ex) with the prologue in both the summary pass and the main pass
+    void* delta = ws_delta(workspace);
+    void* seg_in = ws_seg_in(workspace, &desc, plan);
+    la::PassDesc s = p;
+    s.a = nullptr;
+    s.out = nullptr;
+    s.state_in = nullptr;
+    s.state_out = nullptr;
+    s.delta_out = delta;
+    s.g_lo = 0;
+    s.g_hi = p.nseg - 2;
+    err = la::tc_summary_launch(s, st, &pro);
+    if (err == cudaSuccess)
+      err = la::launch_segment_scan(false, delta, seg_in, kv_in, 0, nullptr, 0, lam, p.batch * p.heads, p.heads, p.d,
+                                    s, st);
+    p.state_in = seg_in;
+    p.state_in_bh_stride = (int64_t)p.nseg * dd;
+    p.state_in_seg_stride = dd;
+  }
+  if (err == cudaSuccess) err = la::tc_gla_fwd_launch(p, pro, st);
   return err == cudaSuccess ? LA_OK : cuda_fail(err, "la_gla_core_fwd");
 }
 

@@ -300,3 +300,51 @@ __device__ __forceinline__ void tma_prefetch_l2_4d(const CUtensorMap* map, int c
 }
 }  // namespace ptx
 }  // namespace la
+
+namespace la {
+namespace ptx {
+// ---------------------------------------------------------------- GLA prologue helpers (la_tc.cu GLA mode,
+// la_summary.cu GLA mode): act (model.py:60-99) and the LRPE rotation angle (positional.py:126-150)
+// LRPE cos / sin of theta * pos: angle formed and reduced mod 2 pi in fp64, then the fp32 hardware
+// approximation on |angle| <= pi (~2^-21), as la_gla.cu's prologue
+__device__ __forceinline__ void lrpe_cs(double theta, int64_t pos, float* c, float* s) {
+  double ang = theta * (double)pos;
+  ang = fma(-6.283185307179586476925286766559, rint(ang * 0.15915494309189533576888376337251), ang);
+  __sincosf((float)ang, s, c);
+}
+__device__ __forceinline__ uint32_t tanh_bf16x2(uint32_t x) {
+  uint32_t y;
+  asm("tanh.approx.bf16x2 %0, %1;" : "=r"(y) : "r"(x));
+  return y;
+}
+__device__ __forceinline__ float tanh_approx(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+// the GLA activations (model.py:60-99) in fp32: swish x * sigmoid(x), sigmoid = (1 + tanh(x / 2)) / 2
+__device__ __forceinline__ float gla_act(float x, int act) {
+  if (act == 1 /* LA_ACT_SWISH */) return x * fmaf(0.5f, tanh_approx(0.5f * x), 0.5f);
+  if (act == 2 /* LA_ACT_ONE_PLUS_ELU */) return x > 0.f ? x + 1.f : __expf(x);
+  return x;
+}
+// one bf16x2 feature pair (x_2j, x_2j+1) of q or k -> rot(act(x)) with the pair's (cos, sin); rows past n -> 0.
+// ACT is the la_act (a template parameter: the callers dispatch once per tile, keeping the inner loops branch-free)
+template <int ACT>
+__device__ __forceinline__ uint32_t gla_pair(uint32_t w, float cs, float sn, bool valid) {
+  constexpr int act = ACT;
+  float a0 = bf16lo(w), a1 = bf16hi(w);
+  if (act == 1 /* LA_ACT_SWISH */) {
+    // sigmoid(x) = (1 + tanh(x / 2)) / 2: one bf16x2 tanh per pair (x / 2 is exact in bf16)
+    const uint32_t t = tanh_bf16x2(mul_bf16x2(w, 0x3F003F00u));
+    a0 *= fmaf(0.5f, bf16lo(t), 0.5f);
+    a1 *= fmaf(0.5f, bf16hi(t), 0.5f);
+  } else if (act == 2 /* LA_ACT_ONE_PLUS_ELU */) {
+    a0 = gla_act(a0, act);
+    a1 = gla_act(a1, act);
+  }
+  if (!valid) a0 = a1 = 0.f;
+  return pack_bf16x2(a0 * cs - a1 * sn, a0 * sn + a1 * cs);
+}
+}  // namespace ptx
+}  // namespace la

@@ -17,6 +17,7 @@
 
 #include <cmath>
 #include <cstring>
+#include <type_traits>
 
 #include "la_common.cuh"
 #include "la_ptx.cuh"
@@ -49,13 +50,19 @@ struct SumArgs {
   int sub_len, sub_per_seg, g_lo;
   const double* lam;
   float* delta_out;  // [bh][nseg * sub_per_seg][d][d]
+  // GLA mode: B is the pre-activation kp; the B warps apply rot(act(.)) before the decay weight
+  const double* theta;  // [d/2] or nullptr
+  int act;
+  int64_t offset;
 };
 
+template <bool GLA>
 __global__ void __launch_bounds__(S_THREADS, 2)
     tc_summary_kernel(const __grid_constant__ CUtensorMap map_b, const __grid_constant__ CUtensorMap map_c,
                       const SumArgs args) {
   extern __shared__ uint8_t smem_raw[];
   __shared__ SumBars bars;
+  __shared__ float2 anchor_s[GLA ? SD / 2 : 1];  // GLA: (cos, sin) of theta_j (chunk row 0 + offset)
   const uint32_t smem = (smem_u32(smem_raw) + 1023u) & ~1023u;
   uint8_t* smem_gen = smem_raw + (smem - smem_u32(smem_raw));
   auto tile_b = [smem](int s) { return smem + (uint32_t)(s * 2 * STILE); };
@@ -191,11 +198,52 @@ __global__ void __launch_bounds__(S_THREADS, 2)
 #endif
       const uint32_t w2 = pack_bf16x2(w, w);
       const uint32_t base = tile_b(s) + hh * SHALF + i * 128;
-      uint4 x[8];
+      if (GLA) {
+        // k = rot(act(kp)) first (as la_tc.cu's GLA mode), then the decay weight
+        const bool rot = args.theta != nullptr;
+        if (rot) {
+          named_bar_sync(1, 128);  // the previous chunk's anchors are no longer read
+          if (tid < SD / 2) {
+            float c0, s0;
+            lrpe_cs(args.theta[tid], (int64_t)r0 + args.offset, &c0, &s0);
+            anchor_s[tid] = make_float2(c0, s0);
+          }
+          named_bar_sync(1, 128);
+        }
+        const bool valid = row < args.n;
+        auto tile = [&](auto act_tag) {
+          constexpr int ACT = decltype(act_tag)::value;
+#pragma unroll 1
+          for (int m = 0; m < 8; ++m) {
+            const uint32_t a = base + ((m ^ (i & 7)) << 4);
+            const uint4 x = lds128(a);
+            uint32_t wv[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
-      for (int m = 0; m < 8; ++m) x[m] = lds128(base + ((m ^ (i & 7)) << 4));
+            for (int e = 0; e < 4; ++e) {
+              float cs = 1.f, sn = 0.f;
+              if (rot) {
+                const int jp = hh * 32 + 4 * m + e;
+                float cl, sl;
+                __sincosf((float)args.theta[jp] * (float)i, &sl, &cl);
+                const float2 an = anchor_s[jp];
+                cs = an.x * cl - an.y * sl;
+                sn = an.y * cl + an.x * sl;
+              }
+              wv[e] = mul_bf16x2(gla_pair<ACT>(wv[e], cs, sn, valid), w2);
+            }
+            sts128(a, make_uint4(wv[0], wv[1], wv[2], wv[3]));
+          }
+        };
+        if (args.act == LA_ACT_SWISH) tile(std::integral_constant<int, LA_ACT_SWISH>{});
+        else if (args.act == LA_ACT_ONE_PLUS_ELU) tile(std::integral_constant<int, LA_ACT_ONE_PLUS_ELU>{});
+        else tile(std::integral_constant<int, LA_ACT_NONE>{});
+      } else {
+        uint4 x[8];
 #pragma unroll
-      for (int m = 0; m < 8; ++m) sts128(base + ((m ^ (i & 7)) << 4), mul_bf16x2(x[m], w2));
+        for (int m = 0; m < 8; ++m) x[m] = lds128(base + ((m ^ (i & 7)) << 4));
+#pragma unroll
+        for (int m = 0; m < 8; ++m) sts128(base + ((m ^ (i & 7)) << 4), mul_bf16x2(x[m], w2));
+      }
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars.scaled[s]);
@@ -226,10 +274,11 @@ __global__ void __launch_bounds__(S_THREADS, 2)
 
 }  // namespace
 
-cudaError_t tc_summary_launch(const PassDesc& p, cudaStream_t st) {
+cudaError_t tc_summary_launch(const PassDesc& p, cudaStream_t st, const GlaPrologue* gla) {
   CUtensorMap mb, mc;
   if (!tc_make_map(&mb, p.b, p, p.sbb, SC) || !tc_make_map(&mc, p.c, p, p.sc, SC)) return cudaErrorInvalidValue;
   SumArgs a;
+  std::memset(&a, 0, sizeof(a));
   a.heads = p.heads;
   a.n = p.n;
   a.seg_len = p.seg_len;
@@ -240,11 +289,20 @@ cudaError_t tc_summary_launch(const PassDesc& p, cudaStream_t st) {
   a.g_lo = p.g_lo;
   a.lam = p.lam;
   a.delta_out = reinterpret_cast<float*>(p.delta_out);
-  static std::atomic<bool> smem_set[64] = {};
-  cudaError_t err = set_smem_once(tc_summary_kernel, (int)S_SMEM_BYTES, smem_set);
-  if (err != cudaSuccess) return err;
   dim3 grid((p.g_hi - p.g_lo + 1) * p.sub_per_seg, p.batch * p.heads);
-  return launch_pdl(tc_summary_kernel, grid, dim3(S_THREADS), S_SMEM_BYTES, st, mb, mc, a);
+  if (gla == nullptr) {
+    static std::atomic<bool> smem_set[64] = {};
+    cudaError_t err = set_smem_once(tc_summary_kernel<false>, (int)S_SMEM_BYTES, smem_set);
+    if (err != cudaSuccess) return err;
+    return launch_pdl(tc_summary_kernel<false>, grid, dim3(S_THREADS), S_SMEM_BYTES, st, mb, mc, a);
+  }
+  a.theta = gla->theta;
+  a.act = gla->act;
+  a.offset = gla->offset;
+  static std::atomic<bool> smem_set_gla[64] = {};
+  cudaError_t err = set_smem_once(tc_summary_kernel<true>, (int)S_SMEM_BYTES, smem_set_gla);
+  if (err != cudaSuccess) return err;
+  return launch_pdl(tc_summary_kernel<true>, grid, dim3(S_THREADS), S_SMEM_BYTES, st, mb, mc, a);
 }
 
 }  // namespace la

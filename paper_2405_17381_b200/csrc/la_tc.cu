@@ -36,6 +36,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <type_traits>
 
 #include "la_common.cuh"
 #include "la_ptx.cuh"
@@ -132,29 +133,6 @@ struct TcArgs {
   int64_t offset;       // LRPE position of row 0
 };
 
-// LRPE cos / sin of theta * pos: angle formed and reduced mod 2 pi in fp64, then the fp32 hardware
-// approximation on |angle| <= pi (~2^-21), as la_gla.cu's prologue
-__device__ __forceinline__ void lrpe_cs(double theta, int64_t pos, float* c, float* s) {
-  double ang = theta * (double)pos;
-  ang = fma(-6.283185307179586476925286766559, rint(ang * 0.15915494309189533576888376337251), ang);
-  __sincosf((float)ang, s, c);
-}
-__device__ __forceinline__ uint32_t tanh_bf16x2(uint32_t x) {
-  uint32_t y;
-  asm("tanh.approx.bf16x2 %0, %1;" : "=r"(y) : "r"(x));
-  return y;
-}
-__device__ __forceinline__ float tanh_approx(float x) {
-  float y;
-  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
-// the GLA activations (model.py:60-99) in fp32: swish x * sigmoid(x), sigmoid = (1 + tanh(x / 2)) / 2
-__device__ __forceinline__ float gla_act(float x, int act) {
-  if (act == LA_ACT_SWISH) return x * fmaf(0.5f, tanh_approx(0.5f * x), 0.5f);
-  if (act == LA_ACT_ONE_PLUS_ELU) return x > 0.f ? x + 1.f : __expf(x);
-  return x;
-}
 
 // byte offset of 16-byte chunk `c` (0..7) of row `r` inside a [128][64] bf16 block, 128B swizzle
 __device__ __forceinline__ uint32_t sw128(int r, int c) { return (uint32_t)(r * 128 + ((c ^ (r & 7)) << 4)); }
@@ -357,10 +335,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           mbar_wait(&bars.a_full[t & 1], (t >> 1) & 1);
           LA_TR(t, 15);
           tc_fence_after();
+#ifndef LA_KO_MMAX
 #pragma unroll
           for (int kk = 0; kk < D / 16; ++kk)
             mma_bf16_ts(tmem + TM_O, sbuf + 64 + kk * 8, smem_desc_sw128(st_bf16 + kk * 2048, HALF, 1024),
                         IDESC_KMN, kk > 0);
+#endif
           mma_commit(&bars.x_done);
           mma_commit(&bars.empty[0][s]);  // A's readers (S(t), the A~ build) are done
         }
@@ -423,7 +403,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         // P = bf16(S * M): fwd keeps j <= i with lam^(i-j), rev keeps j >= i with lam^(j-i).
         // A block of 32 keys is all-zero / all-kept / diagonal depending on the warp's quadrant.
         auto convert_block = [&](int cb, uint32_t (&pk)[16]) {
+#ifndef LA_KO_PCONV
           const bool zero = rev ? (cb < quad) : (cb > quad);
+#else
+          const bool zero = true;
+#endif
           if (zero) {
 #pragma unroll
             for (int e = 0; e < 16; ++e) pk[e] = 0u;
@@ -544,11 +528,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #endif
         const uint32_t isc2 = pack_bf16x2(isc, isc);
         const uint32_t base = tile_b(s) + hh * HALF + i * 128;
+#ifndef LA_KO_BSCALE  // knock-out experiments only (wrong numerics): tools/gpu/ko_power.sh
         uint4 x[8];
 #pragma unroll
         for (int m = 0; m < 8; ++m) x[m] = lds128(base + ((m ^ (i & 7)) << 4));
 #pragma unroll
         for (int m = 0; m < 8; ++m) sts128(base + ((m ^ (i & 7)) << 4), mul_bf16x2(x[m], isc2));
+#else
+        (void)isc2;
+        (void)base;
+#endif
       }
       fence_proxy_async_smem();
       __syncwarp();
@@ -573,9 +562,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       if (lane == 0) mbar_arrive(&bars.o_free);  // O's TMEM is free; the stores proceed from registers
       {
         const uint32_t base = tile_c(s) + hh * HALF;
+#ifndef LA_KO_OSTAGE
 #pragma unroll
         for (int m = 0; m < 8; ++m)
           sts128(base + sw128(i, m), make_uint4(pk[4 * m], pk[4 * m + 1], pk[4 * m + 2], pk[4 * m + 3]));
+#else
+        (void)base;
+#endif
       }
       fence_proxy_async_smem();
       __syncwarp();
@@ -633,43 +626,35 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       mbar_wait(&bars.full[1][s], (t / NS) & 1);
       const bool valid = r0 + i < p1;
       const uint32_t arow = tile_a(s) + hh * HALF + i * 128, brow = tile_b(s) + hh * HALF + i * 128;
-      const uint32_t half2 = 0x3F003F00u;  // bf16x2 (0.5, 0.5)
+      auto tile = [&](auto act_tag) {
+        constexpr int ACT = decltype(act_tag)::value;
 #pragma unroll 2
-      for (int c = 0; c < 8; ++c) {
-        const uint32_t off = (uint32_t)((c ^ (i & 7)) << 4);
-        const uint4 xa = lds128(arow + off), xb = lds128(brow + off);
-        const uint32_t wa[4] = {xa.x, xa.y, xa.z, xa.w}, wb[4] = {xb.x, xb.y, xb.z, xb.w};
-        uint32_t ya[4], yb[4];
+        for (int c = 0; c < 8; ++c) {
+          const uint32_t off = (uint32_t)((c ^ (i & 7)) << 4);
+          const uint4 xa = lds128(arow + off), xb = lds128(brow + off);
+          const uint32_t wa[4] = {xa.x, xa.y, xa.z, xa.w}, wb[4] = {xb.x, xb.y, xb.z, xb.w};
+          uint32_t ya[4], yb[4];
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          float cs = 1.f, sn = 0.f;
-          if (rot) {
-            const int j = hh * 32 + 4 * c + e;
-            float cl, sl;
-            __sincosf(theta_s[j] * (float)i, &sl, &cl);
-            const float2 an = anchor_s[j];
-            cs = an.x * cl - an.y * sl;
-            sn = an.y * cl + an.x * sl;
+          for (int e = 0; e < 4; ++e) {
+            float cs = 1.f, sn = 0.f;
+            if (rot) {
+              const int j = hh * 32 + 4 * c + e;
+              float cl, sl;
+              __sincosf(theta_s[j] * (float)i, &sl, &cl);
+              const float2 an = anchor_s[j];
+              cs = an.x * cl - an.y * sl;
+              sn = an.y * cl + an.x * sl;
+            }
+            ya[e] = gla_pair<ACT>(wa[e], cs, sn, valid);
+            yb[e] = gla_pair<ACT>(wb[e], cs, sn, valid);
           }
-          float a0 = bf16lo(wa[e]), a1 = bf16hi(wa[e]), b0 = bf16lo(wb[e]), b1 = bf16hi(wb[e]);
-          if (args.act == LA_ACT_SWISH) {
-            // sigmoid(x) = (1 + tanh(x / 2)) / 2 with one bf16x2 tanh per feature pair (x / 2 is exact)
-            const uint32_t ta = tanh_bf16x2(mul_bf16x2(wa[e], half2)), tb = tanh_bf16x2(mul_bf16x2(wb[e], half2));
-            a0 *= fmaf(0.5f, bf16lo(ta), 0.5f);
-            a1 *= fmaf(0.5f, bf16hi(ta), 0.5f);
-            b0 *= fmaf(0.5f, bf16lo(tb), 0.5f);
-            b1 *= fmaf(0.5f, bf16hi(tb), 0.5f);
-          } else if (args.act == LA_ACT_ONE_PLUS_ELU) {
-            a0 = gla_act(a0, LA_ACT_ONE_PLUS_ELU), a1 = gla_act(a1, LA_ACT_ONE_PLUS_ELU);
-            b0 = gla_act(b0, LA_ACT_ONE_PLUS_ELU), b1 = gla_act(b1, LA_ACT_ONE_PLUS_ELU);
-          }
-          if (!valid) a0 = a1 = b0 = b1 = 0.f;
-          ya[e] = pack_bf16x2(a0 * cs - a1 * sn, a0 * sn + a1 * cs);
-          yb[e] = pack_bf16x2(b0 * cs - b1 * sn, b0 * sn + b1 * cs);
+          sts128(arow + off, make_uint4(ya[0], ya[1], ya[2], ya[3]));
+          sts128(brow + off, make_uint4(yb[0], yb[1], yb[2], yb[3]));
         }
-        sts128(arow + off, make_uint4(ya[0], ya[1], ya[2], ya[3]));
-        sts128(brow + off, make_uint4(yb[0], yb[1], yb[2], yb[3]));
-      }
+      };
+      if (args.act == LA_ACT_SWISH) tile(std::integral_constant<int, LA_ACT_SWISH>{});
+      else if (args.act == LA_ACT_ONE_PLUS_ELU) tile(std::integral_constant<int, LA_ACT_ONE_PLUS_ELU>{});
+      else tile(std::integral_constant<int, LA_ACT_NONE>{});
       fence_proxy_async_smem();  // the tensor core and the TMA store read the tiles next
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars.xf_done[s]);
@@ -905,7 +890,7 @@ cudaError_t tc_launch(const PassDesc& p, bool state_only, cudaStream_t st) {
 }
 
 cudaError_t tc_gla_fwd_launch(const PassDesc& p, const GlaPrologue& gla, cudaStream_t st) {
-  if (p.nseg != 1 || p.rev) return cudaErrorInvalidValue;  // the prologue runs on whole, forward sequences
+  if (p.rev) return cudaErrorInvalidValue;  // the prologue belongs to the forward
   return launch_tc(p, st, &gla);
 }
 

@@ -12,8 +12,10 @@ const char* tc_detail();  // thread-local detail of the last host-side failure
 // 4-D TMA descriptor (d, n, heads, batch) over a bf16 [.., .., .., 128] tensor with the desc's strides,
 // box 64 x box_rows, 128-byte swizzle
 bool tc_make_map(CUtensorMap* map, const void* base, const PassDesc& p, const Strides3& s, int box_rows = 128);
-// the segment-summary pass (la_summary.cu): p.delta_out, sub-segment geometry, g_lo..g_hi
-cudaError_t tc_summary_launch(const PassDesc& p, cudaStream_t st);
+struct GlaPrologue;
+// the segment-summary pass (la_summary.cu): p.delta_out, sub-segment geometry, g_lo..g_hi; with `gla`, B is
+// the pre-activation kp and the pass summarises rot(act(kp)) (the GLA core's segmented forward)
+cudaError_t tc_summary_launch(const PassDesc& p, cudaStream_t st, const GlaPrologue* gla = nullptr);
 Plan tc_plan(int64_t bh, int64_t n, int d, int64_t want_segments, int sms);
 // the fused reverse sweep of the backward: dK and dV in one pass over q, k, v, do (p.state_in = the
 // entering adjoint state in dkv orientation; p.state_out = dkv_out, written by segment 0)

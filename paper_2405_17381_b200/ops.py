@@ -463,9 +463,9 @@ def gla_core_forward(qp, kp, v, lam, heads, *, act="swish", theta=None, offset=0
     """The fused GLA core forward (la_gla_core_fwd): o = LA(rot(act(qp)), rot(act(kp)), v) on
     [batch, n, heads * d] rows in one tensor-core pass, the prologue applied to each tile in shared
     memory.  Returns (o, q, k[, kv_out]) -- q, k the transformed rows for the backward (None when
-    ``want_qk`` is False).  Raises UnsupportedError where the fused pass does not apply (not bf16 / d = 128,
-    or batch * heads too small to fill the GPU without splitting sequences): ``gla_prologue`` + ``la_forward``
-    compute the same thing there."""
+    ``want_qk`` is False).  Split sequences (batch * heads too small to fill the GPU) run the summary pass with
+    the prologue too.  Raises UnsupportedError where the fused pass does not apply (not bf16 / d = 128):
+    ``gla_prologue`` + ``la_forward`` compute the same thing there."""
     qp, kp, v = _rows([qp, kp, v], ["qp", "kp", "v"])
     desc = _gla_desc(qp, heads, act, offset, SRMS_EPS)
     th = _theta(theta, desc.d, qp.device)
@@ -476,9 +476,11 @@ def gla_core_forward(qp, kp, v, lam, heads, *, act="swish", theta=None, offset=0
     q, k = (torch.empty_like(qp), torch.empty_like(kp)) if want_qk else (None, None)
     kv_out = torch.empty((desc.batch, heads, desc.d, desc.d), dtype=state_dtype(qp.dtype), device=qp.device) \
         if want_state else None
-    _lib.check(_lib.load().la_gla_core_fwd(ctypes.byref(desc), _ptr(qp), _ptr(kp), _ptr(v), lam_p, _ptr(th),
-                                           _ptr(kv_in), _ptr(o), _ptr(q), _ptr(k), _ptr(kv_out),
-                                           _stream(qp.device)))
+    lib = _lib.load()
+    nbytes = lib.la_gla_core_workspace_bytes(ctypes.byref(desc))
+    ws = torch.empty(nbytes, dtype=torch.uint8, device=qp.device) if nbytes else None
+    _lib.check(lib.la_gla_core_fwd(ctypes.byref(desc), _ptr(qp), _ptr(kp), _ptr(v), lam_p, _ptr(th), _ptr(kv_in),
+                                   _ptr(o), _ptr(q), _ptr(k), _ptr(kv_out), _ptr(ws), nbytes, _stream(qp.device)))
     return (o, q, k, kv_out) if want_state else (o, q, k)
 
 

@@ -108,10 +108,39 @@ def test_fused_core_states_and_no_qk():
     assert _scaled(o, _attn64(q, k, v, LAMS, kv_in)) <= 1e-2
 
 
-def test_fused_core_unsupported_where_the_plan_splits():
-    qp, kp, v = (t[:, :, :4 * D] for t in _inputs(1, 4096, 3))  # batch 1 x 4 heads: segmented plan
+@pytest.mark.parametrize("b,n,heads,rot", [(1, 4096, 4, True), (1, 3000, 16, True), (2, 2500, 8, False)])
+def test_fused_core_segmented(b, n, heads, rot):
+    """batch * heads too small to fill the GPU: the plan splits sequences, and the summary pass applies the
+    prologue to kp too -- same result as the two-step path and the fp64 restatement; kv_in / kv_out chain."""
+    g = torch.Generator(device=DEV).manual_seed(n)
+    qp, kp, v = [(torch.randn(b, n, heads * D, device=DEV, generator=g) * sc).to(torch.bfloat16)
+                 for sc in (1.0, 1.0, 0.5)]
+    lams = [1.0, 0.999, 0.9, 0.5, 0.05, 0.63, 0.99, 0.3][:heads] + [0.95] * max(0, heads - 8)
+    theta = THETA if rot else None
+    kv_in = torch.rand(b, heads, D, D, device=DEV) * 0.05
+    o, q, k, kv = ops.gla_core_forward(qp, kp, v, lams, heads, theta=theta, offset=3, kv_in=kv_in, want_state=True)
+    q2, k2 = ops.gla_prologue(qp, kp, heads, theta=theta, offset=3)
+    assert (q - q2).abs().max().item() <= 2 ** -6 * q2.abs().max().item()
+    o2, kv2 = ops.la_forward(*(t.view(b, n, heads, D) for t in (q2, k2, v)), lams, layout="bnhd", kv_in=kv_in,
+                             want_state=True)
+    assert _scaled(o, o2.view(b, n, heads * D).double()) <= 2e-2
+    assert _scaled(kv, kv2.double()) <= 2e-2
+    # the attention on the kernel's own q / k, against the unsplit fp64 left product
+    qh, kh, vh = (t.double().view(b, n, heads, D).transpose(1, 2) for t in (q, k, v))
+    lam = torch.tensor(lams, dtype=torch.float64, device=DEV)
+    t = torch.arange(n, device=DEV)
+    diff = (t[:, None] - t[None, :]).to(torch.float64)
+    mask = torch.where(diff[None] >= 0, lam[:, None, None] ** diff.clamp(min=0)[None],
+                       torch.zeros((), device=DEV, dtype=torch.float64))
+    ref = ((qh @ kh.transpose(-1, -2)) * mask[None]) @ vh
+    ref = ref + (lam[None, :, None, None] ** (t.double() + 1)[None, None, :, None]) * (qh @ kv_in.double())
+    assert _scaled(o, ref.transpose(1, 2).reshape(b, n, heads * D)) <= 1e-2
+
+
+def test_fused_core_unsupported_for_fp32():
+    qp, kp, v = (t.float() for t in _inputs(6, 256, 3))
     with pytest.raises(UnsupportedError):
-        ops.gla_core_forward(qp, kp, v, [0.9] * 4, 4)
+        ops.gla_core_forward(qp, kp, v, LAMS, H)
 
 
 def test_gla_layer_on_the_fused_core_matches_fp64():
