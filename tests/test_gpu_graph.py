@@ -86,3 +86,46 @@ def test_entry_points_from_two_host_threads():
     for i in range(2):
         for a, w in zip(got[i], want[i]):
             assert torch.equal(a, w)
+
+
+@pytest.mark.parametrize("path", ["fp32_tcgen05", "gla_core"])
+def test_round2_paths_replay_from_a_cuda_graph(path):
+    """The fp32 split pass (segmented: its state-only summaries, the scan, the three backward passes with the
+    side stream) and the fused GLA core forward (segmented: the prologue in the summary pass) replay from a
+    CUDA graph bitwise equal to eager calls, and repeated eager calls are bitwise reproducible."""
+    from paper_2405_17381_b200 import ops
+    dev = torch.device("cuda", 0)
+    torch.manual_seed(2)
+    h, d = 4, 128
+    if path == "fp32_tcgen05":
+        q, k, v, do = (torch.randn(1, h, 3000, d, device=dev) * d ** -0.5 for _ in range(4))
+        lam = ops.decay_tensor([0.99, 0.9, 0.5, 1.0], h, dev)
+
+        def step():
+            o, seg = ops.la_forward(q, k, v, None, lam_dev=lam, want_seg_states=True)
+            return (o,) + tuple(ops.la_backward(q, k, v, do, None, lam_dev=lam, fwd_seg_states=seg))
+    else:
+        qp, kp, vv = (torch.randn(1, 3000, h * d, device=dev).to(torch.bfloat16) for _ in range(3))
+        lam = ops.decay_tensor([0.99, 0.9, 0.5, 1.0], h, dev)
+        theta = torch.tensor([10000.0 ** (-2.0 * j / d) for j in range(d // 2)], dtype=torch.float64, device=dev)
+
+        def step():
+            return ops.gla_core_forward(qp, kp, vv, None, h, theta=theta, lam_dev=lam, offset=7)
+
+    want = [t.clone() for t in step()]
+    again = step()
+    for a, w in zip(again, want):
+        assert torch.equal(a, w)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        step()
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        got = step()
+    g.replay()
+    torch.cuda.synchronize()
+    for a, w in zip(got, want):
+        assert torch.equal(a, w)
