@@ -52,7 +52,7 @@
 extern "C" {
 #endif
 
-#define LA_ABI_VERSION 3
+#define LA_ABI_VERSION 4  /* 4: la_gla_core_fwd / la_gla_core_workspace_bytes; LA_BACKEND_TCGEN05 serves fp32 too */
 
 #if defined(__GNUC__)
 #define LA_API __attribute__((visibility("default")))

@@ -26,7 +26,7 @@ EXPORTS = ("la_workspace_bytes", "la_segment_count", "la_fwd", "la_bwd", "la_fwd
            "la_fwd_state", "la_bwd_state",
            "la_decode", "la_gla_workspace_bytes", "la_gla_prologue", "la_gla_prologue_bwd", "la_gla_epilogue",
            "la_gla_epilogue_bwd", "la_gla_core_fwd", "la_gla_core_workspace_bytes", "la_gla_gate_rowsq", "la_gla_rowscale", "la_launch_count", "la_last_error", "la_abi_version", "la_build_info")
-ABI_VERSION = 3
+ABI_VERSION = 4
 # la_fwd_ex / la_bwd_ex flags
 LA_FLAG_RESUME, LA_FLAG_CHECK_DECAY, LA_FLAG_CHECK_FINITE, LA_FLAG_NO_DQ, LA_FLAG_NO_DKDV = 0x1, 0x2, 0x4, 0x8, 0x10
 # la_operand

@@ -27,7 +27,7 @@ def test_library_exports_every_declared_symbol():
     lib = _lib.load()
     for name in _declared():
         assert hasattr(lib, name), name
-    assert lib.la_abi_version() == _lib.ABI_VERSION == 3
+    assert lib.la_abi_version() == _lib.ABI_VERSION == 4
     assert b"sm_100a" in lib.la_build_info()
 
 
