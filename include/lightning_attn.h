@@ -52,7 +52,7 @@
 extern "C" {
 #endif
 
-#define LA_ABI_VERSION 4  /* 4: la_gla_core_fwd / la_gla_core_workspace_bytes; LA_BACKEND_TCGEN05 serves fp32 too */
+#define LA_ABI_VERSION 4  /* 4: la_gla_core_fwd / la_gla_core_bwd (+ their workspace sizes); LA_BACKEND_TCGEN05 serves fp32 too */
 
 #if defined(__GNUC__)
 #define LA_API __attribute__((visibility("default")))
@@ -235,6 +235,17 @@ LA_API size_t la_gla_core_workspace_bytes(const la_gla_desc* desc);
 LA_API int la_gla_core_fwd(const la_gla_desc* desc, const void* qp, const void* kp, const void* v,
                     const double* lam, const double* theta, const void* kv_in, void* o, void* q_out,
                     void* k_out, void* kv_out, void* workspace, size_t workspace_bytes, void* stream);
+/* Fused GLA core backward: the core's backward (la_bwd on the forward's q = rot(act(qp)), k = rot(act(kp)),
+ * v and da = the gradient at the core's output) with the prologue's backward (model.py:434-446: dqp =
+ * act'(qp) * R^T dq, dkp likewise) applied to the dq / dK tiles in shared memory before they are stored
+ * -- dq and dk never reach HBM (4 rows fewer; measured 0.73-0.93x of la_bwd + la_gla_prologue_bwd on B200,
+ * DESIGN.md K7).  No LRPE angle gradient: when theta is learned, use la_bwd + la_gla_prologue_bwd.  bf16,
+ * d = 128 (LA_ERR_UNSUPPORTED otherwise); workspace: la_gla_core_bwd_workspace_bytes. */
+LA_API size_t la_gla_core_bwd_workspace_bytes(const la_gla_desc* desc);
+LA_API int la_gla_core_bwd(const la_gla_desc* desc, const void* qp, const void* kp, const void* q, const void* k,
+                    const void* v, const void* da, const double* lam, const double* theta, const void* kv_in,
+                    const void* dkv_in, void* dqp, void* dkp, void* dv, void* dkv_out, void* workspace,
+                    size_t workspace_bytes, void* stream);
 LA_API int la_gla_epilogue(const la_gla_desc* desc, const void* a, const void* u, void* gated,
                     void* rawnorm, void* stream);
 LA_API int la_gla_epilogue_bwd(const la_gla_desc* desc, const void* dgated, const void* a, const void* u,

@@ -25,7 +25,8 @@ BACKENDS = {"auto": LA_BACKEND_AUTO, "simt": LA_BACKEND_SIMT, "tcgen05": LA_BACK
 EXPORTS = ("la_workspace_bytes", "la_segment_count", "la_fwd", "la_bwd", "la_fwd_ex", "la_bwd_ex", "la_check_decay",
            "la_fwd_state", "la_bwd_state",
            "la_decode", "la_gla_workspace_bytes", "la_gla_prologue", "la_gla_prologue_bwd", "la_gla_epilogue",
-           "la_gla_epilogue_bwd", "la_gla_core_fwd", "la_gla_core_workspace_bytes", "la_gla_gate_rowsq", "la_gla_rowscale", "la_launch_count", "la_last_error", "la_abi_version", "la_build_info")
+           "la_gla_epilogue_bwd", "la_gla_core_fwd", "la_gla_core_workspace_bytes",
+           "la_gla_core_bwd", "la_gla_core_bwd_workspace_bytes", "la_gla_gate_rowsq", "la_gla_rowscale", "la_launch_count", "la_last_error", "la_abi_version", "la_build_info")
 ABI_VERSION = 4
 # la_fwd_ex / la_bwd_ex flags
 LA_FLAG_RESUME, LA_FLAG_CHECK_DECAY, LA_FLAG_CHECK_FINITE, LA_FLAG_NO_DQ, LA_FLAG_NO_DKDV = 0x1, 0x2, 0x4, 0x8, 0x10
@@ -138,11 +139,21 @@ def load() -> ctypes.CDLL:
     lib.la_gla_epilogue.restype = c_int
     lib.la_gla_epilogue_bwd.argtypes = [G, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]
     lib.la_gla_epilogue_bwd.restype = c_int
-    lib.la_gla_core_fwd.argtypes = [G, c_void_p, c_void_p, c_void_p, POINTER(c_double), c_void_p, c_void_p,
-                                    c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]
-    lib.la_gla_core_workspace_bytes.argtypes = [G]
-    lib.la_gla_core_workspace_bytes.restype = c_size_t
-    lib.la_gla_core_fwd.restype = c_int
+    # the fused GLA core entry points (ABI 4) are bound when present, so A/B experiments can load an older build;
+    # calling one that is missing raises AttributeError (build() checks every export of the shipped library)
+    if hasattr(lib, "la_gla_core_fwd"):
+        lib.la_gla_core_fwd.argtypes = [G, c_void_p, c_void_p, c_void_p, POINTER(c_double), c_void_p, c_void_p,
+                                        c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]
+        lib.la_gla_core_fwd.restype = c_int
+        lib.la_gla_core_workspace_bytes.argtypes = [G]
+        lib.la_gla_core_workspace_bytes.restype = c_size_t
+    if hasattr(lib, "la_gla_core_bwd"):
+        lib.la_gla_core_bwd.argtypes = [G, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                        POINTER(c_double), c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                        c_void_p, c_void_p, c_size_t, c_void_p]
+        lib.la_gla_core_bwd.restype = c_int
+        lib.la_gla_core_bwd_workspace_bytes.argtypes = [G]
+        lib.la_gla_core_bwd_workspace_bytes.restype = c_size_t
     lib.la_gla_gate_rowsq.argtypes = [G, c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_void_p]
     lib.la_gla_gate_rowsq.restype = c_int
     lib.la_gla_rowscale.argtypes = [c_int, c_int64, c_int64, c_double, c_void_p, c_void_p, c_void_p]

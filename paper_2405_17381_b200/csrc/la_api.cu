@@ -206,7 +206,8 @@ cudaError_t segment_states(int backend, int dtype, const la::PassDesc& p, void* 
 
 // The main pass.  With one segment the caller's edge state is used as is; with several, the entering
 // states `seg_in` (orientation seg_T) must already be computed.
-cudaError_t main_pass(int backend, int dtype, la::PassDesc p, const void* seg_in, int seg_T, cudaStream_t st) {
+cudaError_t main_pass(int backend, int dtype, la::PassDesc p, const void* seg_in, int seg_T, cudaStream_t st,
+                      const la::GlaEpilogue* epi = nullptr) {
   const int64_t dd = (int64_t)p.d * p.d;
   if (p.nseg > 1) {
     p.state_in = seg_in;
@@ -217,6 +218,7 @@ cudaError_t main_pass(int backend, int dtype, la::PassDesc p, const void* seg_in
     p.state_in_bh_stride = dd;
     p.state_in_seg_stride = 0;
   }
+  if (epi != nullptr) return la::tc_epi_launch(p, *epi, st);  // the fused GLA core backward's dq pass
   return launch(backend, dtype, p, false, st);
 }
 
@@ -374,7 +376,8 @@ int check_finite(const la_desc* desc, std::initializer_list<std::pair<const void
 // The fused dK/dV sweep (la_tc_bwd.cu): q, k, v, do read once, one state update.  seg_in: the
 // adjoint state entering every segment (split sequences), else the caller's dkv_in.
 int dkdv(const la::PassDesc& base, const OpStrides& os, const void* q, const void* k, const void* v, const void* dout,
-         void* dk, void* dv, const void* dkv_in, void* dkv_out, const void* seg_in, cudaStream_t st) {
+         void* dk, void* dv, const void* dkv_in, void* dkv_out, const void* seg_in, cudaStream_t st,
+         const la::GlaEpilogue* epi = nullptr) {
   la::PassDesc p = base;
   p.rev = 1;
   p.b = q;
@@ -395,7 +398,7 @@ int dkdv(const la::PassDesc& base, const OpStrides& os, const void* q, const voi
   if (!la::tc_pointers_ok(p) || (reinterpret_cast<uintptr_t>(v) & 15) || (reinterpret_cast<uintptr_t>(dk) & 15))
     return cuda_fail(cudaErrorMisalignedAddress, "la_bwd dkdv");
   const la::Strides3 s6[6] = {os.s[LA_T_Q], os.s[LA_T_K], os.s[LA_T_V], os.s[LA_T_DO], os.s[LA_T_DK], os.s[LA_T_DV]};
-  cudaError_t err = la::tc_dkdv_launch(p, q, k, v, dout, dk, dv, s6, st);
+  cudaError_t err = la::tc_dkdv_launch(p, q, k, v, dout, dk, dv, s6, st, epi);
   if (err != cudaSuccess) return cuda_fail(err, "la_bwd dkdv");
   return LA_OK;
 }
@@ -487,10 +490,11 @@ int la_fwd(const la_desc* desc, const void* q, const void* k, const void* v, con
                    stream);
 }
 
-int la_bwd_ex(const la_desc* desc, const la_tensor_strides* strides, uint32_t flags, const void* q, const void* k,
-              const void* v, const void* dout, const double* lam, const void* kv_in, const void* dkv_in,
-              const void* fwd_seg_states, void* dq, void* dk, void* dv, void* dkv_out, void* workspace,
-              size_t workspace_bytes, void* stream) {
+// the backward; epi_q / epi_k (the fused GLA core backward, bf16 tcgen05 only): dq -> dqp, dk -> dkp
+static int bwd_impl(const la_desc* desc, const la_tensor_strides* strides, uint32_t flags, const void* q, const void* k,
+                    const void* v, const void* dout, const double* lam, const void* kv_in, const void* dkv_in,
+                    const void* fwd_seg_states, void* dq, void* dk, void* dv, void* dkv_out, void* workspace,
+                    size_t workspace_bytes, void* stream, const la::GlaEpilogue* epi_q, const la::GlaEpilogue* epi_k) {
   if (flags & ~kKnownFlags) return fail(LA_ERR_DOMAIN, "la_bwd_ex: unknown flags 0x%x", flags);
   if (desc == nullptr) return fail(LA_ERR_SHAPE, "null descriptor");
   const bool want_dq = !(flags & LA_FLAG_NO_DQ), want_dkdv = !(flags & LA_FLAG_NO_DKDV);
@@ -539,9 +543,9 @@ int la_bwd_ex(const la_desc* desc, const la_tensor_strides* strides, uint32_t fl
   p.state_in = kv_in;
   p.state_in_T = 1;
   auto run_dq = [&](cudaStream_t s) -> cudaError_t {
-    if (split && fwd_seg_states != nullptr) return main_pass(pr.backend, desc->dtype, p, fwd_seg_states, 1, s);
+    if (split && fwd_seg_states != nullptr) return main_pass(pr.backend, desc->dtype, p, fwd_seg_states, 1, s, epi_q);
     cudaError_t e = split ? segment_states(pr.backend, desc->dtype, p, delta, seg_in, s) : cudaSuccess;
-    return e == cudaSuccess ? main_pass(pr.backend, desc->dtype, p, seg_in, 0, s) : e;
+    return e == cudaSuccess ? main_pass(pr.backend, desc->dtype, p, seg_in, 0, s, epi_q) : e;
   };
   // sweep 2 (kernels.py:320-333): dk = rev(v, do, q) carries dkv^T, dv = rev(k, q, do) carries dkv --
   // one set of segment states (over q, do) serves both passes
@@ -558,7 +562,7 @@ int la_bwd_ex(const la_desc* desc, const la_tensor_strides* strides, uint32_t fl
         (err = segment_states(pr.backend, desc->dtype, pd, delta, seg_in, s, resume)) != cudaSuccess)
       return cuda_fail(err, "la_bwd dkv states");
     if (fused)
-      return dkdv(base, os, q, k, v, dout, dk, dv, dkv_in, dkv_out, split ? seg_in : nullptr, s);
+      return dkdv(base, os, q, k, v, dout, dk, dv, dkv_in, dkv_out, split ? seg_in : nullptr, s, epi_k);
     la::PassDesc r = base;
     r.a = v;
     r.b = dout;
@@ -618,6 +622,14 @@ int la_bwd_ex(const la_desc* desc, const la_tensor_strides* strides, uint32_t fl
   }
   if ((err = run_dq(st)) != cudaSuccess) return cuda_fail(err, "la_bwd dq");
   return run_dkdv(st, false);
+}
+
+int la_bwd_ex(const la_desc* desc, const la_tensor_strides* strides, uint32_t flags, const void* q, const void* k,
+              const void* v, const void* dout, const double* lam, const void* kv_in, const void* dkv_in,
+              const void* fwd_seg_states, void* dq, void* dk, void* dv, void* dkv_out, void* workspace,
+              size_t workspace_bytes, void* stream) {
+  return bwd_impl(desc, strides, flags, q, k, v, dout, lam, kv_in, dkv_in, fwd_seg_states, dq, dk, dv, dkv_out,
+                  workspace, workspace_bytes, stream, nullptr, nullptr);
 }
 
 int la_bwd(const la_desc* desc, const void* q, const void* k, const void* v, const void* dout, const double* lam,
@@ -826,6 +838,32 @@ int la_gla_core_fwd(const la_gla_desc* gdesc, const void* qp, const void* kp, co
   }
   if (err == cudaSuccess) err = la::tc_gla_fwd_launch(p, pro, st);
   return err == cudaSuccess ? LA_OK : cuda_fail(err, "la_gla_core_fwd");
+}
+
+int la_gla_core_bwd(const la_gla_desc* gdesc, const void* qp, const void* kp, const void* q, const void* k,
+                    const void* v, const void* da, const double* lam, const double* theta, const void* kv_in,
+                    const void* dkv_in, void* dqp, void* dkp, void* dv, void* dkv_out, void* workspace,
+                    size_t workspace_bytes, void* stream) {
+  la::GlaRows g;
+  int rc = gla_prepare(gdesc, theta != nullptr, &g);
+  if (rc != LA_OK) return rc;
+  if (!qp || !kp || !q || !k || !v || !da || !lam || !dqp || !dkp || !dv)
+    return fail(LA_ERR_SHAPE, "la_gla_core_bwd: null operand");
+  if (!states_aligned({qp, kp})) return fail(LA_ERR_SHAPE, "la_gla_core_bwd: operands must be 16-byte aligned");
+  la_desc desc;
+  if ((rc = gla_core_desc(gdesc, &desc)) != LA_OK) return rc;
+  const la::Strides3 rows{desc.stride[0], desc.stride[1], desc.stride[2]};
+  const la::GlaEpilogue epi_q{qp, rows, theta, gdesc->act, gdesc->offset};
+  const la::GlaEpilogue epi_k{kp, rows, theta, gdesc->act, gdesc->offset};
+  return bwd_impl(&desc, nullptr, 0, q, k, v, da, lam, kv_in, dkv_in, nullptr, dqp, dkp, dv, dkv_out, workspace,
+                  workspace_bytes, stream, &epi_q, &epi_k);
+}
+
+size_t la_gla_core_bwd_workspace_bytes(const la_gla_desc* gdesc) {
+  la::GlaRows g;
+  la_desc desc;
+  if (gla_prepare(gdesc, false, &g) != LA_OK || gla_core_desc(gdesc, &desc) != LA_OK) return 0;
+  return la_workspace_bytes(&desc);
 }
 
 int la_gla_epilogue(const la_gla_desc* desc, const void* a, const void* u, void* gated, void* rawnorm, void* stream) {

@@ -346,5 +346,23 @@ __device__ __forceinline__ uint32_t gla_pair(uint32_t w, float cs, float sn, boo
   if (!valid) a0 = a1 = 0.f;
   return pack_bf16x2(a0 * cs - a1 * sn, a0 * sn + a1 * cs);
 }
+// the GLA prologue's backward on one bf16x2 pair (model.py:434-441, positional.py:153-176): dx = act'(x) * R^T dy,
+// x the pre-activation pair, dy the gradient w.r.t. the rotated activation, (cs, sn) the pair's rotation;
+// R^T dy = (dy1 c + dy2 s, -dy1 s + dy2 c).  fp32 sigmoid (tanh.approx.f32) for the derivative
+template <int ACT>
+__device__ __forceinline__ uint32_t gla_pair_bwd(uint32_t x, uint32_t dy, float cs, float sn) {
+  const float d0 = bf16lo(dy), d1 = bf16hi(dy);
+  float g0 = d0 * cs + d1 * sn, g1 = d1 * cs - d0 * sn;
+  const float x0 = bf16lo(x), x1 = bf16hi(x);
+  if (ACT == 1 /* LA_ACT_SWISH */) {  // swish'(x) = s (1 + x (1 - s)), s = sigmoid(x)
+    const float s0 = fmaf(0.5f, tanh_approx(0.5f * x0), 0.5f), s1 = fmaf(0.5f, tanh_approx(0.5f * x1), 0.5f);
+    g0 *= s0 * fmaf(x0, 1.f - s0, 1.f);
+    g1 *= s1 * fmaf(x1, 1.f - s1, 1.f);
+  } else if (ACT == 2 /* LA_ACT_ONE_PLUS_ELU */) {
+    g0 *= x0 > 0.f ? 1.f : __expf(x0);
+    g1 *= x1 > 0.f ? 1.f : __expf(x1);
+  }
+  return pack_bf16x2(g0, g1);
+}
 }  // namespace ptx
 }  // namespace la

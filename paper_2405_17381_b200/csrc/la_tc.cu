@@ -96,6 +96,7 @@ constexpr int NSTAGE_MAX = NSTAGE;
 struct Bars {
   uint64_t xf_done[NSTAGE_MAX];   // GLA: A / B tiles of the stage transformed in place -> MMA (S), qk store lane
   uint64_t qk_stored[NSTAGE_MAX]; // GLA: the store lane has read the transformed tiles -> B warps (B~ in place)
+  uint64_t out_ready[NSTAGE_MAX]; // EPI: the staged output tile transformed in place -> store lane
   uint64_t full[3][NSTAGE_MAX];   // TMA -> consumers, one ring per operand tile A, B, C (tx bytes)
   uint64_t empty[3][NSTAGE_MAX];  // MMA commit after the tile's last reader -> TMA
   uint64_t s_full[2];      // MMA: S[t%2] done                 -> P warps, state warps
@@ -131,6 +132,9 @@ struct TcArgs {
   int act;              // la_act
   int qk_out;           // store the transformed q / k tiles (map_qo / map_ko)
   int64_t offset;       // LRPE position of row 0
+  // EPI mode: the pre-activation rows x (bf16, the output's geometry, strides sx)
+  const uint16_t* xp;
+  Strides3 sx;
 };
 
 
@@ -138,7 +142,10 @@ struct TcArgs {
 __device__ __forceinline__ uint32_t sw128(int r, int c) { return (uint32_t)(r * 128 + ((c ^ (r & 7)) << 4)); }
 
 
-template <bool GLA>
+// MODE 0: the plain pass.  1 (GLA): the GLA prologue on the A / B tiles (the fused GLA core forward).
+// 2 (EPI): the GLA prologue's backward on the output tile, out = act'(x) * R^T pass(a, b, c) with x the
+// pre-activation rows args.xp -- the dq pass of the fused GLA core backward, writing dqp instead of dq.
+template <int MODE>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     tc_pass_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                    const __grid_constant__ CUtensorMap map_c, const __grid_constant__ CUtensorMap map_o,
@@ -146,8 +153,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                    const TcArgs args) {
   extern __shared__ uint8_t smem_raw[];
   __shared__ Bars bars;
-  __shared__ float theta_s[GLA ? D / 2 : 1];           // LRPE angles (fp32: local angles theta_j * i, i < 128)
-  __shared__ float2 anchor_s[GLA ? D / 2 : 1];         // (cos, sin) of theta_j * (chunk row 0 + offset), fp64-reduced
+  constexpr bool GLA = MODE == 1, EPI = MODE == 2;
+  __shared__ float theta_s[GLA || EPI ? D / 2 : 1];     // LRPE angles (fp32: local angles theta_j * i, i < 128)
+  __shared__ float2 anchor_s[GLA || EPI ? D / 2 : 1];   // (cos, sin) of theta_j * (chunk row 0 + offset), fp64-reduced
   __shared__ __align__(16) float pw[C + 8];  // lam^0 .. lam^128
   const uint32_t smem = (smem_u32(smem_raw) + 1023u) & ~1023u;
   uint8_t* smem_gen = smem_raw + (smem - smem_u32(smem_raw));
@@ -182,6 +190,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       mbar_init(&bars.b_scaled[s], NUM_KV);
       mbar_init(&bars.xf_done[s], NUM_KV);
       mbar_init(&bars.qk_stored[s], 1);
+      mbar_init(&bars.out_ready[s], NUM_KV);
     }
     for (int s = 0; s < NSTAGE; ++s) {
       mbar_init(&bars.s_full[s], 1);
@@ -205,7 +214,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const double l = load_decay(args.lam, hi);
     pw[threadIdx.x] = (float)(pow_int(l, (int)threadIdx.x) * (l / l));
   }
-  if (GLA && args.theta != nullptr && threadIdx.x >= 160 && threadIdx.x < 160 + D / 2)
+  if ((GLA || EPI) && args.theta != nullptr && threadIdx.x >= 160 && threadIdx.x < 160 + D / 2)
     theta_s[threadIdx.x - 160] = (float)args.theta[threadIdx.x - 160];
   if (warp == WARP_TMA && lane == 0) {
     tma_prefetch(&map_a);
@@ -255,7 +264,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       // and hand the slot back to the C ring once the store has read it
       for (int t = 0; t < nchunks; ++t) {
         const int s = t % NSTAGE;
-        mbar_wait(&bars.o_staged[s], (t / NSTAGE) & 1);
+        mbar_wait(EPI ? &bars.out_ready[s] : &bars.o_staged[s], (t / NSTAGE) & 1);
         uint8_t* g = smem_gen + (s * 3 + 2) * TILE;
         const int r0 = chunk_row0(t);
         tma_store_4d(&map_o, g, 0, r0, hi, bi);
@@ -659,7 +668,71 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars.xf_done[s]);
     };
+    // EPI: out(t) = act'(x) * R^T out(t) on the tile the output warps staged in C's slot, in place; row i,
+    // this warp's 64 columns (pairs j = 32 hh + 4 c + e); x loaded straight from global (one 128-byte row
+    // segment per thread)
+    uint4 xr[8];  // EPI: x row segment of the chunk to transform next, loaded a chunk ahead of its use
+    auto load_x = [&](int t) {
+      const int r0 = chunk_row0(t);
+      if (r0 + i < p1) {
+        const uint4* src = reinterpret_cast<const uint4*>(args.xp + (int64_t)bi * args.sx.b + (int64_t)hi * args.sx.h +
+                                                          (int64_t)(r0 + i) * args.sx.n + hh * 64);
+#pragma unroll
+        for (int c = 0; c < 8; ++c) xr[c] = __ldg(src + c);
+      } else {
+#pragma unroll
+        for (int c = 0; c < 8; ++c) xr[c] = make_uint4(0, 0, 0, 0);
+      }
+    };
+    auto transform_out = [&](int t) {
+      const int s = t % NS;
+      const int r0 = chunk_row0(t);
+      const bool rot = args.theta != nullptr;
+      if (rot) {
+        named_bar_sync(1, NUM_KV * 32);
+        if (warp == WARP_KV + 4 || warp == WARP_KV + 5) {
+          const int j = (warp - WARP_KV - 4) * 32 + lane;
+          float c0, s0;
+          lrpe_cs(args.theta[j], (int64_t)r0 + args.offset, &c0, &s0);
+          anchor_s[j] = make_float2(c0, s0);
+        }
+        named_bar_sync(1, NUM_KV * 32);
+      }
+      mbar_wait(&bars.o_staged[s], (t / NS) & 1);
+      const uint32_t row = tile_c(s) + hh * HALF;
+      auto tile = [&](auto act_tag) {
+        constexpr int ACT = decltype(act_tag)::value;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {  // fully unrolled: xr stays in registers
+          const uint32_t a = row + sw128(i, c);
+          const uint4 dy = lds128(a);
+          const uint32_t dw[4] = {dy.x, dy.y, dy.z, dy.w}, xw[4] = {xr[c].x, xr[c].y, xr[c].z, xr[c].w};
+          uint32_t o[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            float cs = 1.f, sn = 0.f;
+            if (rot) {
+              const int j = hh * 32 + 4 * c + e;
+              float cl, sl;
+              __sincosf(theta_s[j] * (float)i, &sl, &cl);
+              const float2 an = anchor_s[j];
+              cs = an.x * cl - an.y * sl;
+              sn = an.y * cl + an.x * sl;
+            }
+            o[e] = gla_pair_bwd<ACT>(xw[e], dw[e], cs, sn);
+          }
+          sts128(a, make_uint4(o[0], o[1], o[2], o[3]));
+        }
+      };
+      if (args.act == LA_ACT_SWISH) tile(std::integral_constant<int, LA_ACT_SWISH>{});
+      else if (args.act == LA_ACT_ONE_PLUS_ELU) tile(std::integral_constant<int, LA_ACT_ONE_PLUS_ELU>{});
+      else tile(std::integral_constant<int, LA_ACT_NONE>{});
+      fence_proxy_async_smem();  // the TMA store reads the tile next
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars.out_ready[s]);
+    };
     if (GLA && nchunks > 0) transform(0);
+    if (EPI && nchunks > 0) load_x(0);
     if (nchunks > 0) {
       const float d0 = pw[chunk_len(0)];
 #pragma unroll 1
@@ -707,6 +780,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         signal_ready();
       }
       if (warp == WARP_KV && lane == 0) LA_TR(t, 14);
+      if (EPI) {
+        transform_out(t);
+        if (t + 1 < nchunks) load_x(t + 1);  // in flight while the next chunk's products run
+      }
     }
     if (nchunks > 0 && args.state_out != nullptr && (rev ? seg == 0 : seg == args.nseg - 1)) {
       // the pass's final state F(n) / R(0): kv_out / dkv_out
@@ -785,7 +862,8 @@ bool tc_make_map(CUtensorMap* map, const void* base, const PassDesc& p, const St
 namespace {
 
 // gla: nullptr for the plain pass; else the GLA-mode prologue parameters and the q / k out maps
-cudaError_t launch_tc(const PassDesc& p, cudaStream_t st, const GlaPrologue* gla = nullptr) {
+cudaError_t launch_tc(const PassDesc& p, cudaStream_t st, const GlaPrologue* gla = nullptr,
+                      const GlaEpilogue* epi = nullptr) {
   CUtensorMap ma, mb, mc, mo, mqo, mko;
   std::memset(&ma, 0, sizeof(ma));
   std::memset(&mo, 0, sizeof(mo));
@@ -810,11 +888,22 @@ cudaError_t launch_tc(const PassDesc& p, cudaStream_t st, const GlaPrologue* gla
   a.out_T = p.state_out_T;
   const size_t smem_bytes = SMEM_BYTES;
   dim3 grid(p.nseg, p.batch * p.heads);
+  if (epi != nullptr) {
+    a.theta = epi->theta;
+    a.act = epi->act;
+    a.offset = epi->offset;
+    a.xp = reinterpret_cast<const uint16_t*>(epi->xp);
+    a.sx = epi->sx;
+    static std::atomic<bool> smem_set_epi[64] = {};
+    cudaError_t err = set_smem_once(tc_pass_kernel<2>, (int)smem_bytes, smem_set_epi);
+    if (err != cudaSuccess) return err;
+    return launch_pdl(tc_pass_kernel<2>, grid, dim3(NUM_THREADS), smem_bytes, st, ma, mb, mc, mo, mqo, mko, a);
+  }
   if (gla == nullptr) {
     static std::atomic<bool> smem_set[64] = {};
-    cudaError_t err = set_smem_once(tc_pass_kernel<false>, (int)smem_bytes, smem_set);
+    cudaError_t err = set_smem_once(tc_pass_kernel<0>, (int)smem_bytes, smem_set);
     if (err != cudaSuccess) return err;
-    return launch_pdl(tc_pass_kernel<false>, grid, dim3(NUM_THREADS), smem_bytes, st, ma, mb, mc, mo, mqo, mko, a);
+    return launch_pdl(tc_pass_kernel<0>, grid, dim3(NUM_THREADS), smem_bytes, st, ma, mb, mc, mo, mqo, mko, a);
   }
   a.theta = gla->theta;
   a.act = gla->act;
@@ -823,9 +912,9 @@ cudaError_t launch_tc(const PassDesc& p, cudaStream_t st, const GlaPrologue* gla
   if (a.qk_out && (!tc_make_map(&mqo, gla->q_out, p, p.sa) || !tc_make_map(&mko, gla->k_out, p, p.sbb)))
     return cudaErrorInvalidValue;
   static std::atomic<bool> smem_set_gla[64] = {};
-  cudaError_t err = set_smem_once(tc_pass_kernel<true>, (int)smem_bytes, smem_set_gla);
+  cudaError_t err = set_smem_once(tc_pass_kernel<1>, (int)smem_bytes, smem_set_gla);
   if (err != cudaSuccess) return err;
-  return launch_pdl(tc_pass_kernel<true>, grid, dim3(NUM_THREADS), smem_bytes, st, ma, mb, mc, mo, mqo, mko, a);
+  return launch_pdl(tc_pass_kernel<1>, grid, dim3(NUM_THREADS), smem_bytes, st, ma, mb, mc, mo, mqo, mko, a);
 }
 
 bool aligned16(const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15) == 0; }
@@ -887,6 +976,11 @@ Plan tc_plan(int64_t bh, int64_t n, int d, int64_t want_segments, int sms) {
 cudaError_t tc_launch(const PassDesc& p, bool state_only, cudaStream_t st) {
   // summaries: the lean two-CTAs-per-SM kernel of la_summary.cu
   return state_only ? tc_summary_launch(p, st) : launch_tc(p, st);
+}
+
+cudaError_t tc_epi_launch(const PassDesc& p, const GlaEpilogue& epi, cudaStream_t st) {
+  if (!tc_pointers_ok(p) || (reinterpret_cast<uintptr_t>(epi.xp) & 15)) return cudaErrorMisalignedAddress;
+  return launch_tc(p, st, nullptr, &epi);
 }
 
 cudaError_t tc_gla_fwd_launch(const PassDesc& p, const GlaPrologue& gla, cudaStream_t st) {

@@ -20,8 +20,9 @@ Plan tc_plan(int64_t bh, int64_t n, int d, int64_t want_segments, int sms);
 // the fused reverse sweep of the backward: dK and dV in one pass over q, k, v, do (p.state_in = the
 // entering adjoint state in dkv orientation; p.state_out = dkv_out, written by segment 0)
 // s[6]: strides of q, k, v, do, dk, dv
+struct GlaEpilogue;
 cudaError_t tc_dkdv_launch(const PassDesc& p, const void* q, const void* k, const void* v, const void* dout,
-                           void* dk, void* dv, const Strides3* s, cudaStream_t st);
+                           void* dk, void* dv, const Strides3* s, cudaStream_t st, const GlaEpilogue* epi = nullptr);
 // one launch of the main pass kernel (state_only = false) or of the per-segment summary kernel
 cudaError_t tc_launch(const PassDesc& p, bool state_only, cudaStream_t st);
 // GLA core forward (la_tc.cu GLA mode): the pass on (rot(act(a)), rot(act(b)), c) with the prologue
@@ -34,6 +35,16 @@ struct GlaPrologue {
   void* k_out;
 };
 cudaError_t tc_gla_fwd_launch(const PassDesc& p, const GlaPrologue& gla, cudaStream_t st);
+// GLA core backward: the prologue's backward applied to a pass's output tile (dq -> dqp) or the dK/dV sweep's
+// dK tile (dk -> dkp), with x the pre-activation rows (qp / kp: the output's geometry, strides sx)
+struct GlaEpilogue {
+  const void* xp;
+  Strides3 sx;
+  const double* theta;  // [d/2] or nullptr
+  int act;
+  int64_t offset;
+};
+cudaError_t tc_epi_launch(const PassDesc& p, const GlaEpilogue& epi, cudaStream_t st);
 // the fp32 pass (la_tc32.cu): three-term bf16 split on tcgen05, d = 128, 16-byte strides
 bool tc32_supported(int dtype, int d, const int64_t* strides, int count);
 Plan tc32_plan(int64_t bh, int64_t n, int64_t want_segments, int sms);

@@ -23,6 +23,7 @@
 #include <cudaTypedefs.h>
 
 #include <cstring>
+#include <type_traits>
 
 #include "la_common.cuh"
 #include "la_ptx.cuh"
@@ -88,6 +89,7 @@ struct Bars {
   uint64_t dv_staged[2], dk_staged[2];  // BO warps: bf16 dV / dK staged in slot t%2 -> store lane
                                         // (per slot: the BO warps may stage a chunk ahead of the store lane)
   uint64_t st_scaled, st_pub;  // state warps: TMEM state pre-scaled / bf16 copy published
+  uint64_t dk_ready[2];        // EPI: the staged dK tile turned into dkp in place by the state warps -> store lane
   uint32_t tmem_base;
 };
 
@@ -97,10 +99,17 @@ struct BwdArgs {
   const float* state_in;  // entering adjoint state (dkv orientation), nullable
   int64_t in_bh_stride, in_seg_stride;
   float* state_out;       // dkv_out (R(0)), written by segment 0
+  // EPI mode (the fused GLA core backward): dK -> dkp = act'(kp) * R^T dK before the store
+  const uint16_t* xp;
+  Strides3 sx;
+  const double* theta;
+  int act;
+  int64_t offset;
 };
 
 __device__ __forceinline__ uint32_t sw128(int r, int c) { return (uint32_t)(r * 128 + ((c ^ (r & 7)) << 4)); }
 
+template <bool EPI>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     tc_dkdv_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
                    const __grid_constant__ CUtensorMap map_v, const __grid_constant__ CUtensorMap map_do,
@@ -109,6 +118,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   extern __shared__ uint8_t smem_raw[];
   __shared__ Bars bars;
   __shared__ __align__(16) float pw[C + 8];
+  __shared__ float theta_s[EPI ? D / 2 : 1];
+  __shared__ float2 anchor_s[EPI ? D / 2 : 1];
   const uint32_t smem = (smem_u32(smem_raw) + 1023u) & ~1023u;
   uint8_t* smem_gen = smem_raw + (smem - smem_u32(smem_raw));
   auto slot = [smem](int i) { return smem + (uint32_t)(i * TILE); };
@@ -154,6 +165,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
     mbar_init(&bars.st_scaled, NUM_KV);
     mbar_init(&bars.st_pub, NUM_KV);
+    mbar_init(&bars.dk_ready[0], NUM_KV);
+    mbar_init(&bars.dk_ready[1], NUM_KV);
     fence_mbar_init();
   }
   griddep_wait();  // PDL: the previous kernel of the stream has completed (inputs written, outputs free)
@@ -163,6 +176,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const double l = load_decay(args.lam, hi);
     pw[threadIdx.x] = (float)(pow_int(l, (int)threadIdx.x) * (l / l));
   }
+  if (EPI && args.theta != nullptr && threadIdx.x >= 160 && threadIdx.x < 160 + D / 2)
+    theta_s[threadIdx.x - 160] = (float)args.theta[threadIdx.x - 160];
   if (warp == WARP_TMA && lane == 0) {
     tma_prefetch(&map_q);
     tma_prefetch(&map_k);
@@ -285,13 +300,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         tma_store_4d(&map_dv, slot_gen(SLOT_D + s) + HALF, 64, r0, hi, bi);
         tma_store_commit();
         LB_TR(t, 20);
-        mbar_wait(&bars.dk_staged[s], (t >> 1) & 1);
+        if (EPI) {  // dK waits for the state warps' transform: hand dO's slot back as soon as dV's store read it
+          tma_store_wait_read();
+          mbar_arrive(&bars.empty_d[s]);
+        }
+        mbar_wait(EPI ? &bars.dk_ready[s] : &bars.dk_staged[s], (t >> 1) & 1);
         tma_store_4d(&map_dk, slot_gen(SLOT_Q + s), 0, r0, hi, bi);
         tma_store_4d(&map_dk, slot_gen(SLOT_Q + s) + HALF, 64, r0, hi, bi);
         tma_store_commit();
         tma_store_wait_read();
         LB_TR(t, 21);
-        mbar_arrive(&bars.empty_d[s]);
+        if (!EPI) mbar_arrive(&bars.empty_d[s]);
         mbar_arrive(&bars.empty_q[s]);
       }
       tma_store_wait_all();
@@ -575,10 +594,73 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars.st_pub);
     };
+    // EPI: dkp(t) = act'(kp) * R^T dK(t) on the tile the B/O warps staged in Q's slot t % 2, in place; row i,
+    // this warp's 64 columns; kp loaded straight from global (one 128-byte row segment per thread)
+    uint4 xr[8];  // EPI: kp row segment of the chunk to transform next, loaded a chunk ahead of its use
+    auto load_x = [&](int t) {
+      const int r0 = chunk_row0(t);
+      if (r0 + i < p1) {
+        const uint4* src = reinterpret_cast<const uint4*>(args.xp + (int64_t)bi * args.sx.b + (int64_t)hi * args.sx.h +
+                                                          (int64_t)(r0 + i) * args.sx.n + hh * 64);
+#pragma unroll
+        for (int c = 0; c < 8; ++c) xr[c] = __ldg(src + c);
+      } else {
+#pragma unroll
+        for (int c = 0; c < 8; ++c) xr[c] = make_uint4(0, 0, 0, 0);
+      }
+    };
+    auto transform_dk = [&](int t) {
+      const int s = t & 1;
+      const int r0 = chunk_row0(t);
+      const bool rot = args.theta != nullptr;
+      if (rot) {
+        named_bar_sync(1, NUM_KV * 32);
+        if (warp == WARP_KV + 4 || warp == WARP_KV + 5) {
+          const int j = (warp - WARP_KV - 4) * 32 + lane;
+          float c0, s0;
+          lrpe_cs(args.theta[j], (int64_t)r0 + args.offset, &c0, &s0);
+          anchor_s[j] = make_float2(c0, s0);
+        }
+        named_bar_sync(1, NUM_KV * 32);
+      }
+      mbar_wait(&bars.dk_staged[s], (t >> 1) & 1);
+      const uint32_t row = slot(SLOT_Q + s) + hh * HALF;
+      auto tile = [&](auto act_tag) {
+        constexpr int ACT = decltype(act_tag)::value;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {  // fully unrolled: xr stays in registers
+          const uint32_t a = row + sw128(i, c);
+          const uint4 dy = lds128(a);
+          const uint32_t dw[4] = {dy.x, dy.y, dy.z, dy.w}, xw[4] = {xr[c].x, xr[c].y, xr[c].z, xr[c].w};
+          uint32_t o[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            float cs = 1.f, sn = 0.f;
+            if (rot) {
+              const int j = hh * 32 + 4 * c + e;
+              float cl, sl;
+              __sincosf(theta_s[j] * (float)i, &sl, &cl);
+              const float2 an = anchor_s[j];
+              cs = an.x * cl - an.y * sl;
+              sn = an.y * cl + an.x * sl;
+            }
+            o[e] = gla_pair_bwd<ACT>(xw[e], dw[e], cs, sn);
+          }
+          sts128(a, make_uint4(o[0], o[1], o[2], o[3]));
+        }
+      };
+      if (args.act == LA_ACT_SWISH) tile(std::integral_constant<int, LA_ACT_SWISH>{});
+      else if (args.act == LA_ACT_ONE_PLUS_ELU) tile(std::integral_constant<int, LA_ACT_ONE_PLUS_ELU>{});
+      else tile(std::integral_constant<int, LA_ACT_NONE>{});
+      fence_proxy_async_smem();  // the TMA store reads the tile next
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars.dk_ready[s]);
+    };
     if (nchunks > 0) {
       load_scale(true, pw[chunk_len(0)]);
       publish();
     }
+    if (EPI && nchunks > 0) load_x(0);
     for (int t = 0; t < nchunks; ++t) {
       mbar_wait(&bars.ds_full, t & 1);
       tc_fence_after();
@@ -587,6 +669,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         mbar_wait(&bars.x_done, t & 1);  // both products of chunk t read the previous copy
         publish();
         if (warp == WARP_KV && lane == 0) LB_TR(t, 19);
+      }
+      if (EPI) {
+        transform_dk(t);
+        if (t + 1 < nchunks) load_x(t + 1);  // in flight while the next chunk's products run
       }
     }
     if (nchunks > 0 && args.state_out != nullptr && seg == 0) {
@@ -617,12 +703,13 @@ void la_debug_set_trace_bwd(void* dev_ptr) { cudaMemcpyToSymbol(g_la_trace_bwd, 
 #endif
 
 cudaError_t tc_dkdv_launch(const PassDesc& p, const void* q, const void* k, const void* v, const void* dout,
-                           void* dk, void* dv, const Strides3* s, cudaStream_t st) {
+                           void* dk, void* dv, const Strides3* s, cudaStream_t st, const GlaEpilogue* epi) {
   CUtensorMap mq, mk, mv, mdo, mdk, mdv;
   if (!tc_make_map(&mq, q, p, s[0]) || !tc_make_map(&mk, k, p, s[1]) || !tc_make_map(&mv, v, p, s[2]) ||
       !tc_make_map(&mdo, dout, p, s[3]) || !tc_make_map(&mdk, dk, p, s[4]) || !tc_make_map(&mdv, dv, p, s[5]))
     return cudaErrorInvalidValue;
   BwdArgs a;
+  std::memset(&a, 0, sizeof(a));
   a.heads = p.heads;
   a.n = p.n;
   a.seg_len = p.seg_len;
@@ -632,11 +719,23 @@ cudaError_t tc_dkdv_launch(const PassDesc& p, const void* q, const void* k, cons
   a.in_bh_stride = p.state_in_bh_stride;
   a.in_seg_stride = p.state_in_seg_stride;
   a.state_out = reinterpret_cast<float*>(p.state_out);
-  static std::atomic<bool> smem_set[64] = {};
-  cudaError_t err = set_smem_once(tc_dkdv_kernel, (int)SMEM_BYTES, smem_set);
-  if (err != cudaSuccess) return err;
   dim3 grid(p.nseg, p.batch * p.heads);
-  return launch_pdl(tc_dkdv_kernel, grid, dim3(NUM_THREADS), SMEM_BYTES, st, mq, mk, mv, mdo, mdk, mdv, a);
+  if (epi != nullptr) {
+    if (reinterpret_cast<uintptr_t>(epi->xp) & 15) return cudaErrorMisalignedAddress;
+    a.xp = reinterpret_cast<const uint16_t*>(epi->xp);
+    a.sx = epi->sx;
+    a.theta = epi->theta;
+    a.act = epi->act;
+    a.offset = epi->offset;
+    static std::atomic<bool> smem_set_epi[64] = {};
+    cudaError_t err = set_smem_once(tc_dkdv_kernel<true>, (int)SMEM_BYTES, smem_set_epi);
+    if (err != cudaSuccess) return err;
+    return launch_pdl(tc_dkdv_kernel<true>, grid, dim3(NUM_THREADS), SMEM_BYTES, st, mq, mk, mv, mdo, mdk, mdv, a);
+  }
+  static std::atomic<bool> smem_set[64] = {};
+  cudaError_t err = set_smem_once(tc_dkdv_kernel<false>, (int)SMEM_BYTES, smem_set);
+  if (err != cudaSuccess) return err;
+  return launch_pdl(tc_dkdv_kernel<false>, grid, dim3(NUM_THREADS), SMEM_BYTES, st, mq, mk, mv, mdo, mdk, mdv, a);
 }
 
 }  // namespace la

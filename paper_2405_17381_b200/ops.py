@@ -484,6 +484,32 @@ def gla_core_forward(qp, kp, v, lam, heads, *, act="swish", theta=None, offset=0
     return (o, q, k, kv_out) if want_state else (o, q, k)
 
 
+def gla_core_backward(qp, kp, q, k, v, da, lam, heads, *, act="swish", theta=None, offset=0, lam_dev=None,
+                      kv_in=None, dkv_in=None, want_state=False):
+    """The fused GLA core backward (la_gla_core_bwd): (dqp, dkp, dv) of the core on [batch, n, heads * d] rows --
+    the core's backward on the forward's q, k (``gla_core_forward``'s q / k out), v and da, with the prologue's
+    backward (act' and the inverse LRPE rotation) applied to the dq / dK tiles before they are stored.  No angle
+    gradient (use ``la_backward`` + ``gla_prologue_backward`` when theta is learned).  Raises UnsupportedError
+    outside bf16 / d = 128."""
+    qp, kp, q, k, v, da = _rows([qp, kp, q, k, v, da], ["qp", "kp", "q", "k", "v", "da"])
+    desc = _gla_desc(qp, heads, act, offset, SRMS_EPS)
+    th = _theta(theta, desc.d, qp.device)
+    lam_dev, lam_p = _lam(lam, lam_dev, heads, qp.device)
+    g = Geometry(desc.batch, heads, desc.n, desc.d, None)
+    kv_in = _state(kv_in, g, qp.dtype, "kv_in")
+    dkv_in = _state(dkv_in, g, qp.dtype, "dkv_in")
+    dqp, dkp, dv = torch.empty_like(qp), torch.empty_like(kp), torch.empty_like(v)
+    dkv_out = torch.empty((desc.batch, heads, desc.d, desc.d), dtype=state_dtype(qp.dtype), device=qp.device) \
+        if want_state else None
+    lib = _lib.load()
+    nbytes = lib.la_gla_core_bwd_workspace_bytes(ctypes.byref(desc))
+    ws = torch.empty(nbytes, dtype=torch.uint8, device=qp.device) if nbytes else None
+    _lib.check(lib.la_gla_core_bwd(ctypes.byref(desc), _ptr(qp), _ptr(kp), _ptr(q), _ptr(k), _ptr(v), _ptr(da), lam_p,
+                                   _ptr(th), _ptr(kv_in), _ptr(dkv_in), _ptr(dqp), _ptr(dkp), _ptr(dv), _ptr(dkv_out),
+                                   _ptr(ws), nbytes, _stream(qp.device)))
+    return (dqp, dkp, dv, dkv_out) if want_state else (dqp, dkp, dv)
+
+
 def gla_prologue_backward(qp, kp, dq, dk, heads, *, act="swish", theta=None, offset=0, dtheta=None):
     """(dqp, dkp) of gla_prologue; with theta, the angle gradient is accumulated into ``dtheta``
     (fp64 [d/2], created when None) and returned as the third value."""

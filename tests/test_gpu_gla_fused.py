@@ -171,3 +171,38 @@ def test_gla_layer_on_the_fused_core_matches_fp64():
         errs[f"d{k}"] = _scaled(wb[k].grad, w64[k].grad)
     assert errs["y"] <= 5e-2, errs
     assert all(e <= 1.5e-1 for e in errs.values()), errs
+
+
+@pytest.mark.parametrize("act,rot,b,n,heads", [("swish", True, 6, 777, 16), ("swish", False, 1, 3000, 4),
+                                               ("one_plus_elu", True, 2, 1500, 8), ("none", True, 6, 300, 16)])
+def test_fused_core_backward(act, rot, b, n, heads):
+    """la_gla_core_bwd: (dqp, dkp, dv) equal the two-step path (la_bwd + la_gla_prologue_bwd) within the bf16
+    bar, and the fp64 autograd gradients of the restated core (act, LRPE, decayed attention) within 3e-2 --
+    unsplit (batch x heads = 96) and split sequences."""
+    g = torch.Generator(device=DEV).manual_seed(n + heads)
+    qp, kp, v, da = [(torch.randn(b, n, heads * D, device=DEV, generator=g) * sc).to(torch.bfloat16)
+                     for sc in (1.0, 1.0, 0.5, 0.5)]
+    lams = ([1.0, 0.999, 0.9, 0.5, 0.05, 0.63, 0.99, 0.3] * 2)[:heads]
+    theta = THETA if rot else None
+    o, q, k = ops.gla_core_forward(qp, kp, v, lams, heads, act=act, theta=theta, offset=2)
+    dqp, dkp, dv = ops.gla_core_backward(qp, kp, q, k, v, da, lams, heads, act=act, theta=theta, offset=2)
+    dq2, dk2, dv2 = ops.la_backward(*(t.view(b, n, heads, D) for t in (q, k, v, da)), lams, layout="bnhd")
+    dqp2, dkp2, _ = ops.gla_prologue_backward(qp, kp, dq2.view(b, n, -1), dk2.view(b, n, -1), heads, act=act,
+                                              theta=theta, offset=2)
+    for name, got, ref in (("dqp", dqp, dqp2), ("dkp", dkp, dkp2), ("dv", dv, dv2.view(b, n, -1))):
+        assert _scaled(got, ref.double()) <= 2e-2, name
+    # fp64 autograd of the restated core on the same bf16 inputs
+    qp64, kp64, v64 = (t.double().requires_grad_(True) for t in (qp, kp, v))
+    q64, k64 = _act64(qp64, act), _act64(kp64, act)
+    if rot:
+        q64, k64 = _rot64(q64, THETA, 2), _rot64(k64, THETA, 2)
+    qh, kh, vh = (t.view(b, n, heads, D).transpose(1, 2) for t in (q64, k64, v64))
+    lam = torch.tensor(lams, dtype=torch.float64, device=DEV)
+    t = torch.arange(n, device=DEV)
+    diff = (t[:, None] - t[None, :]).to(torch.float64)
+    mask = torch.where(diff[None] >= 0, lam[:, None, None] ** diff.clamp(min=0)[None],
+                       torch.zeros((), device=DEV, dtype=torch.float64))
+    a64 = (((qh @ kh.transpose(-1, -2)) * mask[None]) @ vh).transpose(1, 2).reshape(b, n, heads * D)
+    a64.backward(da.double())
+    for name, got, ref in (("dqp", dqp, qp64.grad), ("dkp", dkp, kp64.grad), ("dv", dv, v64.grad)):
+        assert _scaled(got, ref) <= 3e-2, name

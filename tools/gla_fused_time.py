@@ -37,3 +37,18 @@ for b, n in ((8, 8192), (64, 1024)):
         print(f"[{b},{n},{H * D}] lrpe={th is not None}: prologue {pro:.4f} + core {core:.4f} = {pro + core:.4f} ms | "
               f"fused {fused:.4f} ms (x{(pro + core) / fused:.2f}) | fused no q/k {fnq:.4f} ms (x{(pro + core) / fnq:.2f})",
               flush=True)
+
+# the backward: fused (la_gla_core_bwd) vs two-step (la_bwd + la_gla_prologue_bwd)
+for b, n in ((8, 8192), (64, 1024)):
+    qp, kp, v, da = (torch.randn(b, n, H * D, device="cuda").to(torch.bfloat16) for _ in range(4))
+    for th in (theta, None):
+        _, q, k = ops.gla_core_forward(qp, kp, v, None, H, theta=th, lam_dev=lam)
+
+        def two_step():
+            dq, dk, dv = ops.la_backward(*(t.view(b, n, H, D) for t in (q, k, v, da)), None, lam_dev=lam, layout="bnhd")
+            ops.gla_prologue_backward(qp, kp, dq.view(b, n, -1), dk.view(b, n, -1), H, theta=th)
+
+        t2 = t_ms(two_step)
+        tf = t_ms(lambda: ops.gla_core_backward(qp, kp, q, k, v, da, None, H, theta=th, lam_dev=lam))
+        print(f"bwd [{b},{n},{H * D}] lrpe={th is not None}: two-step {t2:.4f} ms | fused {tf:.4f} ms (x{t2 / tf:.2f})",
+              flush=True)

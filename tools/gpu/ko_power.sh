@@ -3,7 +3,7 @@
 # usage: bash tools/gpu/ko_power.sh name1 name2 ...
 for rep in 1 2; do for n in "$@"; do LA_B200_LIB=build/var/lib$n.so python tools/gpu/ko_power.py; done; done
 [ "${STEPS:-0}" = "1" ] || exit 0
-for rep in 1 2; do for n in "$@"; do
+for rep in ${REPS:-1 2}; do for n in "$@"; do
   LA_B200_LIB=build/var/lib$n.so python tools/step_probe.py 40 > gpurun_out/ko_steps_$n.log 2>&1
   python - gpurun_out/ko_steps_$n.log $n <<'PY'
 import sys, re
