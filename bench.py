@@ -109,7 +109,7 @@ def maybe_relaunch(args) -> None:
         return
     if args.gpus <= 1 or args.impl == "reference":  # the reference arm is host-only: rank 0's work, no ranks
         return
-    if os.environ.get("LA_BENCH_LAUNCH_PROBE") != "1":
+    if os.environ.get("LA_BENCH_LAUNCH_PROBE") != "1" and os.environ.get("LA_BENCH_SHARED_GPU") != "1":
         import torch
 
         have = torch.cuda.device_count()
@@ -196,10 +196,18 @@ def run_ours(args) -> None:
     from paper_2405_17381_b200 import ops
 
     rank, world, local = dist_env()
+    # LA_BENCH_SHARED_GPU=1 (tests only: tests/test_gpu_bench_ranks.py): every rank on cuda:0 over gloo, to run
+    # the multi-rank code path on a one-GPU box -- its numbers are meaningless (the ranks share one GPU)
+    shared = os.environ.get("LA_BENCH_SHARED_GPU") == "1"
+    if shared:
+        local = 0
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=device)
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=device)
     lam_dev = ops.decay_tensor(lams(), H, device)
     seq_lens = [n for n in args.seq_lens]
     gen = torch.Generator(device=device).manual_seed(1234 + rank)
@@ -247,10 +255,15 @@ def run_ours(args) -> None:
     if world > 1:
         dist.barrier()
     total_ms = t0.elapsed_time(t1)
-    if world > 1:
-        t = torch.tensor([total_ms], device=device, dtype=torch.float64)
+
+    def reduce_max(ms: float) -> float:  # max over ranks (a host tensor over gloo, a device one over NCCL)
+        if world == 1:
+            return ms
+        t = torch.tensor([ms], device="cpu" if shared else device, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+        return float(t.item())
+
+    total_ms = reduce_max(total_ms)
 
     pk = peaks()
     sweep = {}
@@ -274,13 +287,6 @@ def run_ours(args) -> None:
     roof = pass_roofline(ops, inputs[args.roofline_n], lam_dev, stream, pk)
     launches = sum(ops.launch_count(tuple(inputs[n][0].shape), which="fwd")
                    + ops.launch_count(tuple(inputs[n][0].shape), which="bwd_saved") for n in seq_lens) * args.steps
-
-    def reduce_max(ms: float) -> float:
-        if world == 1:
-            return ms
-        t = torch.tensor([ms], device=device, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
 
     e2e = None if args.no_e2e else run_e2e(ops, seq_lens, tokens, lam_dev, device, min(args.steps, args.e2e_steps),
                                            world, reduce_max)

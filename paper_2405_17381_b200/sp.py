@@ -124,8 +124,18 @@ class CudaKernels:
         return dq
 
 
+def _host_staged(x: torch.Tensor, group) -> bool:
+    """gloo moves host tensors: a CUDA state crosses it through a host copy (NCCL takes device tensors)."""
+    return x.is_cuda and dist.get_backend(group) == "gloo"
+
+
 def _gather(x: torch.Tensor, group) -> list[torch.Tensor]:
     world = dist.get_world_size(group)
+    if _host_staged(x, group):
+        h = x.detach().cpu()
+        out = [torch.empty_like(h) for _ in range(world)]
+        dist.all_gather(out, h, group=group)
+        return [o.to(x.device) for o in out]
     out = [torch.empty_like(x) for _ in range(world)]
     dist.all_gather(out, x.contiguous(), group=group)
     return out
@@ -158,13 +168,19 @@ def _chain(delta: torch.Tensor, lengths: Sequence[int], lam: torch.Tensor, group
     rank, world = dist.get_rank(group), dist.get_world_size(group)
     src = rank + 1 if reverse else rank - 1
     dst = rank - 1 if reverse else rank + 1
+    staged = _host_staged(delta, group)
     entering = torch.zeros_like(delta)
     if 0 <= src < world:
-        dist.recv(entering, group_src=src, group=group)
+        if staged:
+            h = torch.empty_like(delta, device="cpu")
+            dist.recv(h, group_src=src, group=group)
+            entering = h.to(delta.device)
+        else:
+            dist.recv(entering, group_src=src, group=group)
     if 0 <= dst < world:
         out = (_decay(lam, lengths[rank]).to(delta.device) * entering.to(torch.float64)
                + delta.to(torch.float64)).to(delta.dtype)
-        dist.send(out.contiguous(), group_dst=dst, group=group)
+        dist.send(out.cpu() if staged else out.contiguous(), group_dst=dst, group=group)
     return entering
 
 
