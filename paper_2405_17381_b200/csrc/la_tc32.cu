@@ -531,8 +531,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         T32(t, 9);
         store_at(th, tl);
       }
-      // out(t): O -> fp32 rows staged in C's region (TMA-store layout), stored by the TMA lane
+      // out(t): O -> fp32 rows staged in C's region (TMA-store layout), stored by the TMA lane.  The staging
+      // overwrites C's split, written by other workers: the tensor core has read it (all_done), and the
+      // workers' barrier orders those writes before these in the CTA's own (generic-proxy) order too
       await(&bars.all_done, t);
+      wbar();
       T32(t, 10);
 #pragma unroll 1
       for (int part = 0; part < 2; ++part) {

@@ -41,5 +41,13 @@ for dtype in (torch.bfloat16, torch.float32):
     red = torch.zeros(74, 257, device="cuda", dtype=ops.state_dtype(dtype))
     ops.gla_gate_rowsq(a, u, 4, red[:, 256], rowsq_stride=257)
     ops.gla_rowscale(red, 256)
+# round 2b: the fused GLA core forward (GLA modes of the pass and summary kernels) and backward (EPI modes),
+# unsplit (bh = 96) and split (bh = 4) sequences, LRPE on
+theta = torch.rand(64, dtype=torch.float64, device="cuda")
+for b, n, h in ((6, 300, 16), (1, 1000, 4)):
+    qp, kp, v, da = (torch.rand(b, n, h * 128, device="cuda", dtype=torch.bfloat16) for _ in range(4))
+    lam = [0.9, 0.99, 0.5, 1.0] * (h // 4)
+    o, q, k = ops.gla_core_forward(qp, kp, v, lam, h, theta=theta, offset=3)
+    ops.gla_core_backward(qp, kp, q, k, v, da, lam, h, theta=theta, offset=3)
 torch.cuda.synchronize()
 print("ok")
