@@ -934,7 +934,7 @@ const char* la_last_error(void) { return g_last_error.c_str(); }
 int la_abi_version(void) { return LA_ABI_VERSION; }
 
 const char* la_build_info(void) {
-  return "lightning-attn b200: sm_100a, backends simt(f64/f32/bf16) + tcgen05(bf16, f32 3xbf16 split); decode; GLA stages";
+  return "lightning-attn b200: sm_100a, backends simt(f64/f32/bf16) + tcgen05(bf16, f32 3xbf16 split); decode; GLA stages + fused GLA core";
 }
 
 }  // extern "C"
