@@ -24,28 +24,33 @@ namespace la {
 namespace {
 
 // fp32 accumulation uses the SFU forms (ex2 + rcp approximations, ~2^-21 relative): the stages are
-// bound by instruction issue otherwise; fp64 keeps the library functions
-template <typename Tacc>
+// bound by instruction issue otherwise; fp64 keeps the library functions.  FAST (bf16 operands, whose
+// results round to 2^-9 anyway): one SFU op, tanh.approx (~2^-11), instead of two
+template <typename Tacc, bool FAST = false>
 __device__ __forceinline__ Tacc sigmoid(Tacc x) {
   if constexpr (sizeof(Tacc) == 8) return (Tacc)0.5 * ((Tacc)1 + tanh((Tacc)0.5 * x));  // tanh form, model.py:57-66
-  else return __fdividef(1.f, 1.f + __expf(-x));
+  else if constexpr (FAST) {
+    float t;
+    asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(0.5f * x));
+    return fmaf(0.5f, t, 0.5f);
+  } else return __fdividef(1.f, 1.f + __expf(-x));
 }
 template <typename Tacc>
 __device__ __forceinline__ Tacc expo(Tacc x) {
   if constexpr (sizeof(Tacc) == 8) return exp(x);
   else return __expf(x);
 }
-template <typename Tacc>
+template <typename Tacc, bool FAST = false>
 __device__ __forceinline__ Tacc act_fwd(Tacc x, int act) {
-  if (act == LA_ACT_SWISH) return x * sigmoid(x);
+  if (act == LA_ACT_SWISH) return x * sigmoid<Tacc, FAST>(x);
   if (act == LA_ACT_ONE_PLUS_ELU) return x > (Tacc)0 ? x + (Tacc)1 : expo(x);
   return x;
 }
 // act(x) and act'(x) sharing one sigmoid / exp
-template <typename Tacc>
+template <typename Tacc, bool FAST = false>
 __device__ __forceinline__ void act_both(Tacc x, int act, Tacc& a, Tacc& g) {
   if (act == LA_ACT_SWISH) {
-    const Tacc s = sigmoid(x);
+    const Tacc s = sigmoid<Tacc, FAST>(x);
     a = x * s;
     g = s * ((Tacc)1 + x * ((Tacc)1 - s));
   } else if (act == LA_ACT_ONE_PLUS_ELU) {
@@ -150,8 +155,11 @@ __global__ void __launch_bounds__(256) prologue_kernel(const T* __restrict__ qp,
     if (theta != nullptr) rw.at(tp + offset, row == r0 || tp == 0 || ((row - r0) % kAnchor) == 0);
 #pragma unroll
     for (int pr = 0; pr < V / 2; ++pr) {
-      Tacc q1 = act_fwd<Tacc>((Tacc)Cvt<T>::to_f(xq.v[2 * pr]), act), q2 = act_fwd<Tacc>((Tacc)Cvt<T>::to_f(xq.v[2 * pr + 1]), act);
-      Tacc k1 = act_fwd<Tacc>((Tacc)Cvt<T>::to_f(xk.v[2 * pr]), act), k2 = act_fwd<Tacc>((Tacc)Cvt<T>::to_f(xk.v[2 * pr + 1]), act);
+      constexpr bool FAST = sizeof(T) == 2;
+      Tacc q1 = act_fwd<Tacc, FAST>((Tacc)Cvt<T>::to_f(xq.v[2 * pr]), act),
+           q2 = act_fwd<Tacc, FAST>((Tacc)Cvt<T>::to_f(xq.v[2 * pr + 1]), act);
+      Tacc k1 = act_fwd<Tacc, FAST>((Tacc)Cvt<T>::to_f(xk.v[2 * pr]), act),
+           k2 = act_fwd<Tacc, FAST>((Tacc)Cvt<T>::to_f(xk.v[2 * pr + 1]), act);
       if (theta != nullptr) {
         const Tacc c = rw.c[pr], s = rw.s[pr];
         const Tacc a1 = q1 * c - q2 * s, a2 = q1 * s + q2 * c;
@@ -208,10 +216,11 @@ __global__ void __launch_bounds__(256) prologue_bwd_kernel(const T* __restrict__
         Tacc gq1 = (Tacc)Cvt<T>::to_f(gq.v[2 * pr]), gq2 = (Tacc)Cvt<T>::to_f(gq.v[2 * pr + 1]);
         Tacc gk1 = (Tacc)Cvt<T>::to_f(gk.v[2 * pr]), gk2 = (Tacc)Cvt<T>::to_f(gk.v[2 * pr + 1]);
         Tacc aq1, aq2, ak1, ak2, hq1, hq2, hk1, hk2;  // act and act' (one sigmoid each)
-        act_both<Tacc>(xq1, act, aq1, hq1);
-        act_both<Tacc>(xq2, act, aq2, hq2);
-        act_both<Tacc>(xk1, act, ak1, hk1);
-        act_both<Tacc>(xk2, act, ak2, hk2);
+        constexpr bool FAST = sizeof(T) == 2;
+        act_both<Tacc, FAST>(xq1, act, aq1, hq1);
+        act_both<Tacc, FAST>(xq2, act, aq2, hq2);
+        act_both<Tacc, FAST>(xk1, act, ak1, hk1);
+        act_both<Tacc, FAST>(xk2, act, ak2, hk2);
         if (theta != nullptr) {
           const Tacc c = rw.c[pr], s = rw.s[pr];
           // rotated activations y (recomputed) for the angle gradient
