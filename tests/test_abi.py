@@ -172,3 +172,64 @@ def test_workspace_covers_every_backend_plan():
         tc = _desc(batch=1, heads=4, n=n, d=128, dtype=_lib.LA_BF16)
         simt = _desc(batch=1, heads=4, n=n, d=128, dtype=_lib.LA_BF16, backend=_lib.LA_BACKEND_SIMT)
         assert lib.la_workspace_bytes(ctypes.byref(tc)) >= lib.la_workspace_bytes(ctypes.byref(simt))
+
+
+def _gla_desc(**kw):
+    d = _lib.LaGlaDesc()
+    d.batch, d.n, d.heads, d.d = kw.get("batch", 2), kw.get("n", 300), kw.get("heads", 16), kw.get("d", 128)
+    d.dtype = kw.get("dtype", _lib.LA_BF16)
+    d.act = kw.get("act", _lib.LA_ACT_SWISH)
+    d.offset = kw.get("offset", 0)
+    d.eps = 1e-8
+    return d
+
+
+def test_gla_core_entry_validation():
+    """la_gla_core_fwd / la_gla_core_bwd (ABI 4) reject bad descriptors, missing operands, lone q_out / k_out,
+    misaligned rows and non-tensor-core shapes before any device work; their workspace sizes follow the
+    attention plan (0 when sequences are not split)."""
+    lib = _lib.load()
+    d16 = ctypes.c_void_p(16)
+    lam = ctypes.cast(ctypes.c_void_p(16), ctypes.POINTER(ctypes.c_double))
+
+    def fwd(desc, qp=d16, q_out=None, k_out=None):
+        return lib.la_gla_core_fwd(ctypes.byref(desc), qp, d16, d16, lam, None, None, d16, q_out, k_out, None, None,
+                                   0, None)
+
+    def bwd(desc, dqp=d16):
+        return lib.la_gla_core_bwd(ctypes.byref(desc), d16, d16, d16, d16, d16, d16, lam, None, None, None, dqp, d16,
+                                   d16, None, None, 0, None)
+
+    assert fwd(_gla_desc(n=0)) == _lib.LA_ERR_DOMAIN
+    assert fwd(_gla_desc(act=9)) == _lib.LA_ERR_DOMAIN
+    assert fwd(_gla_desc(offset=-1)) == _lib.LA_ERR_DOMAIN
+    assert fwd(_gla_desc(), qp=None) == _lib.LA_ERR_SHAPE
+    assert fwd(_gla_desc(), q_out=d16) == _lib.LA_ERR_SHAPE and b"together" in lib.la_last_error()
+    assert fwd(_gla_desc(), qp=ctypes.c_void_p(24)) == _lib.LA_ERR_SHAPE  # rows must be 16-byte aligned
+    assert fwd(_gla_desc(dtype=_lib.LA_F32)) == _lib.LA_ERR_UNSUPPORTED
+    assert fwd(_gla_desc(d=64, heads=32)) == _lib.LA_ERR_UNSUPPORTED
+    assert bwd(_gla_desc(), dqp=None) == _lib.LA_ERR_SHAPE
+    assert bwd(_gla_desc(dtype=_lib.LA_F64)) == _lib.LA_ERR_UNSUPPORTED
+    full = _gla_desc(batch=8, n=8192)           # batch x heads = 128: one unsplit wave
+    split = _gla_desc(batch=1, n=1 << 16)       # 16 sequences: split into segments
+    assert lib.la_gla_core_workspace_bytes(ctypes.byref(full)) == 0
+    assert lib.la_gla_core_workspace_bytes(ctypes.byref(split)) > 0
+    assert lib.la_gla_core_bwd_workspace_bytes(ctypes.byref(split)) >= lib.la_gla_core_workspace_bytes(
+        ctypes.byref(split))
+    assert lib.la_gla_core_workspace_bytes(ctypes.byref(_gla_desc(dtype=_lib.LA_F32))) == 0
+
+
+def test_fp32_tensor_core_backend_selection():
+    """fp32 at d = 128 with 16-byte strides is served by the tcgen05 split pass (its own plan: one wave of
+    segments for a long sequence, bounded workspace); fp32 at other head dims cannot be forced onto it."""
+    lib = _lib.load()
+    long32 = _desc(batch=1, heads=16, n=1 << 17, d=128, dtype=_lib.LA_F32, backend=_lib.LA_BACKEND_TCGEN05)
+    assert lib.la_segment_count(ctypes.byref(long32)) == 148 // 16
+    sizes = {lib.la_workspace_bytes(ctypes.byref(_desc(batch=1, heads=16, n=n, d=128, dtype=_lib.LA_F32)))
+             for n in (1 << 14, 1 << 17, 1 << 20)}
+    assert len(sizes) == 1 and sizes.pop() > 0
+    # backward on the split pass: three passes (no fused dK/dV sweep in fp32)
+    assert lib.la_launch_count(ctypes.byref(_desc(batch=64, heads=16, n=1024, d=128, dtype=_lib.LA_F32)), 1) == 3
+    assert _fwd(_desc(d=64, dtype=_lib.LA_F32, backend=_lib.LA_BACKEND_TCGEN05)) == _lib.LA_ERR_UNSUPPORTED
+    assert _fwd(_desc(d=128, dtype=_lib.LA_F32, backend=_lib.LA_BACKEND_TCGEN05, stride=(2 * 64 * 130, 64 * 130, 130))) \
+        == _lib.LA_ERR_UNSUPPORTED  # a position stride of 130 floats is not 16-byte aligned
