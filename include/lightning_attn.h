@@ -77,7 +77,7 @@ typedef enum la_dtype {
 typedef enum la_backend {
   LA_BACKEND_AUTO = 0,     /* tcgen05 when eligible, else SIMT                  */
   LA_BACKEND_SIMT = 1,     /* CUDA-core kernels (any d <= 128, any dtype)       */
-  LA_BACKEND_TCGEN05 = 2   /* TMA + tcgen05/TMEM kernels (bf16 or fp32, d == 128) */
+  LA_BACKEND_TCGEN05 = 2   /* TMA + tcgen05/TMEM kernels (bf16 or fp32, d in {32, 64, 96, 128}) */
 } la_backend;
 
 typedef struct la_desc {

@@ -48,6 +48,7 @@ struct SumBars {
 struct SumArgs {
   int heads, n, seg_len, nseg, rev;
   int sub_len, sub_per_seg, g_lo;
+  int d;  // head dim (64 or 128): features past d are zero (TMA out-of-bounds fill); deltas are d x d
   const double* lam;
   float* delta_out;  // [bh][nseg * sub_per_seg][d][d]
   // GLA mode: B is the pre-activation kp; the B warps apply rot(act(.)) before the decay weight
@@ -253,9 +254,10 @@ __global__ void __launch_bounds__(S_THREADS, 2)
     tc_fence_after();
     const int quad = warp & 3;
     const int r = quad * 32 + lane;
-    float* dst = args.delta_out + ((int64_t)bh * args.nseg * args.sub_per_seg + slot) * SD * SD + (int64_t)r * SD;
+    const int dS = args.d;
+    float* dst = args.delta_out + ((int64_t)bh * args.nseg * args.sub_per_seg + slot) * dS * dS + (int64_t)r * dS;
 #pragma unroll 1
-    for (int cb = 0; cb < 4; ++cb) {
+    for (int cb = 0; cb < (r < dS ? dS / 32 : 0); ++cb) {
       float v[32];
       tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + cb * 32, v);
       tmem_ld_wait();
@@ -287,6 +289,7 @@ cudaError_t tc_summary_launch(const PassDesc& p, cudaStream_t st, const GlaProlo
   a.sub_len = p.sub_len;
   a.sub_per_seg = p.sub_per_seg;
   a.g_lo = p.g_lo;
+  a.d = p.d;
   a.lam = p.lam;
   a.delta_out = reinterpret_cast<float*>(p.delta_out);
   dim3 grid((p.g_hi - p.g_lo + 1) * p.sub_per_seg, p.batch * p.heads);

@@ -120,6 +120,7 @@ constexpr size_t SMEM_BYTES = SMEM_TILES + 1024 /*align slack*/;
 
 struct TcArgs {
   int heads, n, seg_len, nseg, rev;
+  int d;  // head dim (64 or 128): features past d are zero (TMA out-of-bounds fill), states are d x d
   const double* lam;
   uint16_t* out;  // bf16 output (full mode)
   const float* state_in;
@@ -738,14 +739,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll 1
       for (int q4 = 0; q4 < 4; ++q4) {
         float x[16];
-        if (args.state_in != nullptr) {
+        const int dS = args.d, c0 = hh * 64 + q4 * 16;
+        if (args.state_in != nullptr && i < dS && c0 < dS) {
           const float* src = args.state_in + (int64_t)bh * args.in_bh_stride + (int64_t)seg * args.in_seg_stride;
           if (args.in_T) {
 #pragma unroll
-            for (int j = 0; j < 16; ++j) x[j] = src[(hh * 64 + q4 * 16 + j) * D + i];  // lanes: consecutive i
+            for (int j = 0; j < 16; ++j) x[j] = src[(c0 + j) * dS + i];  // lanes: consecutive i
           } else {
             // row i, 16 consecutive columns: four 16-byte loads (the state buffers are 16-byte aligned)
-            const float4* s4 = reinterpret_cast<const float4*>(src + i * D + hh * 64 + q4 * 16);
+            const float4* s4 = reinterpret_cast<const float4*>(src + i * dS + c0);
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
               const float4 w = s4[j];
@@ -787,7 +789,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
     if (nchunks > 0 && args.state_out != nullptr && (rev ? seg == 0 : seg == args.nseg - 1)) {
       // the pass's final state F(n) / R(0): kv_out / dkv_out
-      float* dst = args.state_out + (int64_t)bh * D * D;
+      const int dS = args.d;
+      float* dst = args.state_out + (int64_t)bh * dS * dS;
       const int T = args.out_T;
       {
 #pragma unroll 1
@@ -798,7 +801,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
             const int col = hh * 64 + q4 * 16 + j;
-            dst[T ? (col * D + i) : (i * D + col)] = x[j];
+            if (i < dS && col < dS) dst[T ? (col * dS + i) : (i * dS + col)] = x[j];
           }
         }
       }
@@ -876,6 +879,7 @@ cudaError_t launch_tc(const PassDesc& p, cudaStream_t st, const GlaPrologue* gla
   a.out = reinterpret_cast<uint16_t*>(p.out);
   a.heads = p.heads;
   a.n = p.n;
+  a.d = p.d;
   a.seg_len = p.seg_len;
   a.nseg = p.nseg;
   a.rev = p.rev;
@@ -935,7 +939,9 @@ extern "C" __attribute__((visibility("default"))) int la_debug_set_trace_bwd_c(v
 #endif
 
 bool tc_supported(int dtype, int d, const int64_t* strides, int count) {
-  if (dtype != LA_BF16 || d != D) return false;
+  // d < 128 runs the d = 128 kernels on zero-padded features: the TMA boxes past d read zeros and stores past
+  // d are clipped, states are d x d
+  if (dtype != LA_BF16 || d < 32 || d > D || d % 32 != 0) return false;
   for (int i = 0; i < 3 * count; ++i)
     if ((strides[i] * 2) % 16 != 0) return false;
   return true;

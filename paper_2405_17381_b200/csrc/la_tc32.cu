@@ -91,6 +91,7 @@ struct Bars {
 
 struct Tc32Args {
   int heads, n, seg_len, nseg, rev;
+  int d;  // head dim (a multiple of 32, <= 128): features past d are zero (TMA out-of-bounds fill), states d x d
   const double* lam;
   float* out;
   Strides3 so;
@@ -328,13 +329,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #pragma unroll 1
       for (int q4 = 0; q4 < 4; ++q4) {
         uint32_t w[16];
-        if (!STATE_ONLY && args.state_in != nullptr) {
+        if (!STATE_ONLY && args.state_in != nullptr && i < args.d && 64 * hh + 16 * q4 < args.d) {
+          const int dS = args.d;
           const float* src = args.state_in + (int64_t)bh * args.in_bh_stride + (int64_t)seg * args.in_seg_stride;
           if (args.in_T) {
 #pragma unroll
-            for (int j = 0; j < 16; ++j) w[j] = __float_as_uint(src[(64 * hh + 16 * q4 + j) * D + i]);
+            for (int j = 0; j < 16; ++j) w[j] = __float_as_uint(src[(64 * hh + 16 * q4 + j) * dS + i]);
           } else {
-            const float4* s4 = reinterpret_cast<const float4*>(src + i * D + 64 * hh + 16 * q4);
+            const float4* s4 = reinterpret_cast<const float4*>(src + i * dS + 64 * hh + 16 * q4);
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
               const float4 v = s4[j];
@@ -556,13 +558,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     if (nchunks > 0) {
       float* dst = nullptr;
       int T = 0;
+      const int dS = args.d;
       if (STATE_ONLY) {
-        dst = args.delta_out + ((int64_t)bh * args.nseg + seg) * D * D;
+        dst = args.delta_out + ((int64_t)bh * args.nseg + seg) * dS * dS;
       } else if (args.state_out != nullptr && (rev ? seg == 0 : seg == args.nseg - 1)) {
-        dst = args.state_out + (int64_t)bh * D * D;
+        dst = args.state_out + (int64_t)bh * dS * dS;
         T = args.out_T;
       }
-      if (dst != nullptr) {
+      if (dst != nullptr && i < dS) {
 #pragma unroll 1
         for (int part = 0; part < 2; ++part) {
           float x[32];
@@ -571,7 +574,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
             const int col = 64 * hh + 32 * part + j;
-            dst[T ? (col * D + i) : (i * D + col)] = x[j];
+            if (col < dS) dst[T ? (col * dS + i) : (i * dS + col)] = x[j];
           }
         }
       }
@@ -622,7 +625,8 @@ extern "C" __attribute__((visibility("default"))) int la_debug_set_trace32(void*
 #endif
 
 bool tc32_supported(int dtype, int d, const int64_t* strides, int count) {
-  if (dtype != LA_F32 || d != D) return false;
+  // d < 128 runs the d = 128 kernel on zero-padded features (TMA out-of-bounds fill / clipped stores)
+  if (dtype != LA_F32 || d < 32 || d > D || d % 32 != 0) return false;
   for (int x = 0; x < 3 * count; ++x)
     if ((strides[x] * 4) % 16 != 0) return false;
   return true;
@@ -654,6 +658,7 @@ cudaError_t tc32_launch(const PassDesc& p, bool state_only, cudaStream_t st) {
   std::memset(&a, 0, sizeof(a));
   a.heads = p.heads;
   a.n = p.n;
+  a.d = p.d;
   a.seg_len = p.seg_len;
   a.nseg = p.nseg;
   a.rev = p.rev;

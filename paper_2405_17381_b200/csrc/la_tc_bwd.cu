@@ -95,6 +95,7 @@ struct Bars {
 
 struct BwdArgs {
   int heads, n, seg_len, nseg;
+  int d;  // head dim (64 or 128): features past d are zero (TMA out-of-bounds fill), states are d x d
   const double* lam;
   const float* state_in;  // entering adjoint state (dkv orientation), nullable
   int64_t in_bh_stride, in_seg_stride;
@@ -557,9 +558,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       for (int q4 = 0; q4 < 4; ++q4) {
         float x[16];
         if (from_global) {
-          if (args.state_in != nullptr) {
+          if (args.state_in != nullptr && i < args.d && hh * 64 + q4 * 16 < args.d) {
             const float* src = args.state_in + (int64_t)bh * args.in_bh_stride + (int64_t)seg * args.in_seg_stride +
-                               (int64_t)i * D + hh * 64 + q4 * 16;
+                               (int64_t)i * args.d + hh * 64 + q4 * 16;
             const float4* s4 = reinterpret_cast<const float4*>(src);  // 16-byte aligned state rows
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
@@ -675,15 +676,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (t + 1 < nchunks) load_x(t + 1);  // in flight while the next chunk's products run
       }
     }
-    if (nchunks > 0 && args.state_out != nullptr && seg == 0) {
-      float* dst = args.state_out + (int64_t)bh * D * D + (int64_t)i * D + hh * 64;
+    if (nchunks > 0 && args.state_out != nullptr && seg == 0 && i < args.d && hh * 64 < args.d) {
+      float* dst = args.state_out + (int64_t)bh * args.d * args.d + (int64_t)i * args.d + hh * 64;
 #pragma unroll 1
       for (int q4 = 0; q4 < 4; ++q4) {
         float x[16];
         tmem_ld16(st_cols + q4 * 16, x);
         tmem_ld_wait();
+        if (hh * 64 + q4 * 16 < args.d) {
 #pragma unroll
-        for (int j = 0; j < 16; ++j) dst[q4 * 16 + j] = x[j];
+          for (int j = 0; j < 16; ++j) dst[q4 * 16 + j] = x[j];
+        }
       }
     }
   }
@@ -712,6 +715,7 @@ cudaError_t tc_dkdv_launch(const PassDesc& p, const void* q, const void* k, cons
   std::memset(&a, 0, sizeof(a));
   a.heads = p.heads;
   a.n = p.n;
+  a.d = p.d;
   a.seg_len = p.seg_len;
   a.nseg = p.nseg;
   a.lam = p.lam;

@@ -99,8 +99,8 @@ def _prep(tensors: Sequence[torch.Tensor], names: str, layout: str):
 
     Each operand keeps its own strides (la_tensor_strides): a view with a unit feature stride is
     passed as is.  A copy is made only when the kernels cannot address the view -- a feature
-    stride != 1, or, for bf16 / fp32 d = 128 operands (the tensor-core paths), a base or stride that is no
-    multiple of 16 bytes -- and then only of that operand."""
+    stride != 1, or, for bf16 / fp32 operands at d = 32, 64, 96 or 128 (the tensor-core paths), a
+    base or stride that is no multiple of 16 bytes -- and then only of that operand."""
     first = tensors[0]
     if not isinstance(first, torch.Tensor):
         raise ShapeError(f"{names[0]}: expected a torch.Tensor")
@@ -116,7 +116,7 @@ def _prep(tensors: Sequence[torch.Tensor], names: str, layout: str):
         if t.dtype != first.dtype or t.device != first.device:
             raise ShapeError(f"{name}: dtype/device {t.dtype}/{t.device} != {first.dtype}/{first.device}")
     g = _geometry(first, layout)
-    tc = first.dtype in (torch.bfloat16, torch.float32) and g.d == 128
+    tc = first.dtype in (torch.bfloat16, torch.float32) and g.d % 32 == 0 and g.d <= 128
     out = []
     for t in tensors:
         if t.dim() == 4 and t.stride(3) != 1 and t.shape[3] > 1:

@@ -221,7 +221,8 @@ def test_gla_core_entry_validation():
 
 def test_fp32_tensor_core_backend_selection():
     """fp32 at d = 128 with 16-byte strides is served by the tcgen05 split pass (its own plan: one wave of
-    segments for a long sequence, bounded workspace); fp32 at other head dims cannot be forced onto it."""
+    segments for a long sequence, bounded workspace); head dims that are not a multiple of 32 cannot be forced
+    onto the tensor cores."""
     lib = _lib.load()
     long32 = _desc(batch=1, heads=16, n=1 << 17, d=128, dtype=_lib.LA_F32, backend=_lib.LA_BACKEND_TCGEN05)
     assert lib.la_segment_count(ctypes.byref(long32)) == 148 // 16
@@ -230,6 +231,11 @@ def test_fp32_tensor_core_backend_selection():
     assert len(sizes) == 1 and sizes.pop() > 0
     # backward on the split pass: three passes (no fused dK/dV sweep in fp32)
     assert lib.la_launch_count(ctypes.byref(_desc(batch=64, heads=16, n=1024, d=128, dtype=_lib.LA_F32)), 1) == 3
-    assert _fwd(_desc(d=64, dtype=_lib.LA_F32, backend=_lib.LA_BACKEND_TCGEN05)) == _lib.LA_ERR_UNSUPPORTED
+    # head dims below 128 run on zero-padded features when they are a multiple of 32 (both dtypes)
+    for dt in (_lib.LA_F32, _lib.LA_BF16):
+        for d in (32, 64, 96):
+            assert lib.la_segment_count(ctypes.byref(_desc(d=d, dtype=dt, backend=_lib.LA_BACKEND_TCGEN05))) >= 1
+        for d in (16, 48):
+            assert _fwd(_desc(d=d, dtype=dt, backend=_lib.LA_BACKEND_TCGEN05)) == _lib.LA_ERR_UNSUPPORTED
     assert _fwd(_desc(d=128, dtype=_lib.LA_F32, backend=_lib.LA_BACKEND_TCGEN05, stride=(2 * 64 * 130, 64 * 130, 130))) \
         == _lib.LA_ERR_UNSUPPORTED  # a position stride of 130 floats is not 16-byte aligned

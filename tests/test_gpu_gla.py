@@ -6,7 +6,8 @@ proof.  bf16 (input, weights and every GEMM output rounded to bf16, fp32 accumul
 end-to-end rounding of five chained bf16 GEMMs around the core: 5e-2 on the output, 1.5e-1 on
 gradients (each passes through two more bf16-rounded GEMMs than the output); the LRPE angle
 gradient is not checked in bf16 -- it is a sum over positions of cancelling products of
-bf16-rounded values (positional.py:178-181), meaningful only from fp32 up.
+bf16-rounded values (positional.py:178-181), meaningful only from fp32 up; in fp32 it is held to 1e-4
+on the SIMT core and to 1e-2 on the tensor-core split pass (DTHETA_TOL_SPLIT).
 """
 
 from pathlib import Path
@@ -19,6 +20,10 @@ GOLD = Path(__file__).resolve().parent / "golden" / "gla_golden.npz"
 CASES = ["rot_swish_gate", "norot_swish_gate", "rot_elu_nogate", "norot_none_gate"]
 TOL = {torch.float64: 1e-9, torch.float32: 1e-4, torch.bfloat16: 5e-2}
 GRAD_TOL = {torch.float64: 1e-9, torch.float32: 1e-4, torch.bfloat16: 1.5e-1}
+# fp32 on the tensor-core split pass (la_tc32.cu: three bf16 products, ~2^-16 relative error per product):
+# y, dx and the weight gradients stay within 1e-4, but the angle gradient's cancelling sum over positions
+# amplifies the per-product error ~100x; the SIMT fp32 core (exact fp32 FMAs) is held to 1e-4 on it.
+DTHETA_TOL_SPLIT = 1e-2
 
 
 def _gold():
@@ -50,9 +55,10 @@ def _case(g, c, dtype, dev):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("dtype", [torch.float64, torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("dtype,backend", [(torch.float64, "auto"), (torch.float32, "auto"), (torch.float32, "simt"),
+                                           (torch.bfloat16, "auto")], ids=["f64", "f32", "f32-simt", "bf16"])
 @pytest.mark.parametrize("case", CASES)
-def test_gla_forward_backward_matches_reference(case, dtype):
+def test_gla_forward_backward_matches_reference(case, dtype, backend):
     from paper_2405_17381_b200.gla import gla_forward
     g = _gold()
     dev = torch.device("cuda", 0)
@@ -62,7 +68,7 @@ def test_gla_forward_backward_matches_reference(case, dtype):
     for p in params:
         p.requires_grad_(True)
     theta = cs["theta"].clone().requires_grad_(True) if cs["rotate"] else None
-    y = gla_forward(x, cs["w"], cs["lam"], cs["heads"], act=cs["act"], theta=theta)
+    y = gla_forward(x, cs["w"], cs["lam"], cs["heads"], act=cs["act"], theta=theta, backend=backend)
     dy = cs["t"](g[f"{case}.dy"])[None].repeat(2, 1, 1)
     y.backward(dy)
     tol = TOL[dtype]
@@ -74,7 +80,10 @@ def test_gla_forward_backward_matches_reference(case, dtype):
         errs[f"d{nm}"] = _scaled(p.grad.double().cpu() / 2, g[f"{case}.d{nm}"])
     if cs["rotate"] and dtype != torch.bfloat16:
         errs["dtheta"] = _scaled(theta.grad.double().cpu() / 2, g[f"{case}.dtheta"])
-    bad = {k: v for k, v in errs.items() if not v <= (tol if k == "y" else GRAD_TOL[dtype])}
+    lim = {k: tol if k == "y" else GRAD_TOL[dtype] for k in errs}
+    if dtype == torch.float32 and backend == "auto":
+        lim["dtheta"] = DTHETA_TOL_SPLIT  # the core runs on the fp32 split pass (d a multiple of 32)
+    bad = {k: v for k, v in errs.items() if not v <= lim[k]}
     assert not bad, f"{case} {dtype}: {errs}"
 
 

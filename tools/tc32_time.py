@@ -22,13 +22,14 @@ def time_it(fn, reps=5):
     return e0.elapsed_time(e1) / reps
 
 
-H = 16
-lams = [decay_rate(h + 1, 1, H, 16) for h in range(H)]
-for n, b in ((1024, 64), (8192, 8), (65536, 1)):
-    q, k, v, do = (torch.randn(b, H, n, 128, device="cuda") / 128 ** 0.5 for _ in range(4))
-    for backend in ("tcgen05", "simt"):
-        if backend == "simt" and n > 8192:
-            continue
-        f = time_it(lambda: ops.la_forward(q, k, v, lams, backend=backend))
-        g = time_it(lambda: ops.la_backward(q, k, v, do, lams, backend=backend), reps=3)
-        print(f"n={n} b={b} {backend}: fwd {f:.3f} ms bwd {g:.3f} ms  {b * n / (f + g) / 1e3:.2f}M tok/s", flush=True)
+if __name__ == "__main__":
+    H = 16
+    lams = [decay_rate(h + 1, 1, H, 16) for h in range(H)]
+    for n, b in ((1024, 64), (8192, 8), (65536, 1)):
+        q, k, v, do = (torch.randn(b, H, n, 128, device="cuda") / 128 ** 0.5 for _ in range(4))
+        for backend in ("tcgen05", "simt"):
+            if backend == "simt" and n > 8192:
+                continue
+            f = time_it(lambda: ops.la_forward(q, k, v, lams, backend=backend))
+            g = time_it(lambda: ops.la_backward(q, k, v, do, lams, backend=backend), reps=3)
+            print(f"n={n} b={b} {backend}: fwd {f:.3f} ms bwd {g:.3f} ms  {b * n / (f + g) / 1e3:.2f}M tok/s", flush=True)
