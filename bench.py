@@ -478,18 +478,21 @@ def measure_rows(ops, device, stream, pk) -> dict:
         fp32_rows[be] = {"ms_fwd_bwd": round(t32, 3), "tokens_per_s": round(8 * 8192 / (t32 / 1e3)), "path": path}
     out["fp32_tnl1b_8k"] = {"shape": [8, H, 8192, D], **fp32_rows}
     del q32, k32, v32, d32
-    # BASELINE configs[0] (the reference's CPU-runnable parity case): batch 1, H 4, n 1024, d 64, fp32 on
-    # the precision (SIMT) path, lam (1, 0.99, 0.9, 0.5); latency-bound (4 sequences), so no roofline
+    # BASELINE configs[0] (the reference's CPU-runnable parity case): batch 1, H 4, n 1024, d 64, fp32,
+    # lam (1, 0.99, 0.9, 0.5); the default route is the tensor-core split pass on zero-padded d = 128
+    # tiles, the SIMT pass timed beside it; latency-bound (4 sequences), so no roofline
     c1 = [torch.randn(1, 4, 1024, 64, device=device, generator=g) * 0.5 for _ in range(4)]
     lam1 = ops.decay_tensor([1.0, 0.99, 0.9, 0.5], 4, device)
+    c1_rows = {}
+    for be, path in (("tcgen05", "tcgen05 fp32 (3-term bf16 split, default route)"),
+                     ("simt", "simt fp32 (FFMA)")):
+        def fb1(be=be):
+            ops.la_forward(*c1[:3], None, lam_dev=lam1, backend=be)
+            ops.la_backward(*c1, None, lam_dev=lam1, backend=be)
 
-    def fb1():
-        ops.la_forward(*c1[:3], None, lam_dev=lam1)
-        ops.la_backward(*c1, None, lam_dev=lam1)
-
-    t1 = _time_ms(fb1, stream)
-    out["config1_fp32"] = {"shape": [1, 4, 1024, 64], "ms_fwd_bwd": round(t1, 4),
-                           "tokens_per_s": round(1024 / (t1 / 1e3)), "path": "simt fp32 (1e-4 parity path)"}
+        t1 = _time_ms(fb1, stream)
+        c1_rows[be] = {"ms_fwd_bwd": round(t1, 4), "tokens_per_s": round(1024 / (t1 / 1e3)), "path": path}
+    out["config1_fp32"] = {"shape": [1, 4, 1024, 64], **c1_rows}
     # the whole GLA layer, fwd + bwd through autograd
     x = rnd(b, n, w).requires_grad_(True)
     ws = gla.GlaWeights(*(rnd(w, w).mul_(w ** -0.5 * 2).requires_grad_(True) for _ in range(5)))
