@@ -49,5 +49,17 @@ for b, n, h in ((6, 300, 16), (1, 1000, 4)):
     lam = [0.9, 0.99, 0.5, 1.0] * (h // 4)
     o, q, k = ops.gla_core_forward(qp, kp, v, lam, h, theta=theta, offset=3)
     ops.gla_core_backward(qp, kp, q, k, v, da, lam, h, theta=theta, offset=3)
+# round 2c: head dims below 128 on the tensor-core passes (TMA zero fill past d, d x d state masks), with
+# entering / exiting states, split sequences and the state-only passes
+for dtype in (torch.bfloat16, torch.float32):
+    for d in (32, 64, 96):
+        q, k, v, do = (torch.rand(1, 2, 1000, d, device="cuda", dtype=dtype) for _ in range(4))
+        kv, dkv = (torch.rand(1, 2, d, d, device="cuda") for _ in range(2))
+        (o, kvo), seg = ops.la_forward(q, k, v, [0.9, 0.99], backend="tcgen05", segments=3, kv_in=kv,
+                                       want_state=True, want_seg_states=True)
+        ops.la_backward(q, k, v, do, [0.9, 0.99], backend="tcgen05", segments=3, kv_in=kv, dkv_in=dkv,
+                        want_state=True, fwd_seg_states=seg)
+        ops.la_forward_state(k, v, [0.9, 0.99], backend="tcgen05", segments=3)
+        ops.la_backward_state(q, do, [0.9, 0.99], backend="tcgen05", segments=3)
 torch.cuda.synchronize()
 print("ok")
