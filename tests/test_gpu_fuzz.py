@@ -24,7 +24,7 @@ N_CASES = int(os.environ.get("LA_FUZZ_CASES", "48"))
 def _case(i):
     rng = np.random.default_rng(9000 + i)
     dtype = [torch.bfloat16, torch.bfloat16, torch.float32, torch.float64][rng.integers(4)]
-    d = 128 if dtype == torch.bfloat16 and rng.random() < 0.8 else int(rng.choice([1, 4, 16, 40, 64, 128]))
+    d = 128 if dtype == torch.bfloat16 and rng.random() < 0.8 else int(rng.choice([1, 4, 16, 32, 40, 64, 96, 128]))
     if dtype == torch.float64:
         d = min(d, 64)
     b, h = int(rng.integers(1, 4)), int(rng.integers(1, 5))
