@@ -1,39 +1,40 @@
-"""PCIe copy bandwidth from pinned host memory: H2D on 1 vs 2 streams, and H2D + D2H together."""
-import time
+"""Pinned-host <-> device copy bandwidth on this box: H2D alone, D2H alone, both at once (GB/s)."""
 import torch
 
-dev = torch.device("cuda", 0)
-MB = 1 << 20
-n = 256 * MB // 2
-hs = [torch.empty(n, dtype=torch.bfloat16, pin_memory=True) for _ in range(4)]
-ds = [torch.empty(n, dtype=torch.bfloat16, device=dev) for _ in range(4)]
-streams = [torch.cuda.Stream() for _ in range(4)]
+n = 1 << 30  # 1 GiB per buffer
+h_in = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+h_out = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+d_in = torch.empty(n, dtype=torch.uint8, device="cuda")
+d_out = torch.ones(n, dtype=torch.uint8, device="cuda")
+s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
 
 
-def run(pairs, reps=5):
+def run(h2d, d2h, reps=5):
     for _ in range(2):
-        for fn, s in pairs:
-            with torch.cuda.stream(s):
-                fn()
+        if h2d:
+            with torch.cuda.stream(s1):
+                d_in.copy_(h_in, non_blocking=True)
+        if d2h:
+            with torch.cuda.stream(s2):
+                h_out.copy_(d_out, non_blocking=True)
     torch.cuda.synchronize()
-    t0 = time.perf_counter()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    s1.wait_stream(torch.cuda.current_stream())
+    s2.wait_stream(torch.cuda.current_stream())
     for _ in range(reps):
-        for fn, s in pairs:
-            with torch.cuda.stream(s):
-                fn()
+        if h2d:
+            with torch.cuda.stream(s1):
+                d_in.copy_(h_in, non_blocking=True)
+        if d2h:
+            with torch.cuda.stream(s2):
+                h_out.copy_(d_out, non_blocking=True)
+    torch.cuda.current_stream().wait_stream(s1)
+    torch.cuda.current_stream().wait_stream(s2)
+    b.record()
     torch.cuda.synchronize()
-    return (time.perf_counter() - t0) / reps
+    return reps * n / (a.elapsed_time(b) / 1e3) / 1e9
 
 
-h2d = lambda i: (lambda: ds[i].copy_(hs[i], non_blocking=True))  # noqa: E731
-d2h = lambda i: (lambda: hs[i].copy_(ds[i], non_blocking=True))  # noqa: E731
-t = run([(h2d(0), streams[0]), (h2d(1), streams[0])])
-print(f"H2D 1 stream : {2 * 256 / 1024 / t:.1f} GB/s")
-t = run([(h2d(0), streams[0]), (h2d(1), streams[1])])
-print(f"H2D 2 streams: {2 * 256 / 1024 / t:.1f} GB/s")
-t = run([(d2h(2), streams[2]), (d2h(3), streams[2])])
-print(f"D2H 1 stream : {2 * 256 / 1024 / t:.1f} GB/s")
-t = run([(h2d(0), streams[0]), (h2d(1), streams[0]), (d2h(2), streams[2]), (d2h(3), streams[2])])
-print(f"H2D+D2H      : {2 * 256 / 1024 / t:.1f} GB/s each way")
-t = run([(h2d(0), streams[0]), (h2d(1), streams[1]), (d2h(2), streams[2]), (d2h(3), streams[3])])
-print(f"H2D+D2H x2   : {2 * 256 / 1024 / t:.1f} GB/s each way")
+print(f"H2D alone {run(True, False):.1f} GB/s, D2H alone {run(False, True):.1f} GB/s, "
+      f"both at once {run(True, True):.1f} GB/s per direction")
