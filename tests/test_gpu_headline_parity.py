@@ -10,6 +10,7 @@ kernels.py:253-334, fp64, on the bf16-rounded operands the device saw).
 * The same long shapes with long-memory decays (lam = 1, 0.99995, 0.999): the bench's decays forget
   within a few positions, so these exercise the carried state and the segment summaries across
   the whole 128K sequence.
+* BASELINE configs[4]'s length (2^20 positions, one sequence) on one GPU, with no decay on one head.
 * The bf16 GLA layer at d_model = 2048 (16 heads x 128, the tensor-core core) against a torch fp64
   restatement of the reference layer (model.py:365-453, positional.py:126-182) with autograd
   gradients.
@@ -114,6 +115,22 @@ def test_long_memory_decays_at_full_length(n):
     outs = _bench_step(*tensors, lam_dev)[:4]
     _check_units(tensors, outs, lams, [(0, 0), (b - 1, 5), (0, 11)], orc.max_rel_error, TOL_BF16,
                  f"long-memory n={n}")
+
+
+def test_config5_million_token_sequence():
+    """BASELINE configs[4]'s length on one GPU: TNL-1B heads (H = 16, d = 128, bf16), ONE sequence of
+    2^20 positions (the auto plan splits it into one wave of segments: summaries -> scan -> pass, and the
+    backward's adjoint chain), with no decay on head 0 (the state sums all 2^20 positions) and
+    lam = 0.99995 on head 1; checked on those two heads and the strongest decay (head 15)."""
+    H, n = 16, 1 << 20
+    lams = [decay_rate(h, 1, H, 16) for h in range(1, H + 1)]
+    lams[0], lams[1] = 1.0, 0.99995
+    lam_dev = ops.decay_tensor(lams, H, DEV)
+    tensors = _inputs(1, H, n, "pos", seed=20)
+    outs = _bench_step(*tensors, lam_dev)[:4]
+    torch.cuda.synchronize()
+    assert ops.segment_count(ops._desc(ops._geometry(tensors[0], "bhnd"), torch.bfloat16, None, "auto", 0)) > 1
+    _check_units(tensors, outs, lams, [(0, 0), (0, 1), (0, H - 1)], orc.max_rel_error, TOL_BF16, "1M tokens")
 
 
 # ----------------------------------------------------------------------------------------------
