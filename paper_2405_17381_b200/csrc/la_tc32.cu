@@ -26,8 +26,9 @@
 //   out  TMEM O -> fp32 rows staged in C's region -> TMA store
 //
 // SMEM: 3 x 64 KB operand regions + 32 KB state half = 224 KB.  TMEM: S | A~ | O | state = 512 columns.
-// Overlap: the state is published while S runs (C is split last: its refill waits for the previous output's
-// store); the next chunk's A is split while the state update, X_1 and Y run.  The A region is refilled as soon as S has read it,
+// Overlap: the state is published while S runs; B~ and C's split come right after S so the state update
+// (B's last reader) runs while the scores are converted and B's refill for the next chunk is issued early;
+// the next chunk's A is split while X_1 and Y run.  The A region is refilled as soon as S has read it,
 // B after the state update, C once the output rows staged in it are stored.  State-only mode (segment summaries, la_api.cu segment_states) runs B~ and
 // U only.
 #include <cudaTypedefs.h>
@@ -84,7 +85,7 @@ struct Bars {
   uint64_t u1_done;   // MMA: the state update done (the last reader of B)
   uint64_t x1_done;   // MMA: X_1 done (A~'s last reader)
   uint64_t all_done;  // MMA: every product of the chunk done
-  uint64_t go_s, go_x0, go_x1;  // workers -> issuer: operands of S / of X_0, U_0 / of X_1, U_1, Y ready
+  uint64_t go_s, go_u, go_x0, go_x1;  // workers -> issuer: operands of S / of U / of X_0 / of X_1, Y ready
   uint64_t o_staged;            // workers -> issuer: O(t) staged in C's region for the TMA store
   uint32_t tmem_base;
 };
@@ -174,6 +175,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     mbar_init(&bars.x1_done, 1);
     mbar_init(&bars.all_done, 1);
     mbar_init(&bars.go_s, NUM_WORKERS);
+    mbar_init(&bars.go_u, NUM_WORKERS);
     mbar_init(&bars.go_x0, NUM_WORKERS);
     mbar_init(&bars.go_x1, NUM_WORKERS);
     mbar_init(&bars.o_staged, NUM_WORKERS);
@@ -287,12 +289,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
       }
       mma_commit(&bars.s_done);
-      // X_0 = A~ state[:, 0:64], the state update (B's last reader)
-      go(&bars.go_x0, t);  // P, B~, C, the first state half's copy, the state pre-scaled; O(t-1) drained
-      issue_x(0);
-      mma_commit(&bars.x0_done);
+      // the state update first (B's last reader: B's refill for the next chunk starts as early as possible;
+      // X reads the SMEM copy of the state taken before it, so the TMEM update does not disturb X)
+      go(&bars.go_u, t);  // B~, C split; the TMEM state pre-scaled
       issue_u();
       mma_commit(&bars.u1_done);
+      // X_0 = A~ state[:, 0:64]
+      go(&bars.go_x0, t);  // P, the first state half's copy; O(t-1) drained
+      issue_x(0);
+      mma_commit(&bars.x0_done);
       // X_1 (A~'s last reader), Y = P C
       go(&bars.go_x1, t);  // the second state half's copy in SMEM
       issue_x(1);
@@ -457,6 +462,24 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       take_state(t);  // while S runs
       await(&bars.s_done, t);
       T32(t, 4);
+      // B~ = in_scale * B, in place (S has read B)
+      {
+        const uint32_t hb = B_HI + (uint32_t)(hh * HALF), lb = B_LO + (uint32_t)(hh * HALF);
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const uint4 xh = lds128(hb + sw128(i, c)), xl = lds128(lb + sw128(i, c));
+          const uint32_t hs[4] = {xh.x, xh.y, xh.z, xh.w}, ls[4] = {xl.x, xl.y, xl.z, xl.w};
+          uint32_t ho[4], lo[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            split2(isc * (bf16lo(hs[e]) + bf16lo(ls[e])), isc * (bf16hi(hs[e]) + bf16hi(ls[e])), ho[e], lo[e]);
+          sts128(hb + sw128(i, c), make_uint4(ho[0], ho[1], ho[2], ho[3]));
+          sts128(lb + sw128(i, c), make_uint4(lo[0], lo[1], lo[2], lo[3]));
+        }
+      }
+      split_region(R_C, 2, t, 1.f);
+      signal(&bars.go_u);  // B~, C: the state update may run while the scores are converted
+      T32(t, 2);
       // P = S * M, split in place: per 32-key block, a zero block (causality), an off-diagonal block
       // (lam^|i-j| = per-row base x a broadcast ladder), or the diagonal block
 #pragma unroll 1
@@ -500,22 +523,6 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         tmem_st16(tmem + lane_off + TM_S + 32 * cb, hw);
         tmem_st16(tmem + lane_off + TM_S + 32 * cb + 16, lw);
       }
-      // B~ = in_scale * B, in place (S has read B)
-      {
-        const uint32_t hb = B_HI + (uint32_t)(hh * HALF), lb = B_LO + (uint32_t)(hh * HALF);
-#pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          const uint4 xh = lds128(hb + sw128(i, c)), xl = lds128(lb + sw128(i, c));
-          const uint32_t hs[4] = {xh.x, xh.y, xh.z, xh.w}, ls[4] = {xl.x, xl.y, xl.z, xl.w};
-          uint32_t ho[4], lo[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e)
-            split2(isc * (bf16lo(hs[e]) + bf16lo(ls[e])), isc * (bf16hi(hs[e]) + bf16hi(ls[e])), ho[e], lo[e]);
-          sts128(hb + sw128(i, c), make_uint4(ho[0], ho[1], ho[2], ho[3]));
-          sts128(lb + sw128(i, c), make_uint4(lo[0], lo[1], lo[2], lo[3]));
-        }
-      }
-      split_region(R_C, 2, t, 1.f);  // C last: its load (after the previous output's store) had the most time
       T32(t, 5);
       signal(&bars.go_x0);
       await(&bars.x0_done, t);
