@@ -22,7 +22,7 @@
 //        32 KB left; half 1's copy waits in registers until X_0 read half 0's)
 //                                                3 x 8 TS-MMAs each (M = 128, N = 64)
 //   U    state = lam^b state + B~^T C           TMEM state pre-scaled by the workers; 3 x 8 SS-MMAs (N = 128)
-//   Y    O += P C                                3 x 8 TS-MMAs (M = N = 128)
+//   Y    O = P C (issued before X_0 / X_1, which accumulate onto it)   3 x 8 TS-MMAs (M = N = 128)
 //   out  TMEM O -> fp32 rows staged in C's region -> TMA store
 //
 // SMEM: 3 x 64 KB operand regions + 32 KB state half = 224 KB.  TMEM: S | A~ | O | state = 512 columns.
@@ -249,14 +249,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       mbar_wait(bar, t & 1);
       tc_fence_after();
     };
-    auto issue_x = [&](int h) {  // O[:, h] = A~ state[:, h]
+    auto issue_x = [&](int h) {  // O[:, h] += A~ state[:, h]  (Y initialised O)
 #pragma unroll 1
       for (int g = 0; g < 3; ++g) {
         const uint32_t at = TM_AT + (g == 2 ? 64 : 0), st = g == 1 ? ST_LO : ST_HI;
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk)
           mma_bf16_ts(tmem + TM_O + 64 * h, tmem + at + kk * 8, smem_desc_sw128(st + kk * 2048, HALF, 1024),
-                      IDESC_X, (g | kk) != 0);
+                      IDESC_X, 1);
       }
     };
     auto issue_u = [&]() {  // state += B~^T C, both halves
@@ -294,23 +294,24 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       go(&bars.go_u, t);  // B~, C split; the TMEM state pre-scaled
       issue_u();
       mma_commit(&bars.u1_done);
-      // X_0 = A~ state[:, 0:64]
+      // Y = P C first (it initialises O; both X halves accumulate onto it), then X_0 = A~ state[:, 0:64]
       go(&bars.go_x0, t);  // P, the first state half's copy; O(t-1) drained
-      issue_x(0);
-      mma_commit(&bars.x0_done);
-      // X_1 (A~'s last reader), Y = P C
-      go(&bars.go_x1, t);  // the second state half's copy in SMEM
-      issue_x(1);
-      mma_commit(&bars.x1_done);
 #pragma unroll 1
       for (int g = 0; g < 3; ++g) {
         const uint32_t pofs = g == 2 ? 16 : 0, c = g == 1 ? C_LO : C_HI;
 #pragma unroll
         for (int kk = 0; kk < C / 16; ++kk) {
           const uint32_t pcol = 32 * (kk >> 1) + pofs + 8 * (kk & 1);
-          mma_bf16_ts(tmem + TM_O, tmem + TM_S + pcol, smem_desc_sw128(c + kk * 2048, HALF, 1024), IDESC_Y, 1);
+          mma_bf16_ts(tmem + TM_O, tmem + TM_S + pcol, smem_desc_sw128(c + kk * 2048, HALF, 1024), IDESC_Y,
+                      (g | kk) != 0);
         }
       }
+      issue_x(0);
+      mma_commit(&bars.x0_done);
+      // X_1 (A~'s last reader, the chunk's last product)
+      go(&bars.go_x1, t);  // the second state half's copy in SMEM
+      issue_x(1);
+      mma_commit(&bars.x1_done);
       mma_commit(&bars.all_done);
     }
     // drain: every commit must land before the CTA retires
