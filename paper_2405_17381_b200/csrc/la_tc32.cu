@@ -478,6 +478,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           sts128(lb + sw128(i, c), make_uint4(lo[0], lo[1], lo[2], lo[3]));
         }
       }
+      T32(t, 3);
       split_region(R_C, 2, t, 1.f);
       signal(&bars.go_u);  // B~, C: the state update may run while the scores are converted
       T32(t, 2);

@@ -5,7 +5,7 @@ import numpy as np, torch
 sys.path.insert(0, '.')
 from paper_2405_17381_b200 import ops, _lib
 lib = _lib.load()
-names = ["start", "go_s", "go_u(B~C)", "-", "S_done", "go_x0(P)", "Y+X0_done", "pub1", "A_next", "X1_done", "all_done",
+names = ["start", "go_s", "go_u(B~C)", "B~done", "S_done", "go_x0(P)", "Y+X0_done", "pub1", "A_next", "X1_done", "all_done",
          "O_staged"]
 b, n = 8, 8192
 q, k, v = (torch.randn(b, 16, n, 128, device="cuda") / 128 ** 0.5 for _ in range(3))
