@@ -3,7 +3,7 @@
  *
  * Shows that the drop-in boundary needs nothing but C: the CUDA runtime for device memory and the
  * library's extern "C" entry points (no torch, no Python).  It runs la_fwd / la_bwd on one small problem
- * per dtype (fp32 on the tensor cores at d = 64, fp64 on the SIMT path at d = 40) with an entering state,
+ * per dtype (bf16 and fp32 on the tensor cores at d = 128 / 64, fp64 on the SIMT path at d = 40) with entering states,
  * and checks every output against a direct O(n^2 d) restatement in double of the reference's definitions
  * (kernels.py:253-334 as SPEC'd in the header: o[t] = sum_{s<=t} lam^(t-s) (q[t].k[s]) v[s], and its
  * gradients), plus the error contract (a bad descriptor -> LA_ERR_DOMAIN with a message).
@@ -26,6 +26,20 @@ extern cudaError_t cudaFree(void* p);
 extern cudaError_t cudaMemcpy(void* dst, const void* src, size_t bytes, int kind);
 extern cudaError_t cudaDeviceSynchronize(void);
 enum { H2D = 1, D2H = 2 };
+
+/* bf16 <-> float (round to nearest even) for the bf16 problem */
+static unsigned short to_bf16(float x) {
+  unsigned int u;
+  memcpy(&u, &x, 4);
+  u += 0x7FFFu + ((u >> 16) & 1u);
+  return (unsigned short)(u >> 16);
+}
+static double from_bf16(unsigned short h) {
+  unsigned int u = (unsigned int)h << 16;
+  float x;
+  memcpy(&x, &u, 4);
+  return x;
+}
 
 static double urand(unsigned long long* s) {
   *s = *s * 6364136223846793005ULL + 1442695040888963407ULL;
@@ -103,7 +117,7 @@ static double max_rel(const double* got, const double* want, size_t count) {
 
 /* one problem: B = 1, H heads (lam per head), n, d, dtype; tolerance `tol` (per-entry relative) */
 static void run(int dtype, int H, int n, int d, const double* lams, double tol, const char* label) {
-  const size_t esz = dtype == LA_F64 ? 8 : 4, ssz = dtype == LA_F64 ? 8 : 4;
+  const size_t esz = dtype == LA_F64 ? 8 : dtype == LA_BF16 ? 2 : 4, ssz = dtype == LA_F64 ? 8 : 4;
   const size_t cnt = (size_t)H * n * d, scnt = (size_t)H * d * d;
   unsigned long long seed = 12345 + (unsigned long long)dtype;
   double* hx[4];
@@ -112,12 +126,14 @@ static void run(int dtype, int H, int n, int d, const double* lams, double tol, 
     for (size_t i = 0; i < cnt; ++i) hx[x][i] = urand(&seed);
     if (dtype == LA_F32)
       for (size_t i = 0; i < cnt; ++i) hx[x][i] = (double)(float)hx[x][i];
+    if (dtype == LA_BF16)  /* the reference sees exactly the operands the device sees */
+      for (size_t i = 0; i < cnt; ++i) hx[x][i] = from_bf16(to_bf16((float)hx[x][i]));
   }
   double* hs[2];
   for (int x = 0; x < 2; ++x) {
     hs[x] = malloc(scnt * sizeof(double));
     for (size_t i = 0; i < scnt; ++i) hs[x][i] = 0.02 * urand(&seed);
-    if (dtype == LA_F32)
+    if (dtype != LA_F64)
       for (size_t i = 0; i < scnt; ++i) hs[x][i] = (double)(float)hs[x][i];
   }
   /* device copies in the call's dtype */
@@ -126,6 +142,7 @@ static void run(int dtype, int H, int n, int d, const double* lams, double tol, 
   for (int x = 0; x < 4; ++x) {
     for (size_t i = 0; i < cnt; ++i) {
       if (dtype == LA_F64) ((double*)buf)[i] = hx[x][i];
+      else if (dtype == LA_BF16) ((unsigned short*)buf)[i] = to_bf16((float)hx[x][i]);
       else ((float*)buf)[i] = (float)hx[x][i];
     }
     CHECK(cudaMalloc(&dx[x], cnt * esz));
@@ -170,7 +187,8 @@ static void run(int dtype, int H, int n, int d, const double* lams, double tol, 
   for (int x = 0; x < 6; ++x) {
     const size_t c = x < 4 ? cnt : scnt, sz = x < 4 ? esz : ssz;
     CHECK(cudaMemcpy(buf, have[x], c * sz, D2H));
-    for (size_t i = 0; i < c; ++i) got[i] = sz == 8 ? ((double*)buf)[i] : (double)((float*)buf)[i];
+    for (size_t i = 0; i < c; ++i)
+      got[i] = sz == 8 ? ((double*)buf)[i] : sz == 2 ? from_bf16(((unsigned short*)buf)[i]) : (double)((float*)buf)[i];
     const double e = max_rel(got, want[x], c);
     printf("%s %-8s max rel err %.3e (tol %g)\n", label, names[x], e, tol);
     if (!(e <= tol)) {
@@ -201,6 +219,7 @@ int main(void) {
     return 1;
   }
   const double lams[3] = {1.0, 0.99, 0.5};
+  run(LA_BF16, 3, 300, 128, lams, 2e-2, "bf16 (tcgen05, d = 128)");
   run(LA_F32, 3, 300, 64, lams, 1e-4, "fp32 (tcgen05 split pass, d = 64)");
   run(LA_F64, 3, 200, 40, lams, 1e-10, "fp64 (SIMT, d = 40)");
   printf("abi_caller ok (%s)\n", la_build_info());
