@@ -429,6 +429,17 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       convert_a(0, th, tl);
       store_at(th, tl);
     }
+    // O columns [64 h + 32 hh, +32) of row i -> fp32 TMA-store box 2 h + hh of C's region
+    auto stage_o_box = [&](int h) {
+      float y[32];
+      tmem_ld32(tmem + lane_off + TM_O + 64 * h + 32 * hh, y);
+      tmem_ld_wait();
+      const uint32_t box = smem + R_C + (uint32_t)((2 * h + hh) * BOX) + (uint32_t)(i * 128);
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        sts128(box + ((c ^ (i & 7)) << 4), make_uint4(__float_as_uint(y[4 * c]), __float_as_uint(y[4 * c + 1]),
+                                                       __float_as_uint(y[4 * c + 2]), __float_as_uint(y[4 * c + 3])));
+    };
     const int quad = warp & 3;
     const uint32_t pw_addr = smem_u32(pw);
     for (int t = 0; t < nchunks; ++t) {
@@ -532,6 +543,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       publish(h1w, h1l);
       signal(&bars.go_x1);
       T32(t, 7);
+      // out(t), value half 0: final once X_0 is done (Y, issued before it, and the state update were C's
+      // readers), so it is staged in C's region now, box `hh` per thread; half 1 after X_1 below.  The
+      // workers' barrier orders the staging after every worker's C split in the CTA's own order too.
+      wbar();
+      stage_o_box(0);
       // while the state update, X_1 and Y run: the next chunk's A (its SMEM tiles are free since S), its A~
       // once X_1 has read A~
       if (t + 1 < nchunks) {
@@ -542,23 +558,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         T32(t, 9);
         store_at(th, tl);
       }
-      // out(t): O -> fp32 rows staged in C's region (TMA-store layout), stored by the TMA lane.  The staging
-      // overwrites C's split, written by other workers: the tensor core has read it (all_done), and the
-      // workers' barrier orders those writes before these in the CTA's own (generic-proxy) order too
+      // out(t), value half 1 (final after X_1), then the TMA lane stores the staged rows
       await(&bars.all_done, t);
-      wbar();
       T32(t, 10);
-#pragma unroll 1
-      for (int part = 0; part < 2; ++part) {
-        float y[32];
-        tmem_ld32(tmem + lane_off + TM_O + 64 * hh + 32 * part, y);
-        tmem_ld_wait();
-        const uint32_t box = smem + R_C + (uint32_t)((2 * hh + part) * BOX) + (uint32_t)(i * 128);
-#pragma unroll
-        for (int c = 0; c < 8; ++c)
-          sts128(box + ((c ^ (i & 7)) << 4), make_uint4(__float_as_uint(y[4 * c]), __float_as_uint(y[4 * c + 1]),
-                                                         __float_as_uint(y[4 * c + 2]), __float_as_uint(y[4 * c + 3])));
-      }
+      stage_o_box(1);
       signal(&bars.o_staged);
       T32(t, 11);
     }
