@@ -372,6 +372,21 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       wbar();  // every worker has read the fp32 region
       write_split(smem + region, i, hh, h, l);
     };
+    // B of chunk t: SMEM hi / lo tiles for S; B~ = in_scale B's words kept in registers (bt_h / bt_l) and
+    // written over B's tiles once S has read them -- no second pass over B in shared memory
+    auto split_b = [&](int t, float isc, uint32_t (&bth)[32], uint32_t (&btl)[32]) {
+      mbar_wait(&bars.full[1], t & 1);
+      float v[64];
+      read_f32_row(smem + R_B, i, hh, v);
+      uint32_t h[32], l[32];
+#pragma unroll
+      for (int q = 0; q < 32; ++q) {
+        split2(v[2 * q], v[2 * q + 1], h[q], l[q]);
+        split2(isc * v[2 * q], isc * v[2 * q + 1], bth[q], btl[q]);
+      }
+      wbar();  // every worker has read the fp32 region
+      write_split(smem + R_B, i, hh, h, l);
+    };
     // A of chunk t: SMEM hi / lo tiles; A~ = out_scale A's words returned for TMEM
     auto convert_a = [&](int t, uint32_t (&th)[32], uint32_t (&tl)[32]) {
       const int b = chunk_len(t);
@@ -468,27 +483,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         await(&bars.all_done, t);
         continue;
       }
-      split_region(R_B, 1, t, 1.f);
+      uint32_t bth[32], btl[32];
+      split_b(t, isc, bth, btl);
       signal(&bars.go_s);  // A(t), A~(t), B(t)
       T32(t, 1);
       take_state(t);  // while S runs
       await(&bars.s_done, t);
       T32(t, 4);
-      // B~ = in_scale * B, in place (S has read B)
-      {
-        const uint32_t hb = B_HI + (uint32_t)(hh * HALF), lb = B_LO + (uint32_t)(hh * HALF);
-#pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          const uint4 xh = lds128(hb + sw128(i, c)), xl = lds128(lb + sw128(i, c));
-          const uint32_t hs[4] = {xh.x, xh.y, xh.z, xh.w}, ls[4] = {xl.x, xl.y, xl.z, xl.w};
-          uint32_t ho[4], lo[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e)
-            split2(isc * (bf16lo(hs[e]) + bf16lo(ls[e])), isc * (bf16hi(hs[e]) + bf16hi(ls[e])), ho[e], lo[e]);
-          sts128(hb + sw128(i, c), make_uint4(ho[0], ho[1], ho[2], ho[3]));
-          sts128(lb + sw128(i, c), make_uint4(lo[0], lo[1], lo[2], lo[3]));
-        }
-      }
+      // B~ = in_scale * B over B's tiles (S has read them), from the words kept since B's split
+      write_split(smem + R_B, i, hh, bth, btl);
       T32(t, 3);
       split_region(R_C, 2, t, 1.f);
       signal(&bars.go_u);  // B~, C: the state update may run while the scores are converted
